@@ -1,0 +1,152 @@
+/*
+ * droidspeak.h — C ABI of the B200-native DroidSpeak cross-model prefill path.
+ *
+ * Plain C: device/host pointers, sizes and cudaStream_t passed as void*.  No
+ * torch types.  Every entry point validates all arguments before its first
+ * kernel launch (an error never leaves a half-written cache), returns a
+ * ds_status, and records a message retrievable with ds_last_error()
+ * (thread-local).  Nothing allocates device memory: callers pass workspace.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/crosskv/...).  INTEGRATION.md shows the ctypes
+ * binding a crosskv maintainer would add.
+ */
+#ifndef DROIDSPEAK_H
+#define DROIDSPEAK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DS_API __attribute__((visibility("default")))
+#else
+#define DS_API
+#endif
+#define DS_PAGE_SIZE 64 /* tokens per KV page */
+
+/* Status codes -> Python exceptions (errors.py:6-27):
+ * DS_ERR_INVALID -> ValueError, DS_ERR_CACHE_MISS -> CacheMissError(layer, kind),
+ * DS_ERR_DEGENERATE -> DegenerateInputError, DS_ERR_CUDA -> RuntimeError. */
+enum ds_status { DS_OK = 0, DS_ERR_INVALID = 1, DS_ERR_CACHE_MISS = 2, DS_ERR_DEGENERATE = 3, DS_ERR_CUDA = 4 };
+enum ds_miss_kind { DS_MISS_NONE = 0, DS_MISS_KV = 1, DS_MISS_E = 2 };
+
+/* ModelConfig (model.py:70-124) minus the seed. */
+typedef struct ds_dims {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab_size, max_seq;
+} ds_dims;
+
+/* One layer's weights on device.  Matrices are the reference's [in,out]
+ * tensors (model.py:256-270) transposed once to K-major [out][in] bf16. */
+typedef struct ds_layer_weights {
+  const void* wqkv;    /* bf16 [(H+2*KVH)*D][d] = concat(wq, wk, wv)^T */
+  const void* wo;      /* bf16 [d][H*D]          = wo^T */
+  const void* w1;      /* bf16 [d_ff][d]         = w1^T */
+  const void* w2;      /* bf16 [d][d_ff]         = w2^T */
+  const float* g_attn; /* f32 [d] */
+  const float* g_mlp;  /* f32 [d] */
+} ds_layer_weights;
+
+/* ModelWeights (model.py:234-243) on device. */
+typedef struct ds_model {
+  ds_dims dims;
+  const void* embed;              /* bf16 [V][d] */
+  const void* unembed;            /* bf16 [V][d] = unembed^T */
+  const float* g_final;           /* f32 [d] */
+  const float* rope_cos;          /* f32 [max_seq][D/2] (angles in f64, model.py:475-479) */
+  const float* rope_sin;          /* f32 [max_seq][D/2] */
+  const ds_layer_weights* layers; /* HOST array [n_layers] */
+} ds_model;
+
+/* A K/V cache over layers.  Element offset of (layer, head, pos, j):
+ *   layer*layer_stride + head*head_stride + table[pos/64]*page_stride + (pos%64)*head_dim + j
+ * Dense export [L][KVH][n][D] (LayerKV, model.py:342-370):
+ *   layer_stride = KVH*n*D, head_stride = n*D, page_stride = 64*D, block_table = NULL.
+ * Consumer paged cache [L][pages][KVH][64][D]:
+ *   layer_stride = pages*KVH*64*D, head_stride = 64*D, page_stride = KVH*64*D. */
+typedef struct ds_kv_cache {
+  void* k;                    /* bf16 */
+  void* v;                    /* bf16 */
+  int64_t layer_stride, head_stride, page_stride;
+  const int32_t* block_table; /* device int32 [ceil(positions/64)] or NULL (identity) */
+  int32_t n_layers;           /* layers present */
+  int32_t positions;          /* positions present per layer */
+} ds_kv_cache;
+
+/* ECache (model.py:373-391): residual-stream input of `layer`, bf16 [positions][width]. */
+typedef struct ds_e_cache {
+  int32_t layer;
+  int32_t positions;
+  int32_t width;
+  const void* hidden;
+} ds_e_cache;
+
+DS_API int ds_abi_version(void);
+DS_API const char* ds_last_error(void);
+
+/* Bytes of device workspace ds_partial_prefill / ds_full_prefill need for n tokens. */
+DS_API size_t ds_workspace_size(const ds_dims* dims, int32_t n_tokens);
+
+/* KV ingest — the reuse copy of _mixed_prefill (model.py:590-603):
+ * for l in reused[0..n_reused) (HOST array, ascending): dst[l, :, 0:window] = src[l, :, 0:window],
+ * bit-exact bf16, TMA bulk-copied 64-position page blocks.  Misses (src lacks
+ * layer l or window positions) are reported in ascending layer order. */
+DS_API int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const int32_t* reused, int32_t n_reused,
+                 int32_t window, int32_t n_kv_heads, int32_t head_dim, void* stream, int32_t* miss_layer);
+
+/* Consumer partial prefill — partial_prefill (model.py:660-679) / the paper's
+ * partial_prefill(recompute_config, context).
+ *   tokens_host   int64 [n] (validated here: check_tokens, model.py:425-437)
+ *   tokens_dev    optional device copy (NULL: copied into the workspace on compute_stream)
+ *   groups        HOST int32 [n_groups][2], RecomputeConfig normal form (model.py:166-178)
+ *   sender_kv     producer export (may be NULL iff groups cover every layer)
+ *   sender_e      E caches; one per transition layer (group start > 0)
+ *   out_kv        consumer cache receiving K/V for positions 0..n-1 of every layer
+ *   logits_out    device f32 [V];  token_out  device int32 [1] (argmax, lowest id on ties)
+ *   copy_stream   optional second stream: KV ingest overlaps recompute (sched.py:212-263)
+ * On DS_ERR_CACHE_MISS, *miss_layer / *miss_kind name the first miss in the
+ * reference's order (KV misses ascending, then E per group, model.py:590-617). */
+DS_API int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
+                       const int32_t* groups, int32_t n_groups, const ds_kv_cache* sender_kv,
+                       const ds_e_cache* sender_e, int32_t n_e, const ds_kv_cache* out_kv, float* logits_out,
+                       int32_t* token_out, void* workspace, size_t workspace_bytes, void* compute_stream,
+                       void* copy_stream, int32_t* miss_layer, int32_t* miss_kind);
+
+/* Producer export — full_prefill (model.py:641-649): K/V of all n positions into
+ * out_kv, E (bf16 [n-1][d]) for each layer listed in e_layers (store_prefill's
+ * serving-mode filter keeps only transition layers, store.py:202-203), logits. */
+DS_API int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
+                    const ds_kv_cache* out_kv, const int32_t* e_layers, int32_t n_e, void* const* e_out,
+                    float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* ---- single-kernel entry points (used by the parity tests and the scheduler) ---- */
+
+/* C = epilogue(A[M][K] . B[N][K]^T); mode 0 bf16 store, 1 f32 out = resid + acc,
+ * 2 bf16 silu, 4 f32 store.  tcgen05/TMEM kernel. */
+DS_API int ds_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const float* resid,
+            int64_t ld_resid, int32_t M, int32_t N, int32_t K, int32_t mode, void* stream);
+
+/* RMSNorm (model.py:466-468): out_bf16[r] = bf16(x[r] / sqrt(mean(x[r]^2) + 1e-6) * gain).
+ * x is f32 (x_is_bf16 = 0) or bf16; optional row gather (int64 ids); optional f32 and
+ * bf16 copies of the (gathered) input rows. */
+DS_API int ds_rmsnorm(const void* x, int32_t x_is_bf16, const int64_t* gather, int32_t M, int32_t d, const float* gain,
+               void* out_bf16, float* copy_f32, void* copy_bf16, void* stream);
+
+/* Causal GQA flash-attention prefill over a cache layer (model.py:506-519):
+ * q bf16 [n_q][H*D] (row r at absolute position q_pos0 + r, keys 0..q_pos0+r),
+ * o bf16 [n_q][H*D]. */
+DS_API int ds_attention_prefill(const void* q, int64_t ldq, const ds_kv_cache* kv, int32_t layer, int32_t n_q,
+                         int32_t q_pos0, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, void* o,
+                         int64_t ldo, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DROIDSPEAK_H */

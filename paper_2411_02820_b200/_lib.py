@@ -1,0 +1,99 @@
+"""ctypes binding of the C ABI (include/droidspeak.h).
+
+The library is the product path: if it is missing or fails to load, every
+entry point raises — there is no CPU or eager-PyTorch fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import CacheMissError, DegenerateInputError
+
+LIB_PATH = Path(__file__).resolve().parent / "libdroidspeak.so"
+
+DS_OK, DS_ERR_INVALID, DS_ERR_CACHE_MISS, DS_ERR_DEGENERATE, DS_ERR_CUDA = range(5)
+MISS_KIND = {1: "kv", 2: "e"}
+
+# epilogue modes of ds_gemm
+EPI_STORE_BF16, EPI_RESID_F32, EPI_SILU_BF16, EPI_QKV_ROPE, EPI_STORE_F32 = range(5)
+
+
+class Dims(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in
+                ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab_size", "max_seq")]
+
+
+class LayerWeights(C.Structure):
+    _fields_ = [("wqkv", C.c_void_p), ("wo", C.c_void_p), ("w1", C.c_void_p), ("w2", C.c_void_p),
+                ("g_attn", C.c_void_p), ("g_mlp", C.c_void_p)]
+
+
+class Model(C.Structure):
+    _fields_ = [("dims", Dims), ("embed", C.c_void_p), ("unembed", C.c_void_p), ("g_final", C.c_void_p),
+                ("rope_cos", C.c_void_p), ("rope_sin", C.c_void_p), ("layers", C.POINTER(LayerWeights))]
+
+
+class KvCache(C.Structure):
+    _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("layer_stride", C.c_int64), ("head_stride", C.c_int64),
+                ("page_stride", C.c_int64), ("block_table", C.c_void_p), ("n_layers", C.c_int32),
+                ("positions", C.c_int32)]
+
+
+class ECacheDesc(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("positions", C.c_int32), ("width", C.c_int32), ("hidden", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH.name} is not built; run `python -m paper_2411_02820_b200._build` "
+                "(the CUDA path has no CPU fallback)")
+        h = C.CDLL(str(LIB_PATH))
+        P, I32, I64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
+        sig = {
+            "ds_abi_version": (I32, []),
+            "ds_last_error": (C.c_char_p, []),
+            "ds_workspace_size": (SZ, [C.POINTER(Dims), I32]),
+            "ds_kv_ingest": (I32, [C.POINTER(KvCache), C.POINTER(KvCache), P, I32, I32, I32, I32, P,
+                                   C.POINTER(I32)]),
+            "ds_partial_prefill": (I32, [C.POINTER(Model), P, P, I32, P, I32, C.POINTER(KvCache),
+                                         C.POINTER(ECacheDesc), I32, C.POINTER(KvCache), P, P, P, SZ, P, P,
+                                         C.POINTER(I32), C.POINTER(I32)]),
+            "ds_full_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), P, I32, P, P, P, P, SZ, P]),
+            "ds_gemm": (I32, [P, I64, P, I64, P, I64, P, I64, I32, I32, I32, I32, P]),
+            "ds_rmsnorm": (I32, [P, I32, P, I32, I32, P, P, P, P, P]),
+            "ds_attention_prefill": (I32, [P, I64, C.POINTER(KvCache), I32, I32, I32, I32, I32, I32, P, I64, P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        if h.ds_abi_version() != 1:
+            raise RuntimeError("droidspeak ABI version mismatch")
+        _lib = h
+    return _lib
+
+
+def check(rc: int, miss_layer: int | None = None, miss_kind: int | None = None) -> None:
+    """Map a ds_status onto the reference's exception types (errors.py:6-27)."""
+    if rc == DS_OK:
+        return
+    msg = lib().ds_last_error().decode(errors="replace")
+    if rc == DS_ERR_CACHE_MISS:
+        raise CacheMissError(int(miss_layer), MISS_KIND.get(miss_kind, "kv"), msg)
+    if rc == DS_ERR_DEGENERATE:
+        raise DegenerateInputError(msg)
+    if rc == DS_ERR_INVALID:
+        raise ValueError(msg)
+    raise RuntimeError(f"droidspeak CUDA error: {msg}")
+
+
+EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_workspace_size", "ds_kv_ingest", "ds_partial_prefill",
+                    "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill")

@@ -1,0 +1,512 @@
+// C ABI (include/droidspeak.h) and the native orchestration of the
+// cross-model prefill: validation in the reference's order, workspace
+// carving, the per-layer kernel sequence, and the two-stream pipeline
+// (ingest on the copy stream overlapping recompute on the compute stream,
+// anchor gated on both — the pipelined plan of sched.py:212-263).
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace ds;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return fail(DS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define DS_TRY(expr, what)                      \
+  do {                                          \
+    int _rc = (expr);                           \
+    if (_rc != DS_OK) {                         \
+      if (_rc == DS_ERR_CUDA) return cuda_fail(what); \
+      return fail(_rc, "%s: invalid launch arguments", what); \
+    }                                           \
+  } while (0)
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Workspace {
+  int64_t* tokens;
+  float* h;   // [n][d] residual stream
+  bf16* a;    // [n][d] normalised GEMM operand
+  bf16* q;    // [n][H*D]
+  bf16* o;    // [n][H*D]
+  bf16* u;    // [n][d_ff]
+  float* h_a;  // [d] anchor residual
+  bf16* a_a;   // [d] scratch
+  bf16* q_a;   // [H*D]
+  bf16* o_a;   // [H*D]
+  bf16* u_a;   // [d_ff]
+  float* part_o;
+  float* part_ml;
+  unsigned long long* argmax;
+  size_t bytes;
+};
+
+Workspace carve(const ds_dims& m, int n, void* base) {
+  Workspace w{};
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> uint8_t* {
+    uint8_t* r = p ? p + off : nullptr;
+    off += align_up(bytes);
+    return r;
+  };
+  const size_t hd = (size_t)m.n_heads * m.head_dim;
+  const int splits = decode_splits(n);
+  w.tokens = reinterpret_cast<int64_t*>(take(8ull * n));
+  w.h = reinterpret_cast<float*>(take(4ull * n * m.d_model));
+  w.a = reinterpret_cast<bf16*>(take(2ull * n * m.d_model));
+  w.q = reinterpret_cast<bf16*>(take(2ull * n * hd));
+  w.o = reinterpret_cast<bf16*>(take(2ull * n * hd));
+  w.u = reinterpret_cast<bf16*>(take(2ull * n * m.d_ff));
+  w.h_a = reinterpret_cast<float*>(take(4ull * m.d_model));
+  w.a_a = reinterpret_cast<bf16*>(take(2ull * m.d_model));
+  w.q_a = reinterpret_cast<bf16*>(take(2ull * hd));
+  w.o_a = reinterpret_cast<bf16*>(take(2ull * hd));
+  w.u_a = reinterpret_cast<bf16*>(take(2ull * m.d_ff));
+  w.part_o = reinterpret_cast<float*>(take(4ull * splits * hd));
+  w.part_ml = reinterpret_cast<float*>(take(8ull * splits * m.n_heads));
+  w.argmax = reinterpret_cast<unsigned long long*>(take(8));
+  w.bytes = off;
+  return w;
+}
+
+int check_dims(const ds_dims& d) {
+  if (d.n_layers < 1 || d.n_layers > kMaxLayers) return fail(DS_ERR_INVALID, "n_layers %d outside [1,%d]", d.n_layers, kMaxLayers);
+  if (d.head_dim != 64 && d.head_dim != 128) return fail(DS_ERR_INVALID, "head_dim %d unsupported (64|128)", d.head_dim);
+  if (d.n_kv_heads < 1 || d.n_heads % d.n_kv_heads) return fail(DS_ERR_INVALID, "n_kv_heads must divide n_heads");
+  if (d.n_heads / d.n_kv_heads > 8) return fail(DS_ERR_INVALID, "GQA ratio > 8 unsupported");
+  if (d.d_model != d.n_heads * d.head_dim) return fail(DS_ERR_INVALID, "d_model != n_heads*head_dim");
+  if (d.d_model % 64 || d.d_ff % 64) return fail(DS_ERR_INVALID, "d_model and d_ff must be multiples of 64");
+  if (d.vocab_size < 2 || d.vocab_size % 2) return fail(DS_ERR_INVALID, "vocab_size must be even");
+  if (d.max_seq < 2) return fail(DS_ERR_INVALID, "max_seq must be >= 2");
+  return DS_OK;
+}
+
+// check_tokens (model.py:425-437)
+int check_tokens(const ds_dims& d, const int64_t* tokens, int n) {
+  if (!tokens) return fail(DS_ERR_INVALID, "tokens_host is NULL");
+  if (n < 2) return fail(DS_ERR_DEGENERATE, "need at least 2 tokens, got %d", n);
+  if (n > d.max_seq) return fail(DS_ERR_INVALID, "sequence length %d exceeds max_seq %d", n, d.max_seq);
+  for (int i = 0; i < n; ++i)
+    if (tokens[i] < 0 || tokens[i] >= d.vocab_size) return fail(DS_ERR_INVALID, "token id out of vocabulary range");
+  return DS_OK;
+}
+
+KvAddr layer_addr(const ds_kv_cache& c, int layer, int head_dim) {
+  KvAddr a;
+  a.k = static_cast<bf16*>(c.k) + (long long)layer * c.layer_stride;
+  a.v = static_cast<bf16*>(c.v) + (long long)layer * c.layer_stride;
+  a.head_stride = c.head_stride;
+  a.page_stride = c.page_stride;
+  a.table = c.block_table;
+  a.head_dim = head_dim;
+  return a;
+}
+
+struct Ctx {
+  const ds_model* m;
+  const ds_dims& d;
+  Workspace w;
+  const ds_kv_cache* kv;
+  cudaStream_t s;
+};
+
+// (a = RMSNorm(h) already in the workspace) QKV (+RoPE, K/V into the cache) -> [attention -> o-proj+resid -> RMSNorm -> W1+SiLU -> W2+resid]
+// over `rows` window rows at positions 0..rows-1 (model.py:536-544).  `kv_only`: the window output of
+// this layer is dead (last layer of a group, model.py:625), so only the K/V columns are projected.
+int window_layer(Ctx& c, int l, int rows, bool kv_only) {
+  const ds_dims& d = c.d;
+  const ds_layer_weights& W = c.m->layers[l];
+  const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
+  GemmEpi e{};
+  e.mode = EPI_QKV_ROPE;
+  e.M = rows;
+  e.N = kv_only ? 2 * kvd : hd + 2 * kvd;
+  e.n_offset = kv_only ? hd : 0;
+  e.n_heads = d.n_heads;
+  e.n_kv_heads = d.n_kv_heads;
+  e.head_dim = d.head_dim;
+  e.q_out = c.w.q;
+  e.ld_q = hd;
+  e.kv = layer_addr(*c.kv, l, d.head_dim);
+  e.pos0 = 0;
+  e.rope_cos = c.m->rope_cos;
+  e.rope_sin = c.m->rope_sin;
+  const bf16* wqkv = static_cast<const bf16*>(W.wqkv) + (kv_only ? (long long)hd * d.d_model : 0);
+  DS_TRY(gemm_launch(c.w.a, d.d_model, wqkv, d.d_model, d.d_model, e, c.s), "qkv gemm");
+  if (kv_only) return DS_OK;
+  const KvAddr ka = layer_addr(*c.kv, l, d.head_dim);
+  DS_TRY(attention_prefill_launch(c.w.q, hd, ka.k, ka.v, ka.head_stride, ka.page_stride, ka.table, rows, 0,
+                                  d.n_heads, d.n_kv_heads, d.head_dim, c.w.o, hd, c.s),
+         "attention");
+  GemmEpi r{};
+  r.mode = EPI_RESID_F32;
+  r.M = rows;
+  r.N = d.d_model;
+  r.out = c.w.h;
+  r.ld_out = d.d_model;
+  r.resid = c.w.h;
+  r.ld_resid = d.d_model;
+  DS_TRY(gemm_launch(c.w.o, hd, W.wo, hd, hd, r, c.s), "o-proj gemm");
+  DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, rows, d.d_model, W.g_mlp, c.w.a, nullptr, nullptr, 0, c.s),
+         "rmsnorm");
+  GemmEpi f{};
+  f.mode = EPI_SILU_BF16;
+  f.M = rows;
+  f.N = d.d_ff;
+  f.out = c.w.u;
+  f.ld_out = d.d_ff;
+  DS_TRY(gemm_launch(c.w.a, d.d_model, W.w1, d.d_model, d.d_model, f, c.s), "w1 gemm");
+  DS_TRY(gemm_launch(c.w.u, d.d_ff, W.w2, d.d_ff, d.d_ff, r, c.s), "w2 gemm");
+  return DS_OK;
+}
+
+// The single anchor row at position `pos` through layer l (_layer_single, model.py:547-562).
+int anchor_layer(Ctx& c, int l, int pos, float* h_a) {
+  const ds_dims& d = c.d;
+  const ds_layer_weights& W = c.m->layers[l];
+  const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
+  GemvArgs g{};
+  g.W = static_cast<const bf16*>(W.wqkv);
+  g.ldw = d.d_model;
+  g.N = hd + 2 * kvd;
+  g.K = d.d_model;
+  g.x_f32 = h_a;
+  g.gain = W.g_attn;
+  g.mode = EPI_QKV_ROPE;
+  g.n_heads = d.n_heads;
+  g.n_kv_heads = d.n_kv_heads;
+  g.head_dim = d.head_dim;
+  g.pos = pos;
+  g.q_out = c.w.q_a;
+  g.kv = layer_addr(*c.kv, l, d.head_dim);
+  g.rope_cos = c.m->rope_cos;
+  g.rope_sin = c.m->rope_sin;
+  DS_TRY(gemv_launch(g, c.s), "anchor qkv");
+  const KvAddr ka = g.kv;
+  DS_TRY(decode_attention_launch(c.w.q_a, ka.k, ka.v, ka.head_stride, ka.page_stride, ka.table, pos + 1,
+                                 d.n_heads, d.n_kv_heads, d.head_dim, c.w.part_o, c.w.part_ml, c.w.o_a, c.s),
+         "anchor attention");
+  GemvArgs o{};
+  o.W = static_cast<const bf16*>(W.wo);
+  o.ldw = hd;
+  o.N = d.d_model;
+  o.K = hd;
+  o.x_bf16 = c.w.o_a;
+  o.mode = EPI_RESID_F32;
+  o.out_f32 = h_a;
+  o.resid = h_a;
+  DS_TRY(gemv_launch(o, c.s), "anchor o-proj");
+  GemvArgs f{};
+  f.W = static_cast<const bf16*>(W.w1);
+  f.ldw = d.d_model;
+  f.N = d.d_ff;
+  f.K = d.d_model;
+  f.x_f32 = h_a;
+  f.gain = W.g_mlp;
+  f.mode = EPI_SILU_BF16;
+  f.out_bf16 = c.w.u_a;
+  DS_TRY(gemv_launch(f, c.s), "anchor w1");
+  GemvArgs s2{};
+  s2.W = static_cast<const bf16*>(W.w2);
+  s2.ldw = d.d_ff;
+  s2.N = d.d_model;
+  s2.K = d.d_ff;
+  s2.x_bf16 = c.w.u_a;
+  s2.mode = EPI_RESID_F32;
+  s2.out_f32 = h_a;
+  s2.resid = h_a;
+  DS_TRY(gemv_launch(s2, c.s), "anchor w2");
+  return DS_OK;
+}
+
+// _final_logits + greedy first token (model.py:565-566, 779).
+int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token) {
+  const ds_dims& d = c.d;
+  if (cudaMemsetAsync(c.w.argmax, 0, 8, c.s) != cudaSuccess) return cuda_fail("memset");
+  GemvArgs g{};
+  g.W = static_cast<const bf16*>(c.m->unembed);
+  g.ldw = d.d_model;
+  g.N = d.vocab_size;
+  g.K = d.d_model;
+  g.x_f32 = h_a;
+  g.gain = c.m->g_final;
+  g.mode = EPI_STORE_F32;
+  g.out_f32 = logits;
+  g.argmax = c.w.argmax;
+  DS_TRY(gemv_launch(g, c.s), "lm head");
+  if (token) DS_TRY(argmax_finalize_launch(c.w.argmax, token, c.s), "argmax");
+  return DS_OK;
+}
+
+const int64_t* stage_tokens(const int64_t* host, const int64_t* dev, int n, Workspace& w, cudaStream_t s) {
+  if (dev) return dev;
+  if (cudaMemcpyAsync(w.tokens, host, 8ull * n, cudaMemcpyHostToDevice, s) != cudaSuccess) return nullptr;
+  return w.tokens;
+}
+
+int check_cache(const ds_kv_cache* c, const ds_dims& d, int n, const char* what) {
+  if (!c || !c->k || !c->v) return fail(DS_ERR_INVALID, "%s cache is NULL", what);
+  if (c->n_layers < d.n_layers || c->positions < n)
+    return fail(DS_ERR_INVALID, "%s cache holds %d layers x %d positions, need %d x %d", what, c->n_layers,
+                c->positions, d.n_layers, n);
+  return DS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ds_abi_version(void) { return DS_ABI_VERSION; }
+const char* ds_last_error(void) { return g_err.c_str(); }
+
+size_t ds_workspace_size(const ds_dims* dims, int32_t n_tokens) {
+  if (!dims || n_tokens < 1) return 0;
+  return carve(*dims, n_tokens, nullptr).bytes;
+}
+
+int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const int32_t* reused, int32_t n_reused,
+                  int32_t window, int32_t n_kv_heads, int32_t head_dim, void* stream, int32_t* miss_layer) {
+  g_err.clear();
+  if (!dst || (!reused && n_reused) || n_reused < 0 || window < 1 || n_kv_heads < 1 ||
+      (head_dim != 64 && head_dim != 128))
+    return fail(DS_ERR_INVALID, "bad ingest arguments");
+  if (n_reused > kMaxLayers) return fail(DS_ERR_INVALID, "too many layers");
+  for (int i = 0; i < n_reused; ++i) {
+    const int l = reused[i];
+    if (i && reused[i - 1] >= l) return fail(DS_ERR_INVALID, "reused layers must ascend");
+    if (!src || src->n_layers <= l || src->positions < window) {
+      if (miss_layer) *miss_layer = l;
+      return fail(DS_ERR_CACHE_MISS, "missing kv cache for layer %d", l);
+    }
+    if (l < 0 || l >= dst->n_layers || dst->positions < window) return fail(DS_ERR_INVALID, "destination too small");
+  }
+  DS_TRY(kv_ingest_launch(*src, *dst, reused, n_reused, n_kv_heads, head_dim, window, (cudaStream_t)stream),
+         "kv ingest");
+  return DS_OK;
+}
+
+int ds_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, const float* resid,
+            int64_t ld_resid, int32_t M, int32_t N, int32_t K, int32_t mode, void* stream) {
+  g_err.clear();
+  if (!A || !B || !C || M < 1 || N < 16 || K < 8 || (N % 16) || (K % 8))
+    return fail(DS_ERR_INVALID, "bad gemm shape M=%d N=%d K=%d", M, N, K);
+  if (mode != EPI_STORE_BF16 && mode != EPI_RESID_F32 && mode != EPI_SILU_BF16 && mode != EPI_STORE_F32)
+    return fail(DS_ERR_INVALID, "bad epilogue mode %d", mode);
+  if (mode == EPI_RESID_F32 && !resid) return fail(DS_ERR_INVALID, "resid required");
+  GemmEpi e{};
+  e.mode = mode;
+  e.M = M;
+  e.N = N;
+  e.out = C;
+  e.ld_out = ldc;
+  e.resid = resid;
+  e.ld_resid = ld_resid;
+  DS_TRY(gemm_launch(A, lda, B, ldb, K, e, (cudaStream_t)stream), "gemm");
+  return DS_OK;
+}
+
+int ds_rmsnorm(const void* x, int32_t x_is_bf16, const int64_t* gather, int32_t M, int32_t d, const float* gain,
+               void* out_bf16, float* copy_f32, void* copy_bf16, void* stream) {
+  g_err.clear();
+  if (!x || !gain || !out_bf16 || M < 1 || d < 8 || (d % 8)) return fail(DS_ERR_INVALID, "bad rmsnorm arguments");
+  DS_TRY(rmsnorm_launch(x, x_is_bf16 != 0, gather, M, d, gain, static_cast<bf16*>(out_bf16), copy_f32,
+                        static_cast<bf16*>(copy_bf16), M, (cudaStream_t)stream),
+         "rmsnorm");
+  return DS_OK;
+}
+
+int ds_attention_prefill(const void* q, int64_t ldq, const ds_kv_cache* kv, int32_t layer, int32_t n_q,
+                         int32_t q_pos0, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, void* o,
+                         int64_t ldo, void* stream) {
+  g_err.clear();
+  if (!q || !kv || !o || n_q < 1 || q_pos0 < 0 || n_kv_heads < 1 || n_heads % n_kv_heads ||
+      (head_dim != 64 && head_dim != 128) || layer < 0 || layer >= kv->n_layers || q_pos0 + n_q > kv->positions)
+    return fail(DS_ERR_INVALID, "bad attention arguments");
+  const KvAddr a = layer_addr(*kv, layer, head_dim);
+  DS_TRY(attention_prefill_launch(static_cast<const bf16*>(q), ldq, a.k, a.v, a.head_stride, a.page_stride, a.table,
+                                  n_q, q_pos0, n_heads, n_kv_heads, head_dim, static_cast<bf16*>(o), ldo,
+                                  (cudaStream_t)stream),
+         "attention");
+  return DS_OK;
+}
+
+int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
+                       const int32_t* groups, int32_t n_groups, const ds_kv_cache* sender_kv,
+                       const ds_e_cache* sender_e, int32_t n_e, const ds_kv_cache* out_kv, float* logits_out,
+                       int32_t* token_out, void* workspace, size_t workspace_bytes, void* compute_stream,
+                       void* copy_stream, int32_t* miss_layer, int32_t* miss_kind) {
+  g_err.clear();
+  if (miss_kind) *miss_kind = DS_MISS_NONE;
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if ((rc = check_tokens(d, tokens_host, n_tokens))) return rc;
+  const int L = d.n_layers, n = n_tokens, P = n - 1;
+  // RecomputeConfig normal form + validate_for (model.py:166-178, 204-208)
+  if (n_groups < 0 || (n_groups && !groups)) return fail(DS_ERR_INVALID, "bad groups");
+  std::vector<char> covered(L, 0);
+  for (int i = 0; i < n_groups; ++i) {
+    const int a = groups[2 * i], b = groups[2 * i + 1];
+    if (a < 0 || a > b) return fail(DS_ERR_INVALID, "range [%d,%d] invalid", a, b);
+    if (i && a <= groups[2 * i - 1] + 1) return fail(DS_ERR_INVALID, "groups not in normal form");
+    if (b > L - 1) return fail(DS_ERR_INVALID, "config exceeds layer range [0,%d]", L - 1);
+    for (int l = a; l <= b; ++l) covered[l] = 1;
+  }
+  if ((rc = check_cache(out_kv, d, n, "output"))) return rc;
+  if (!logits_out) return fail(DS_ERR_INVALID, "logits_out is NULL");
+  // KV misses in ascending layer order (model.py:590-601)
+  std::vector<int32_t> reused;
+  for (int l = 0; l < L; ++l) {
+    if (covered[l]) continue;
+    if (!sender_kv || !sender_kv->k || sender_kv->n_layers <= l || sender_kv->positions < P) {
+      if (miss_layer) *miss_layer = l;
+      if (miss_kind) *miss_kind = DS_MISS_KV;
+      return fail(DS_ERR_CACHE_MISS, "missing kv cache for layer %d", l);
+    }
+    reused.push_back(l);
+  }
+  // E misses per group (model.py:611-617)
+  std::vector<const ds_e_cache*> seed(n_groups, nullptr);
+  for (int i = 0; i < n_groups; ++i) {
+    const int a = groups[2 * i];
+    if (a == 0) continue;
+    for (int j = 0; j < n_e; ++j)
+      if (sender_e && sender_e[j].layer == a) seed[i] = &sender_e[j];
+    const ds_e_cache* e = seed[i];
+    if (!e || !e->hidden || e->positions < P || e->width != d.d_model) {
+      if (miss_layer) *miss_layer = a;
+      if (miss_kind) *miss_kind = DS_MISS_E;
+      return fail(DS_ERR_CACHE_MISS, "missing e cache for layer %d", a);
+    }
+  }
+  Workspace w = carve(d, n, workspace);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
+
+  cudaStream_t cs = (cudaStream_t)compute_stream;
+  cudaStream_t xs = copy_stream ? (cudaStream_t)copy_stream : cs;
+  const int64_t* tok = stage_tokens(tokens_host, tokens_dev, n, w, cs);
+  if (!tok) return cuda_fail("token upload");
+  Ctx c{m, d, w, out_kv, cs};
+
+  // ---- ingest (copy stream) overlapping recompute (compute stream)
+  struct Events {
+    cudaEvent_t fork = nullptr, join = nullptr;
+    ~Events() {
+      if (fork) cudaEventDestroy(fork);
+      if (join) cudaEventDestroy(join);
+    }
+  } ev;
+  cudaEvent_t& ev_fork = ev.fork;
+  cudaEvent_t& ev_join = ev.join;
+  if (xs != cs) {
+    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_fail("event");
+    cudaEventRecord(ev_fork, cs);
+    cudaStreamWaitEvent(xs, ev_fork, 0);
+  }
+  if (!reused.empty())
+    DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P, xs),
+           "kv ingest");
+  if (xs != cs) cudaEventRecord(ev_join, xs);
+
+  // ---- selective recompute of each group over the window
+  for (int i = 0; i < n_groups; ++i) {
+    const int a = groups[2 * i], b = groups[2 * i + 1];
+    const ds_layer_weights& Wa = m->layers[a];
+    if (a == 0)
+      DS_TRY(rmsnorm_launch(m->embed, true, tok, P, d.d_model, Wa.g_attn, w.a, w.h, nullptr, P, cs), "seed");
+    else
+      DS_TRY(rmsnorm_launch(seed[i]->hidden, true, nullptr, P, d.d_model, Wa.g_attn, w.a, w.h, nullptr, P, cs),
+             "seed");
+    for (int l = a; l <= b; ++l) {
+      if (l > a)
+        DS_TRY(rmsnorm_launch(w.h, false, nullptr, P, d.d_model, m->layers[l].g_attn, w.a, nullptr, nullptr, 0, cs),
+               "rmsnorm");
+      rc = window_layer(c, l, P, l == b);
+      if (rc) return rc;
+    }
+  }
+
+  // ---- anchor pass after all KV has landed (sched.py:256)
+  if (xs != cs) cudaStreamWaitEvent(cs, ev_join, 0);
+  DS_TRY(rmsnorm_launch(m->embed, true, tok + P, 1, d.d_model, m->layers[0].g_attn, w.a_a, w.h_a, nullptr, 1, cs),
+         "anchor seed");
+  for (int l = 0; l < L; ++l) {
+    rc = anchor_layer(c, l, P, w.h_a);
+    if (rc) return rc;
+  }
+  return lm_head(c, w.h_a, logits_out, token_out);
+}
+
+int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
+                    const ds_kv_cache* out_kv, const int32_t* e_layers, int32_t n_e, void* const* e_out,
+                    float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if ((rc = check_tokens(d, tokens_host, n_tokens))) return rc;
+  if ((rc = check_cache(out_kv, d, n_tokens, "output"))) return rc;
+  if (!logits_out) return fail(DS_ERR_INVALID, "logits_out is NULL");
+  const int L = d.n_layers, n = n_tokens, P = n - 1;
+  std::vector<bf16*> e_at(L, nullptr);
+  for (int i = 0; i < n_e; ++i) {
+    const int l = e_layers[i];
+    if (l < 0 || l >= L || !e_out || !e_out[i]) return fail(DS_ERR_INVALID, "bad e export layer %d", l);
+    e_at[l] = static_cast<bf16*>(e_out[i]);
+  }
+  Workspace w = carve(d, n, workspace);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t* tok = stage_tokens(tokens_host, tokens_dev, n, w, s);
+  if (!tok) return cuda_fail("token upload");
+  Ctx c{m, d, w, out_kv, s};
+  // All n rows run batched through layers 0..L-2 (the anchor row is just row P
+  // of the causal prefill); at the last layer only the window's K/V are live,
+  // so rows 0..P-1 project K/V and row P finishes through the anchor path.
+  // E at layer 0 = the token embeddings over the window (model.py:609, 620-621)
+  DS_TRY(rmsnorm_launch(m->embed, true, tok, n, d.d_model, m->layers[0].g_attn, w.a, w.h, e_at[0], P, s), "seed");
+  for (int l = 0; l < L; ++l) {
+    const bool last = l == L - 1;
+    if (l > 0)
+      DS_TRY(rmsnorm_launch(w.h, false, nullptr, n, d.d_model, m->layers[l].g_attn, w.a, nullptr, e_at[l], P, s),
+             "rmsnorm");
+    if (!last) {
+      rc = window_layer(c, l, n, false);
+    } else {
+      rc = window_layer(c, l, P, true);
+      if (!rc) rc = anchor_layer(c, l, P, w.h + (long long)P * d.d_model);
+    }
+    if (rc) return rc;
+  }
+  return lm_head(c, w.h + (long long)P * d.d_model, logits_out, token_out);
+}
+
+}  // extern "C"

@@ -1,0 +1,331 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+//   C[M,N] = A[M,K] . B[N,K]^T      A = activations (bf16, K-major)
+//                                   B = weights     (bf16, K-major: the reference
+//                                       [in,out] matrices transposed once at load)
+//
+// Roles (192 threads, 1 CTA per SM):
+//   warp 0      TMA producer: A 128x64 and B BNx64 tiles, SWIZZLE_128B, STAGES-deep ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 2..5  epilogue: tcgen05.ld accumulator rows -> fused epilogue -> global
+// Two TMEM accumulators (2*BN columns) let the epilogue of tile i overlap the
+// MMAs of tile i+1.
+//
+// Epilogues (the reference block math, model.py:522-544):
+//   EPI_QKV_ROPE  q/k rotate-half RoPE (model.py:475-488) in fp32; q -> bf16 buffer,
+//                 k/v -> bf16 KV cache through KvAddr (paged or dense export layout)
+//   EPI_RESID_F32 out = resid + acc                (x = h + attn@wo, out = x + mlp)
+//   EPI_SILU_BF16 out = bf16(silu(acc))            (silu(rms(x)*g @ w1))
+//   EPI_STORE_*   plain stores (tests / lm head)
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ds {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 192;
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
+  static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
+  static constexpr uint32_t TOTAL = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
+};
+
+DS_DEV void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  // Grouped raster: GROUP m-blocks sweep all n-blocks before moving on, so the
+  // ~148 concurrently resident tiles share A rows and B columns in L2.
+  constexpr int GROUP = 16;
+  int per_group = GROUP * num_n;
+  int g = t / per_group;
+  int first_m = g * GROUP;
+  int gsize = min(num_m - first_m, GROUP);
+  int r = t - g * per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+template <int BN>
+DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
+  const bool row_ok = row < e.M;
+  const int col0 = nb * BN;
+  if (e.mode == EPI_QKV_ROPE) {
+    const int D = e.head_dim;
+    const int half = D >> 1;
+    const int pos = e.pos0 + row;
+    for (int cb = 0; cb < BN; cb += D) {
+      const int gcol = col0 + cb;  // column within this launch's N range
+      if (gcol >= e.N) break;      // uniform across the warp
+      const int head = (gcol + e.n_offset) / D;
+      const bool is_q = head < e.n_heads;
+      const bool is_k = !is_q && head < e.n_heads + e.n_kv_heads;
+      for (int j = 0; j < half; j += 16) {
+        float lo[16], hi[16];
+        tmem_ld16x2(tbase + cb + j, tbase + cb + half + j, lo, hi);
+        if (!row_ok) continue;
+        if (is_q || is_k) {
+          const float* cs = e.rope_cos + (long long)pos * half + j;
+          const float* sn = e.rope_sin + (long long)pos * half + j;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float c = __ldg(cs + i), s = __ldg(sn + i);
+            float x1 = lo[i], x2 = hi[i];
+            lo[i] = x1 * c - x2 * s;
+            hi[i] = x1 * s + x2 * c;
+          }
+        }
+        uint32_t pl[8], ph[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          pl[i] = pack_bf16x2(lo[2 * i], lo[2 * i + 1]);
+          ph[i] = pack_bf16x2(hi[2 * i], hi[2 * i + 1]);
+        }
+        bf16* dst;
+        if (is_q) {
+          dst = e.q_out + (long long)row * e.ld_q + (long long)head * D + j;
+        } else if (is_k) {
+          dst = e.kv.k + e.kv.off(head - e.n_heads, pos) + j;
+        } else {
+          dst = e.kv.v + e.kv.off(head - e.n_heads - e.n_kv_heads, pos) + j;
+        }
+        st_global_v4(dst, pl[0], pl[1], pl[2], pl[3]);
+        st_global_v4(dst + 8, pl[4], pl[5], pl[6], pl[7]);
+        st_global_v4(dst + half, ph[0], ph[1], ph[2], ph[3]);
+        st_global_v4(dst + half + 8, ph[4], ph[5], ph[6], ph[7]);
+      }
+    }
+    return;
+  }
+  for (int c = 0; c < BN; c += 16) {
+    const int col = col0 + c;
+    if (col >= e.N) break;
+    float v[16];
+    tmem_ld16(tbase + c, v);
+    if (!row_ok) continue;
+    if (e.mode == EPI_RESID_F32) {
+      const float4* r = reinterpret_cast<const float4*>(e.resid + (long long)row * e.ld_resid + col);
+      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float4 a = r[i];
+        o[i] = make_float4(a.x + v[4 * i], a.y + v[4 * i + 1], a.z + v[4 * i + 2], a.w + v[4 * i + 3]);
+      }
+    } else if (e.mode == EPI_STORE_F32) {
+      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+      if (e.mode == EPI_SILU_BF16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = silu(v[i]);
+      }
+      uint32_t p[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+      bf16* o = reinterpret_cast<bf16*>(e.out) + (long long)row * e.ld_out + col;
+      st_global_v4(o, p[0], p[1], p[2], p[3]);
+      st_global_v4(o + 8, p[4], p[5], p[6], p[7]);
+    }
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
+                        GemmEpi epi) {
+  using L = GemmSmem<BN, STAGES>;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * L::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (epi.M + GEMM_BM - 1) / GEMM_BM;
+  const int num_n = (epi.N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int k_blocks = (K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], L::STAGE_BYTES);
+          tma_load_2d(sA + stage * L::A_BYTES, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM);
+          tma_load_2d(sB + stage * L::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t IDESC = umma_idesc_bf16(GEMM_BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + stage * L::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * L::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            const uint64_t ad = sdesc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = sdesc_sw128(b_addr + k * 32, 16, 1024);
+            umma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (kb == k_blocks - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      epilogue_tile<BN>(epi, tbase, mb * GEMM_BM + quarter * 32 + lane, nb);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows][cols] matrix with leading dimension ld
+// (elements), box = box_rows x 64 columns, 128-byte swizzle.
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld,
+                   int box_rows, int box_cols) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -(int)r - 2;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int STAGES>
+static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int K, const GemmEpi& epi,
+                                 cudaStream_t stream, int max_ctas) {
+  using L = GemmSmem<BN, STAGES>;
+  auto kern = gemm_tcgen05_kernel<BN, STAGES>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((epi.M + GEMM_BM - 1) / GEMM_BM) * ((epi.N + BN - 1) / BN);
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  kern<<<grid, GEMM_THREADS, L::TOTAL, stream>>>(ta, tb, K, epi);
+  return cudaGetLastError();
+}
+
+// A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks BN from N.
+int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
+                cudaStream_t stream, int force_bn, int max_ctas) {
+  int bn = force_bn ? force_bn : (epi.N >= 1024 ? 256 : 128);
+  CUtensorMap ta, tb;
+  if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK)) return DS_ERR_CUDA;
+  if (make_tmap_bf16(&tb, B, epi.N, K, ldb, bn, GEMM_BK)) return DS_ERR_CUDA;
+  cudaError_t e = bn == 256 ? launch_gemm_t<256, 4>(ta, tb, K, epi, stream, max_ctas)
+                            : launch_gemm_t<128, 6>(ta, tb, K, epi, stream, max_ctas);
+  return e == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+}  // namespace ds

@@ -1,0 +1,130 @@
+// KV ingest: the reuse copy of _mixed_prefill (model.py:590-603) as a
+// TMA-bulk-staged scatter into the consumer's paged cache.
+//
+// Work unit = one (reused layer, K|V, kv head, 64-position page): a
+// contiguous run of rows*head_dim bf16 in both the producer's dense export
+// [L][KVH][n][D] and the consumer's paged [L][pages][KVH][64][D] layouts
+// (16 KB at D=128).  One elected thread per CTA streams its units through a
+// STAGES-deep ring of shared-memory buffers:
+//   cp.async.bulk global->shared (mbarrier complete_tx)  ->  cp.async.bulk shared->global
+// so every byte moves as a 16-byte-aligned bulk transfer with no register
+// staging.  HBM-bound: algorithmic bytes = 2 (read+write) x copied bytes.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ds {
+
+constexpr int INGEST_STAGES = 4;
+
+struct IngestArgs {
+  const uint8_t* src_k;
+  const uint8_t* src_v;
+  uint8_t* dst_k;
+  uint8_t* dst_v;
+  long long src_layer_stride, src_head_stride, src_page_stride;  // bytes
+  long long dst_layer_stride, dst_head_stride, dst_page_stride;  // bytes
+  const int32_t* src_table;
+  const int32_t* dst_table;
+  int32_t layers[kMaxLayers];  // reused layers, by value (graph-capturable)
+  int n_layers, n_kv_heads, head_dim, window, n_pages;
+};
+
+DS_DEV void ingest_unit(const IngestArgs& a, int u, const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
+  // u = ((li * 2 + kv) * KVH + h) * n_pages + p
+  int p = u % a.n_pages;
+  int t = u / a.n_pages;
+  int h = t % a.n_kv_heads;
+  t /= a.n_kv_heads;
+  int kv = t & 1;
+  int li = t >> 1;
+  int layer = a.layers[li];
+  int rows = min(kPage, a.window - p * kPage);
+  bytes = (uint32_t)rows * a.head_dim * 2;
+  int sp = a.src_table ? __ldg(a.src_table + p) : p;
+  int dp = a.dst_table ? __ldg(a.dst_table + p) : p;
+  src = (kv ? a.src_v : a.src_k) + layer * a.src_layer_stride + h * a.src_head_stride + sp * a.src_page_stride;
+  dst = (kv ? a.dst_v : a.dst_k) + layer * a.dst_layer_stride + h * a.dst_head_stride + dp * a.dst_page_stride;
+}
+
+__global__ void __launch_bounds__(32) kv_ingest_kernel(const __grid_constant__ IngestArgs a, int total_units, int stage_bytes) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t bars[INGEST_STAGES];
+  if (threadIdx.x != 0) return;
+  const int n_my = (total_units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  if (n_my <= 0) return;
+  for (int s = 0; s < INGEST_STAGES; ++s) mbar_init(&bars[s], 1);
+  fence_mbar_init();
+
+  auto issue_load = [&](int i) {
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    ingest_unit(a, (int)blockIdx.x + i * (int)gridDim.x, src, dst, bytes);
+    const int s = i % INGEST_STAGES;
+    mbar_expect_tx(&bars[s], bytes);
+    bulk_g2s(ring + s * stage_bytes, src, bytes, &bars[s]);
+  };
+
+  const int pro = n_my < INGEST_STAGES ? n_my : INGEST_STAGES;
+  for (int i = 0; i < pro; ++i) issue_load(i);
+  for (int i = 0; i < n_my; ++i) {
+    const int s = i % INGEST_STAGES;
+    mbar_wait(&bars[s], (uint32_t)(i / INGEST_STAGES) & 1u);
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t bytes;
+    ingest_unit(a, (int)blockIdx.x + i * (int)gridDim.x, src, dst, bytes);
+    bulk_s2g(dst, ring + s * stage_bytes, bytes);
+    bulk_commit();
+    const int refill = i - 1 + INGEST_STAGES;
+    if (i >= 1 && refill < n_my) {
+      bulk_wait_read<1>();  // the store of unit i-1 has finished reading its stage
+      issue_load(refill);
+    }
+  }
+  bulk_wait<0>();
+}
+
+int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
+                     int n_kv_heads, int head_dim, int window, cudaStream_t stream) {
+  if (n_layers <= 0 || window <= 0) return DS_OK;
+  IngestArgs a;
+  a.src_k = static_cast<const uint8_t*>(src.k);
+  a.src_v = static_cast<const uint8_t*>(src.v);
+  a.dst_k = static_cast<uint8_t*>(dst.k);
+  a.dst_v = static_cast<uint8_t*>(dst.v);
+  a.src_layer_stride = src.layer_stride * 2;
+  a.src_head_stride = src.head_stride * 2;
+  a.src_page_stride = src.page_stride * 2;
+  a.dst_layer_stride = dst.layer_stride * 2;
+  a.dst_head_stride = dst.head_stride * 2;
+  a.dst_page_stride = dst.page_stride * 2;
+  a.src_table = src.block_table;
+  a.dst_table = dst.block_table;
+  if (n_layers > kMaxLayers) return DS_ERR_INVALID;
+  for (int i = 0; i < n_layers; ++i) a.layers[i] = layers_host[i];
+  a.n_layers = n_layers;
+  a.n_kv_heads = n_kv_heads;
+  a.head_dim = head_dim;
+  a.window = window;
+  a.n_pages = (window + kPage - 1) / kPage;
+  const int stage_bytes = kPage * head_dim * 2;
+  const int smem = INGEST_STAGES * stage_bytes;
+  static int attr_smem = 0;
+  if (smem > attr_smem) {
+    if (cudaFuncSetAttribute(kv_ingest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return DS_ERR_CUDA;
+    attr_smem = smem;
+  }
+  const long long total = (long long)n_layers * 2 * n_kv_heads * a.n_pages;
+  if (total > 0x7fffffffLL) return DS_ERR_INVALID;
+  int per_sm = (200 * 1024) / (smem + 1024);
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 8) per_sm = 8;
+  long long grid = (long long)num_sms() * per_sm;
+  if (grid > total) grid = total;
+  kv_ingest_kernel<<<(int)grid, 32, smem, stream>>>(a, (int)total, stage_bytes);
+  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+}  // namespace ds

@@ -1,0 +1,77 @@
+// Internal kernel-launch interface shared by the .cu translation units.
+// (The public C ABI is include/droidspeak.h; this header is not installed.)
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/droidspeak.h"
+#include "common.cuh"
+
+namespace ds {
+
+enum EpiMode { EPI_STORE_BF16 = 0, EPI_RESID_F32 = 1, EPI_SILU_BF16 = 2, EPI_QKV_ROPE = 3, EPI_STORE_F32 = 4 };
+
+struct GemmEpi {
+  int mode;
+  int M, N;
+  void* out;            // bf16 / f32 [M][ld_out]
+  long long ld_out;
+  const float* resid;   // EPI_RESID_F32 (may alias out)
+  long long ld_resid;
+  // EPI_QKV_ROPE
+  int n_offset;         // column of the fused [q|k|v] projection that tile column 0 maps to
+  int n_heads, n_kv_heads, head_dim;
+  bf16* q_out;
+  long long ld_q;
+  KvAddr kv;
+  int pos0;             // absolute position of row 0
+  const float* rope_cos;  // [max_seq][head_dim/2]
+  const float* rope_sin;
+};
+
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_rows,
+                   int box_cols);
+int num_sms();
+int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
+                cudaStream_t stream, int force_bn = 0, int max_ctas = 0);
+
+int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
+                     int n_kv_heads, int head_dim, int window, cudaStream_t stream);
+
+int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,
+                   float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream);
+
+int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
+                             long long head_stride, long long page_stride, const int32_t* table, int n_q, int q_pos0,
+                             int n_heads, int n_kv_heads, int head_dim, bf16* o, long long ldo, cudaStream_t stream);
+
+// Single-row GEMV (anchor pass); see anchor.cu.
+struct GemvArgs {
+  const bf16* W;
+  long long ldw;
+  int N, K;
+  const float* x_f32;   // normalised when gain != nullptr
+  const float* gain;
+  const bf16* x_bf16;   // used when x_f32 == nullptr
+  int mode;             // EPI_QKV_ROPE / EPI_RESID_F32 / EPI_SILU_BF16 / EPI_STORE_F32
+  float* out_f32;
+  const float* resid;
+  bf16* out_bf16;
+  int n_heads, n_kv_heads, head_dim, pos;
+  bf16* q_out;
+  KvAddr kv;
+  const float* rope_cos;
+  const float* rope_sin;
+  unsigned long long* argmax;  // EPI_STORE_F32: packed (orderable value, ~index) max
+};
+
+int gemv_launch(const GemvArgs& a, cudaStream_t stream);
+int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, cudaStream_t stream);
+int decode_splits(int n_keys);
+int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_layer, long long head_stride,
+                            long long page_stride, const int32_t* table, int n_keys, int n_heads, int n_kv_heads,
+                            int head_dim, float* part_o, float* part_ml, bf16* out, cudaStream_t stream);
+
+}  // namespace ds

@@ -1,0 +1,87 @@
+// Row RMSNorm (model.py:466-468) producing the bf16 GEMM operand, optionally
+// gathering rows (token-embedding lookup, model.py:609/629) and emitting f32 /
+// bf16 copies of the input rows (the bf16 copy only for rows < copy_rows) (the residual stream seed, and the producer's
+// E-cache export, model.py:620-621).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ds {
+
+constexpr int NORM_THREADS = 256;
+
+template <bool IN_BF16>
+DS_DEV void load8(const void* x, long long idx, float* v) {
+  if (IN_BF16) {
+    uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(x) + idx);
+    float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), c = unpack_bf16x2(u.z), d = unpack_bf16x2(u.w);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y; v[6] = d.x; v[7] = d.y;
+  } else {
+    const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + idx);
+    float4 a = p[0], b = p[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+
+template <bool IN_BF16>
+__global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, const int64_t* gather, int d,
+                                                               const float* gain, bf16* out, float* copy_f32,
+                                                               bf16* copy_bf16, int copy_rows) {
+  const int r = blockIdx.x;
+  const long long src = gather ? (long long)__ldg(gather + r) : (long long)r;
+  const long long base = src * d;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 8; c < d; c += NORM_THREADS * 8) {
+    float v[8];
+    load8<IN_BF16>(x, base + c, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
+  }
+  __shared__ float red[NORM_THREADS / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < NORM_THREADS / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[0] / (float)d + 1e-6f);
+  const long long obase = (long long)r * d;
+  for (int c = threadIdx.x * 8; c < d; c += NORM_THREADS * 8) {
+    float v[8];
+    load8<IN_BF16>(x, base + c, v);
+    const float4 g0 = *reinterpret_cast<const float4*>(gain + c);
+    const float4 g1 = *reinterpret_cast<const float4*>(gain + c + 4);
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    uint32_t p[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = pack_bf16x2(v[2 * i] * inv * g[2 * i], v[2 * i + 1] * inv * g[2 * i + 1]);
+    *reinterpret_cast<uint4*>(out + obase + c) = make_uint4(p[0], p[1], p[2], p[3]);
+    if (copy_f32) {
+      float4* o = reinterpret_cast<float4*>(copy_f32 + obase + c);
+      o[0] = make_float4(v[0], v[1], v[2], v[3]);
+      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    if (copy_bf16 && r < copy_rows) {
+      uint32_t q[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+      *reinterpret_cast<uint4*>(copy_bf16 + obase + c) = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+  }
+}
+
+int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,
+                   float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream) {
+  if (M <= 0) return DS_OK;
+  if (x_bf16)
+    rmsnorm_kernel<true><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
+  else
+    rmsnorm_kernel<false><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
+  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+}  // namespace ds

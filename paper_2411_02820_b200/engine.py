@@ -1,0 +1,281 @@
+"""Producer export and consumer partial prefill on the B200 (the hot path).
+
+Python mirror of the reference entry points — same names, argument meaning
+and error behaviour as crosskv.model:
+
+    full_prefill(model, tokens)                                   model.py:641-649
+    partial_prefill(receiver, tokens, config, sender_kv, sender_e) model.py:660-679
+
+Each call validates on the host in the reference's order (check_tokens,
+validate_for, KV misses ascending, then E per group) and then makes ONE
+C-ABI call (ds_full_prefill / ds_partial_prefill) that launches the sm_100a
+kernel sequence on the caller's stream(s).  Torch only provides device
+memory and streams.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Iterable, Mapping, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .config import ModelConfig, RecomputeConfig
+from .errors import CacheMissError, DegenerateInputError
+from .weights import ModelWeights
+
+PAGE = 64
+
+
+def check_tokens(tokens, config: ModelConfig) -> np.ndarray:
+    """model.py:425-437: canonical int64 ids or raise."""
+    ids = np.asarray(tokens.cpu() if isinstance(tokens, torch.Tensor) else tokens, dtype=np.int64)
+    if ids.ndim != 1:
+        raise ValueError("token sequence must be one-dimensional")
+    n = ids.shape[0]
+    if n < 2:
+        raise DegenerateInputError(f"need at least 2 tokens, got {n}")
+    if n > config.max_seq:
+        raise ValueError(f"sequence length {n} exceeds max_seq {config.max_seq}")
+    if ids.min() < 0 or ids.max() >= config.vocab_size:
+        raise ValueError("token id out of vocabulary range")
+    return np.ascontiguousarray(ids)
+
+
+def make_synthetic_dataset(seed: int, size: int, length: int, vocab_size: int) -> list[np.ndarray]:
+    """model.py:455-458."""
+    rng = np.random.default_rng(seed)
+    return [rng.integers(0, vocab_size, size=length, dtype=np.int64) for _ in range(size)]
+
+
+# ---------------------------------------------------------------------------
+# Caches
+# ---------------------------------------------------------------------------
+
+
+@dataclass(eq=False)
+class LayerKV:
+    """Dense per-layer K/V, [L, n_kv_heads, positions, head_dim] bf16 on device
+    (the reference LayerKV layout, model.py:342-370; the producer export)."""
+
+    k: torch.Tensor
+    v: torch.Tensor
+
+    def __post_init__(self) -> None:
+        if self.k.shape != self.v.shape or self.k.dim() != 4:
+            raise ValueError(f"inconsistent KV shapes {tuple(self.k.shape)} / {tuple(self.v.shape)}")
+
+    @property
+    def n_layers(self) -> int:
+        return self.k.shape[0]
+
+    @property
+    def positions(self) -> int:
+        return self.k.shape[2]
+
+    def layer_bytes(self, layer: int) -> int:
+        return int(self.k[layer].nbytes + self.v[layer].nbytes)
+
+    def desc(self) -> L.KvCache:
+        Ln, G, n, D = self.k.shape
+        assert self.k.is_contiguous() and self.v.is_contiguous()
+        return L.KvCache(self.k.data_ptr(), self.v.data_ptr(), G * n * D, n * D, PAGE * D, None, Ln, n)
+
+    @classmethod
+    def empty(cls, config: ModelConfig, positions: int, device="cuda") -> "LayerKV":
+        shape = (config.n_layers, config.n_kv_heads, positions, config.head_dim)
+        return cls(torch.empty(shape, dtype=torch.bfloat16, device=device),
+                   torch.empty(shape, dtype=torch.bfloat16, device=device))
+
+
+@dataclass(eq=False)
+class PagedKV:
+    """Consumer paged cache: [L, pages, n_kv_heads, 64, head_dim] bf16 + int32
+    block table (position p lives in page table[p // 64], slot p % 64).  Each
+    (layer, page, head) is one contiguous 64 x D block, the ingest/attention unit."""
+
+    k: torch.Tensor
+    v: torch.Tensor
+    table: torch.Tensor
+    positions: int
+
+    @property
+    def n_layers(self) -> int:
+        return self.k.shape[0]
+
+    def desc(self) -> L.KvCache:
+        Ln, pages, G, ps, D = self.k.shape
+        return L.KvCache(self.k.data_ptr(), self.v.data_ptr(), pages * G * PAGE * D, PAGE * D, G * PAGE * D,
+                         self.table.data_ptr(), Ln, self.positions)
+
+    @classmethod
+    def allocate(cls, config: ModelConfig, positions: int, device="cuda", spare_pages: int = 0,
+                 shuffle_seed: int | None = None) -> "PagedKV":
+        need = (positions + PAGE - 1) // PAGE
+        pages = need + spare_pages
+        shape = (config.n_layers, pages, config.n_kv_heads, PAGE, config.head_dim)
+        if shuffle_seed is None:
+            table = torch.arange(need, dtype=torch.int32, device=device)
+        else:
+            g = torch.Generator().manual_seed(shuffle_seed)
+            table = torch.randperm(pages, generator=g)[:need].to(torch.int32).to(device)
+        return cls(torch.empty(shape, dtype=torch.bfloat16, device=device),
+                   torch.empty(shape, dtype=torch.bfloat16, device=device), table, positions)
+
+    def dense(self) -> LayerKV:
+        """Gather into the reference [L, KVH, n, D] layout (tests / export)."""
+        idx = self.table.long()
+        Ln, _, G, _, D = self.k.shape
+        k = self.k[:, idx].permute(0, 2, 1, 3, 4).reshape(Ln, G, -1, D)[:, :, :self.positions]
+        v = self.v[:, idx].permute(0, 2, 1, 3, 4).reshape(Ln, G, -1, D)[:, :, :self.positions]
+        return LayerKV(k.contiguous(), v.contiguous())
+
+
+@dataclass(eq=False)
+class ECache:
+    """Residual-stream input of one layer over the window, bf16 [positions, d_model]
+    (model.py:373-391)."""
+
+    layer: int
+    hidden: torch.Tensor
+
+    def __post_init__(self) -> None:
+        if self.hidden.dim() != 2:
+            raise ValueError(f"E cache must be 2-D, got shape {tuple(self.hidden.shape)}")
+
+    @property
+    def positions(self) -> int:
+        return self.hidden.shape[0]
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.hidden.nbytes)
+
+
+@dataclass(eq=False)
+class PrefillResult:
+    kv: LayerKV
+    e_caches: tuple
+    logits: torch.Tensor       # f32 [V] on device
+    token_dev: torch.Tensor    # int32 [1] greedy first token on device
+
+    def e_map(self) -> dict:
+        return {e.layer: e for e in self.e_caches}
+
+    @property
+    def token(self) -> int:
+        return int(self.token_dev.item())
+
+
+@dataclass(eq=False)
+class MixedPrefill:
+    kv: PagedKV
+    logits: torch.Tensor
+    token_dev: torch.Tensor
+
+    @property
+    def token(self) -> int:
+        return int(self.token_dev.item())
+
+
+# ---------------------------------------------------------------------------
+# Workspace
+# ---------------------------------------------------------------------------
+
+_WS: dict = {}
+
+
+def workspace_bytes(config: ModelConfig, n_tokens: int) -> int:
+    dims = L.Dims(config.n_layers, config.d_model, config.n_heads, config.n_kv_heads, config.head_dim,
+                  config.d_ff, config.vocab_size, config.max_seq)
+    return int(L.lib().ds_workspace_size(C.byref(dims), n_tokens))
+
+
+def _workspace(model: ModelWeights, n: int) -> torch.Tensor:
+    need = workspace_bytes(model.config, n)
+    key = (model.device, id(model.config))
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=model.device)
+        _WS[key] = ws
+    return ws
+
+
+def _normalize_e(sender_e) -> dict:
+    if sender_e is None:
+        return {}
+    if isinstance(sender_e, Mapping):
+        return dict(sender_e)
+    return {e.layer: e for e in sender_e}
+
+
+# ---------------------------------------------------------------------------
+# Entry points
+# ---------------------------------------------------------------------------
+
+
+def full_prefill(model: ModelWeights, tokens, e_layers: Iterable[int] | None = None, *, out: LayerKV | None = None,
+                 stream=None, tokens_dev: torch.Tensor | None = None) -> PrefillResult:
+    """Producer export: K/V at every layer over all n positions, E over the
+    window (n-1 rows) at ``e_layers`` (default: every layer, profiling mode;
+    pass the transition layers for the serving-mode filter, store.py:202-203),
+    and first-token logits."""
+    cfg = model.config
+    ids = check_tokens(tokens, cfg)
+    n = ids.shape[0]
+    layers = list(range(cfg.n_layers)) if e_layers is None else sorted(set(int(l) for l in e_layers))
+    kv = out if out is not None else LayerKV.empty(cfg, n, model.device)
+    e_bufs = [torch.empty(n - 1, cfg.d_model, dtype=torch.bfloat16, device=model.device) for _ in layers]
+    logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=model.device)
+    tok = torch.empty(1, dtype=torch.int32, device=model.device)
+    ws = _workspace(model, n)
+    s = stream if stream is not None else torch.cuda.current_stream(model.device)
+    la = (C.c_int32 * max(1, len(layers)))(*layers)
+    ptrs = (C.c_void_p * max(1, len(layers)))(*[b.data_ptr() for b in e_bufs])
+    desc = kv.desc()
+    rc = L.lib().ds_full_prefill(C.byref(model.desc()), ids.ctypes.data,
+                                 tokens_dev.data_ptr() if tokens_dev is not None else None, n, C.byref(desc), la,
+                                 len(layers), ptrs, logits.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel(),
+                                 s.cuda_stream)
+    L.check(rc)
+    return PrefillResult(kv=kv, e_caches=tuple(ECache(l, b) for l, b in zip(layers, e_bufs)), logits=logits,
+                         token_dev=tok)
+
+
+def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sender_kv: LayerKV | None,
+                    sender_e: Mapping[int, ECache] | Iterable[ECache] | None = None, *, out: PagedKV | None = None,
+                    stream=None, copy_stream=None, tokens_dev: torch.Tensor | None = None) -> MixedPrefill:
+    """Consumer partial prefill (model.py:660-679): ingest the sender's K/V at
+    reused layers, recompute each group over the window from embeddings (a=0)
+    or the sender's E at its transition layer, run the anchor position through
+    every layer, and produce first-token logits.  ``copy_stream`` runs the
+    ingest concurrently with the recompute (pipelined plan, sched.py:212-263)."""
+    cfg = receiver.config
+    ids = check_tokens(tokens, cfg)
+    config.validate_for(cfg.n_layers)
+    n = ids.shape[0]
+    e_map = _normalize_e(sender_e)
+    cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
+    logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
+    tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
+    ws = _workspace(receiver, n)
+    s = stream if stream is not None else torch.cuda.current_stream(receiver.device)
+    groups = [x for g in config.groups for x in g]
+    ga = (C.c_int32 * max(1, len(groups)))(*groups)
+    e_list = [L.ECacheDesc(l, e.positions, e.hidden.shape[1], e.hidden.data_ptr())
+              for l, e in sorted(e_map.items()) if e.hidden.dtype == torch.bfloat16 and e.hidden.is_cuda
+              and e.hidden.is_contiguous()]
+    ea = (L.ECacheDesc * max(1, len(e_list)))(*e_list)
+    skv = sender_kv.desc() if sender_kv is not None else None
+    odesc = cache.desc()
+    ml, mk = C.c_int32(-1), C.c_int32(0)
+    rc = L.lib().ds_partial_prefill(
+        C.byref(receiver.desc()), ids.ctypes.data, tokens_dev.data_ptr() if tokens_dev is not None else None, n, ga,
+        len(config.groups), C.byref(skv) if skv is not None else None, ea, len(e_list), C.byref(odesc),
+        logits.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream,
+        copy_stream.cuda_stream if copy_stream is not None else None, C.byref(ml), C.byref(mk))
+    L.check(rc, ml.value, mk.value)
+    return MixedPrefill(kv=cache, logits=logits, token_dev=tok)
