@@ -88,6 +88,8 @@ typedef struct ds_e_cache {
 
 DS_API int ds_abi_version(void);
 DS_API const char* ds_last_error(void);
+/* Kernels this library has launched in this process (benchmark evidence). */
+DS_API unsigned long long ds_launch_count(void);
 
 /* Bytes of device workspace ds_partial_prefill / ds_full_prefill need for n tokens. */
 DS_API size_t ds_workspace_size(const ds_dims* dims, int32_t n_tokens);

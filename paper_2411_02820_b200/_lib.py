@@ -60,6 +60,7 @@ def lib() -> C.CDLL:
         sig = {
             "ds_abi_version": (I32, []),
             "ds_last_error": (C.c_char_p, []),
+            "ds_launch_count": (C.c_uint64, []),
             "ds_workspace_size": (SZ, [C.POINTER(Dims), I32]),
             "ds_kv_ingest": (I32, [C.POINTER(KvCache), C.POINTER(KvCache), P, I32, I32, I32, I32, P,
                                    C.POINTER(I32)]),
@@ -95,5 +96,5 @@ def check(rc: int, miss_layer: int | None = None, miss_kind: int | None = None) 
     raise RuntimeError(f"droidspeak CUDA error: {msg}")
 
 
-EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_workspace_size", "ds_kv_ingest", "ds_partial_prefill",
+EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_launch_count", "ds_workspace_size", "ds_kv_ingest", "ds_partial_prefill",
                     "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill")

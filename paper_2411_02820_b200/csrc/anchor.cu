@@ -189,11 +189,13 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
       return DS_ERR_CUDA;
     attr = smem;
   }
+  count_launch();
   gemv_kernel<<<grid, GEMV_THREADS, smem, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, cudaStream_t stream) {
+  count_launch();
   argmax_finalize_kernel<<<1, 1, 0, stream>>>(packed, token);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
@@ -337,6 +339,7 @@ int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_la
   DecArgs a{q, k_layer, v_layer, head_stride, page_stride, table, n_keys, n_heads, n_kv_heads, head_dim,
             part_o, part_ml, (float)(1.4426950408889634 / sqrt((double)head_dim))};
   const int splits = decode_splits(n_keys);
+  count_launch(2);
   decode_attn_kernel<<<dim3(n_kv_heads, splits), DEC_THREADS, 0, stream>>>(a);
   decode_combine_kernel<<<n_heads, head_dim, 0, stream>>>(part_o, part_ml, splits, n_heads, head_dim, out);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;

@@ -14,6 +14,10 @@
 
 using namespace ds;
 
+namespace ds {
+unsigned long long g_launches = 0;
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -279,6 +283,7 @@ int check_cache(const ds_kv_cache* c, const ds_dims& d, int n, const char* what)
 extern "C" {
 
 int ds_abi_version(void) { return DS_ABI_VERSION; }
+unsigned long long ds_launch_count(void) { return __atomic_load_n(&ds::g_launches, __ATOMIC_RELAXED); }
 const char* ds_last_error(void) { return g_err.c_str(); }
 
 size_t ds_workspace_size(const ds_dims* dims, int32_t n_tokens) {
@@ -413,18 +418,11 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
   Ctx c{m, d, w, out_kv, cs};
 
   // ---- ingest (copy stream) overlapping recompute (compute stream)
-  struct Events {
-    cudaEvent_t fork = nullptr, join = nullptr;
-    ~Events() {
-      if (fork) cudaEventDestroy(fork);
-      if (join) cudaEventDestroy(join);
-    }
-  } ev;
-  cudaEvent_t& ev_fork = ev.fork;
-  cudaEvent_t& ev_join = ev.join;
+  // fork/join events, created once per host thread (capturable into CUDA graphs)
+  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   if (xs != cs) {
-    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+    if (!ev_fork && (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess))
       return cuda_fail("event");
     cudaEventRecord(ev_fork, cs);
     cudaStreamWaitEvent(xs, ev_fork, 0);

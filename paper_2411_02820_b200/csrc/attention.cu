@@ -251,6 +251,7 @@ int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, 
   FaArgs a{q, ldq, o, ldo, k_layer, v_layer, head_stride, page_stride, table, n_q, q_pos0, n_heads, n_kv_heads,
            (float)(1.4426950408889634 / sqrt((double)head_dim))};
   dim3 grid(n_heads, (n_q + 63) / 64);
+  count_launch();
   if (head_dim == 128) {
     const int smem = 5 * 64 * 128 * 2;
     static bool set = false;

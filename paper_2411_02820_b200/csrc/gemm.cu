@@ -312,6 +312,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
   const int tiles = ((epi.M + GEMM_BM - 1) / GEMM_BM) * ((epi.N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  count_launch();
   kern<<<grid, GEMM_THREADS, L::TOTAL, stream>>>(ta, tb, K, epi);
   return cudaGetLastError();
 }

@@ -123,6 +123,7 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   if (per_sm > 8) per_sm = 8;
   long long grid = (long long)num_sms() * per_sm;
   if (grid > total) grid = total;
+  count_launch();
   kv_ingest_kernel<<<(int)grid, 32, smem, stream>>>(a, (int)total, stage_bytes);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }

@@ -31,6 +31,10 @@ struct GemmEpi {
   const float* rope_sin;
 };
 
+// Every kernel launch of this library bumps this counter (ds_launch_count()).
+extern unsigned long long g_launches;
+inline void count_launch(int n = 1) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld, int box_rows,
                    int box_cols);
 int num_sms();

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, co
 int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,
                    float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream) {
   if (M <= 0) return DS_OK;
+  count_launch();
   if (x_bf16)
     rmsnorm_kernel<true><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
   else
