@@ -74,8 +74,14 @@ typedef struct ds_kv_cache {
   void* v;                    /* bf16 */
   int64_t layer_stride, head_stride, page_stride;
   const int32_t* block_table; /* device int32 [ceil(positions/64)] or NULL (identity) */
-  int32_t n_layers;           /* layers present */
+  int32_t n_layers;           /* layers addressable */
   int32_t positions;          /* positions present per layer */
+  /* Optional HOST arrays [n_layers] of per-layer K / V bases (replacing
+   * k/v + layer*layer_stride); a NULL entry means the layer is absent (a
+   * cache miss).  Used for per-layer store payloads (store.py:351-395) that
+   * the ingest kernel reads in place — including peer-GPU memory. */
+  void* const* layer_k;
+  void* const* layer_v;
 } ds_kv_cache;
 
 /* ECache (model.py:373-391): residual-stream input of `layer`, bf16 [positions][width]. */

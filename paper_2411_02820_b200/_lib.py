@@ -38,7 +38,7 @@ class Model(C.Structure):
 class KvCache(C.Structure):
     _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("layer_stride", C.c_int64), ("head_stride", C.c_int64),
                 ("page_stride", C.c_int64), ("block_table", C.c_void_p), ("n_layers", C.c_int32),
-                ("positions", C.c_int32)]
+                ("positions", C.c_int32), ("layer_k", C.POINTER(C.c_void_p)), ("layer_v", C.POINTER(C.c_void_p))]
 
 
 class ECacheDesc(C.Structure):

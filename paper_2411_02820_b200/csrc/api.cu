@@ -119,8 +119,8 @@ int check_tokens(const ds_dims& d, const int64_t* tokens, int n) {
 
 KvAddr layer_addr(const ds_kv_cache& c, int layer, int head_dim) {
   KvAddr a;
-  a.k = static_cast<bf16*>(c.k) + (long long)layer * c.layer_stride;
-  a.v = static_cast<bf16*>(c.v) + (long long)layer * c.layer_stride;
+  a.k = kv_layer_base(c, layer, false);
+  a.v = kv_layer_base(c, layer, true);
   a.head_stride = c.head_stride;
   a.page_stride = c.page_stride;
   a.table = c.block_table;
@@ -271,7 +271,7 @@ const int64_t* stage_tokens(const int64_t* host, const int64_t* dev, int n, Work
 }
 
 int check_cache(const ds_kv_cache* c, const ds_dims& d, int n, const char* what) {
-  if (!c || !c->k || !c->v) return fail(DS_ERR_INVALID, "%s cache is NULL", what);
+  if (!c || ((!c->k || !c->v) && !(c->layer_k && c->layer_v))) return fail(DS_ERR_INVALID, "%s cache is NULL", what);
   if (c->n_layers < d.n_layers || c->positions < n)
     return fail(DS_ERR_INVALID, "%s cache holds %d layers x %d positions, need %d x %d", what, c->n_layers,
                 c->positions, d.n_layers, n);
@@ -301,7 +301,7 @@ int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const int32_t* 
   for (int i = 0; i < n_reused; ++i) {
     const int l = reused[i];
     if (i && reused[i - 1] >= l) return fail(DS_ERR_INVALID, "reused layers must ascend");
-    if (!src || src->n_layers <= l || src->positions < window) {
+    if (!src || !kv_layer_present(*src, l) || src->positions < window) {
       if (miss_layer) *miss_layer = l;
       return fail(DS_ERR_CACHE_MISS, "missing kv cache for layer %d", l);
     }
@@ -386,7 +386,7 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
   std::vector<int32_t> reused;
   for (int l = 0; l < L; ++l) {
     if (covered[l]) continue;
-    if (!sender_kv || !sender_kv->k || sender_kv->n_layers <= l || sender_kv->positions < P) {
+    if (!sender_kv || !kv_layer_present(*sender_kv, l) || sender_kv->positions < P) {
       if (miss_layer) *miss_layer = l;
       if (miss_kind) *miss_kind = DS_MISS_KV;
       return fail(DS_ERR_CACHE_MISS, "missing kv cache for layer %d", l);

@@ -16,16 +16,17 @@ namespace ds {
 
 constexpr int INGEST_STAGES = 4;
 
+// Per-(reused layer) K/V bases travel by value (graph-capturable, 4 KB of
+// kernel parameters); they may point into a peer GPU's HBM (P2P pull).
 struct IngestArgs {
-  const uint8_t* src_k;
-  const uint8_t* src_v;
-  uint8_t* dst_k;
-  uint8_t* dst_v;
-  long long src_layer_stride, src_head_stride, src_page_stride;  // bytes
-  long long dst_layer_stride, dst_head_stride, dst_page_stride;  // bytes
+  const uint8_t* src_k[kMaxLayers];
+  const uint8_t* src_v[kMaxLayers];
+  uint8_t* dst_k[kMaxLayers];
+  uint8_t* dst_v[kMaxLayers];
+  long long src_head_stride, src_page_stride;  // bytes
+  long long dst_head_stride, dst_page_stride;  // bytes
   const int32_t* src_table;
   const int32_t* dst_table;
-  int32_t layers[kMaxLayers];  // reused layers, by value (graph-capturable)
   int n_layers, n_kv_heads, head_dim, window, n_pages;
 };
 
@@ -37,13 +38,12 @@ DS_DEV void ingest_unit(const IngestArgs& a, int u, const uint8_t*& src, uint8_t
   t /= a.n_kv_heads;
   int kv = t & 1;
   int li = t >> 1;
-  int layer = a.layers[li];
   int rows = min(kPage, a.window - p * kPage);
   bytes = (uint32_t)rows * a.head_dim * 2;
   int sp = a.src_table ? __ldg(a.src_table + p) : p;
   int dp = a.dst_table ? __ldg(a.dst_table + p) : p;
-  src = (kv ? a.src_v : a.src_k) + layer * a.src_layer_stride + h * a.src_head_stride + sp * a.src_page_stride;
-  dst = (kv ? a.dst_v : a.dst_k) + layer * a.dst_layer_stride + h * a.dst_head_stride + dp * a.dst_page_stride;
+  src = (kv ? a.src_v[li] : a.src_k[li]) + h * a.src_head_stride + sp * a.src_page_stride;
+  dst = (kv ? a.dst_v[li] : a.dst_k[li]) + h * a.dst_head_stride + dp * a.dst_page_stride;
 }
 
 __global__ void __launch_bounds__(32) kv_ingest_kernel(const __grid_constant__ IngestArgs a, int total_units, int stage_bytes) {
@@ -89,20 +89,20 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
                      int n_kv_heads, int head_dim, int window, cudaStream_t stream) {
   if (n_layers <= 0 || window <= 0) return DS_OK;
   IngestArgs a;
-  a.src_k = static_cast<const uint8_t*>(src.k);
-  a.src_v = static_cast<const uint8_t*>(src.v);
-  a.dst_k = static_cast<uint8_t*>(dst.k);
-  a.dst_v = static_cast<uint8_t*>(dst.v);
-  a.src_layer_stride = src.layer_stride * 2;
   a.src_head_stride = src.head_stride * 2;
   a.src_page_stride = src.page_stride * 2;
-  a.dst_layer_stride = dst.layer_stride * 2;
   a.dst_head_stride = dst.head_stride * 2;
   a.dst_page_stride = dst.page_stride * 2;
   a.src_table = src.block_table;
   a.dst_table = dst.block_table;
   if (n_layers > kMaxLayers) return DS_ERR_INVALID;
-  for (int i = 0; i < n_layers; ++i) a.layers[i] = layers_host[i];
+  for (int i = 0; i < n_layers; ++i) {
+    const int l = layers_host[i];
+    a.src_k[i] = reinterpret_cast<const uint8_t*>(kv_layer_base(src, l, false));
+    a.src_v[i] = reinterpret_cast<const uint8_t*>(kv_layer_base(src, l, true));
+    a.dst_k[i] = reinterpret_cast<uint8_t*>(kv_layer_base(dst, l, false));
+    a.dst_v[i] = reinterpret_cast<uint8_t*>(kv_layer_base(dst, l, true));
+  }
   a.n_layers = n_layers;
   a.n_kv_heads = n_kv_heads;
   a.head_dim = head_dim;

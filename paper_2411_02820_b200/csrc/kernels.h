@@ -31,6 +31,17 @@ struct GemmEpi {
   const float* rope_sin;
 };
 
+// Base of layer `layer`'s K (v = false) or V block in a cache descriptor:
+// the per-layer pointer table when present, else base + layer * layer_stride.
+inline bf16* kv_layer_base(const ds_kv_cache& c, int layer, bool v) {
+  void* const* tab = v ? c.layer_v : c.layer_k;
+  if (tab) return static_cast<bf16*>(tab[layer]);
+  return static_cast<bf16*>(v ? c.v : c.k) + (long long)layer * c.layer_stride;
+}
+inline bool kv_layer_present(const ds_kv_cache& c, int layer) {
+  return layer >= 0 && layer < c.n_layers && kv_layer_base(c, layer, false) && kv_layer_base(c, layer, true);
+}
+
 // Every kernel launch of this library bumps this counter (ds_launch_count()).
 extern unsigned long long g_launches;
 inline void count_launch(int n = 1) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }

@@ -1,0 +1,65 @@
+"""The C-ABI library loads and exports every entry point include/*.h declares (CPU, no compute calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from conftest import ROOT
+
+HEADERS = sorted((ROOT / "include").glob("*.h"))
+
+
+def declared():
+    names = []
+    for h in HEADERS:
+        text = h.read_text()
+        names += re.findall(r"DS_API\s+[\w\s\*]+?\b(ds_\w+)\s*\(", text)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2411_02820_b200 import _lib
+    if not _lib.LIB_PATH.exists():
+        from paper_2411_02820_b200 import _build
+        _build.build()
+    return _lib
+
+
+def test_headers_declare_entry_points():
+    names = declared()
+    for must in ("ds_kv_ingest", "ds_partial_prefill", "ds_full_prefill", "ds_recompute_group", "ds_anchor",
+                 "ds_workspace_size", "ds_last_error", "ds_abi_version"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    h = ctypes.CDLL(str(lib.LIB_PATH))
+    missing = [n for n in declared() if not hasattr(h, n)]
+    assert not missing, missing
+    # the Python binding covers the same set
+    assert sorted(lib.EXPORTED_SYMBOLS) == declared()
+
+
+def test_host_only_entry_points(lib):
+    L = lib.lib()
+    assert L.ds_abi_version() == 1
+    dims = lib.Dims(32, 4096, 32, 8, 128, 14336, 128256, 8192)
+    assert L.ds_workspace_size(ctypes.byref(dims), 8192) > 8192 * 4096 * 4
+    assert L.ds_workspace_size(None, 8) == 0
+    # argument validation happens before any device work and maps to ValueError
+    rc = L.ds_kv_ingest(None, None, None, 0, 0, 8, 128, None, None)
+    assert rc == lib.DS_ERR_INVALID
+    with pytest.raises(ValueError):
+        lib.check(rc)
+    assert b"ingest" in L.ds_last_error()
+
+
+def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
+    from paper_2411_02820_b200 import _lib
+    monkeypatch.setattr(_lib, "LIB_PATH", tmp_path / "absent.so")
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(RuntimeError, match="not built"):
+        _lib.lib()
