@@ -133,6 +133,27 @@ DS_API int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const 
                     float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes,
                     void* stream);
 
+/* ---- stage entry points (the layer-pipelined scheduler drives these on its own
+ * streams: ingest on the link stream, recompute gated on E, anchor last;
+ * sched.py:212-263) ---- */
+
+/* Selective recompute of ONE group [a, b] over the window positions 0..n-2
+ * (model.py:607-625): h = embed[tokens[0..n-1)] (a == 0, tokens_dev required)
+ * or the sender's E at layer a (seed: bf16 [seed_positions >= n-1][d], may live
+ * in a peer GPU's HBM); layers a..b run over the window and write K/V of
+ * positions 0..n-2 into out_kv.  The E read is the first kernel of the group, so
+ * a peer-resident seed is pulled over NVLink by the compute itself. */
+DS_API int ds_recompute_group(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, int32_t a, int32_t b,
+                              const void* seed, int32_t seed_positions, const ds_kv_cache* out_kv, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/* Anchor pass (model.py:627-637): position n-1 through every layer with the
+ * receiver's weights, attending over kv[l, :, 0..n-2] plus itself (its K/V are
+ * written at n-1), then logits = RMSNorm(h)*g_final @ unembed and the greedy
+ * token (lowest id on ties, model.py:779). */
+DS_API int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, const ds_kv_cache* kv,
+                     float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- single-kernel entry points (used by the parity tests and the scheduler) ---- */
 
 /* C = epilogue(A[M][K] . B[N][K]^T); mode 0 bf16 store, 1 f32 out = resid + acc,

@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
                                          C.POINTER(ECacheDesc), I32, C.POINTER(KvCache), P, P, P, SZ, P, P,
                                          C.POINTER(I32), C.POINTER(I32)]),
             "ds_full_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), P, I32, P, P, P, P, SZ, P]),
+            "ds_recompute_group": (I32, [C.POINTER(Model), P, I32, I32, I32, P, I32, C.POINTER(KvCache), P, SZ, P]),
+            "ds_anchor": (I32, [C.POINTER(Model), P, I32, C.POINTER(KvCache), P, P, P, SZ, P]),
             "ds_gemm": (I32, [P, I64, P, I64, P, I64, P, I64, I32, I32, I32, I32, P]),
             "ds_rmsnorm": (I32, [P, I32, P, I32, I32, P, P, P, P, P]),
             "ds_attention_prefill": (I32, [P, I64, C.POINTER(KvCache), I32, I32, I32, I32, I32, I32, P, I64, P]),
@@ -97,4 +99,5 @@ def check(rc: int, miss_layer: int | None = None, miss_kind: int | None = None) 
 
 
 EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_launch_count", "ds_workspace_size", "ds_kv_ingest", "ds_partial_prefill",
-                    "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill")
+                    "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill", "ds_recompute_group",
+                    "ds_anchor")

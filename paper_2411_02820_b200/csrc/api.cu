@@ -264,6 +264,40 @@ int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token) {
   return DS_OK;
 }
 
+// One recompute group [a,b] over the window rows 0..P-1 (model.py:607-625):
+// seed h from the token embeddings (a == 0) or the sender's E at layer a.
+int recompute_group(Ctx& c, const int64_t* tok, int P, int a, int b, const void* seed) {
+  const ds_dims& d = c.d;
+  const ds_layer_weights& Wa = c.m->layers[a];
+  if (a == 0)
+    DS_TRY(rmsnorm_launch(c.m->embed, true, tok, P, d.d_model, Wa.g_attn, c.w.a, c.w.h, nullptr, P, c.s), "seed");
+  else
+    DS_TRY(rmsnorm_launch(seed, true, nullptr, P, d.d_model, Wa.g_attn, c.w.a, c.w.h, nullptr, P, c.s), "seed");
+  for (int l = a; l <= b; ++l) {
+    if (l > a)
+      DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, P, d.d_model, c.m->layers[l].g_attn, c.w.a, nullptr, nullptr, 0,
+                            c.s),
+             "rmsnorm");
+    int rc = window_layer(c, l, P, l == b);
+    if (rc) return rc;
+  }
+  return DS_OK;
+}
+
+// The anchor position P through every layer, then logits + greedy token
+// (model.py:627-637).
+int anchor_pass(Ctx& c, const int64_t* tok, int P, float* logits, int32_t* token) {
+  const ds_dims& d = c.d;
+  DS_TRY(rmsnorm_launch(c.m->embed, true, tok + P, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr, 1,
+                        c.s),
+         "anchor seed");
+  for (int l = 0; l < d.n_layers; ++l) {
+    int rc = anchor_layer(c, l, P, c.w.h_a);
+    if (rc) return rc;
+  }
+  return lm_head(c, c.w.h_a, logits, token);
+}
+
 const int64_t* stage_tokens(const int64_t* host, const int64_t* dev, int n, Workspace& w, cudaStream_t s) {
   if (dev) return dev;
   if (cudaMemcpyAsync(w.tokens, host, 8ull * n, cudaMemcpyHostToDevice, s) != cudaSuccess) return nullptr;
@@ -434,31 +468,53 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
 
   // ---- selective recompute of each group over the window
   for (int i = 0; i < n_groups; ++i) {
-    const int a = groups[2 * i], b = groups[2 * i + 1];
-    const ds_layer_weights& Wa = m->layers[a];
-    if (a == 0)
-      DS_TRY(rmsnorm_launch(m->embed, true, tok, P, d.d_model, Wa.g_attn, w.a, w.h, nullptr, P, cs), "seed");
-    else
-      DS_TRY(rmsnorm_launch(seed[i]->hidden, true, nullptr, P, d.d_model, Wa.g_attn, w.a, w.h, nullptr, P, cs),
-             "seed");
-    for (int l = a; l <= b; ++l) {
-      if (l > a)
-        DS_TRY(rmsnorm_launch(w.h, false, nullptr, P, d.d_model, m->layers[l].g_attn, w.a, nullptr, nullptr, 0, cs),
-               "rmsnorm");
-      rc = window_layer(c, l, P, l == b);
-      if (rc) return rc;
-    }
+    rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
+    if (rc) return rc;
   }
 
   // ---- anchor pass after all KV has landed (sched.py:256)
   if (xs != cs) cudaStreamWaitEvent(cs, ev_join, 0);
-  DS_TRY(rmsnorm_launch(m->embed, true, tok + P, 1, d.d_model, m->layers[0].g_attn, w.a_a, w.h_a, nullptr, 1, cs),
-         "anchor seed");
-  for (int l = 0; l < L; ++l) {
-    rc = anchor_layer(c, l, P, w.h_a);
-    if (rc) return rc;
-  }
-  return lm_head(c, w.h_a, logits_out, token_out);
+  return anchor_pass(c, tok, P, logits_out, token_out);
+}
+
+int ds_recompute_group(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, int32_t a, int32_t b,
+                       const void* seed, int32_t seed_positions, const ds_kv_cache* out_kv, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if (n_tokens < 2) return fail(DS_ERR_DEGENERATE, "need at least 2 tokens, got %d", n_tokens);
+  if (n_tokens > d.max_seq) return fail(DS_ERR_INVALID, "sequence length %d exceeds max_seq %d", n_tokens, d.max_seq);
+  if (a < 0 || a > b || b >= d.n_layers) return fail(DS_ERR_INVALID, "range [%d,%d] invalid for %d layers", a, b, d.n_layers);
+  const int P = n_tokens - 1;
+  if (a == 0 && !tokens_dev) return fail(DS_ERR_INVALID, "tokens_dev required for a group starting at layer 0");
+  if (a > 0 && (!seed || seed_positions < P)) return fail(DS_ERR_CACHE_MISS, "missing e cache for layer %d", a);
+  if ((rc = check_cache(out_kv, d, n_tokens, "output"))) return rc;
+  Workspace w = carve(d, n_tokens, workspace);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
+  Ctx c{m, d, w, out_kv, (cudaStream_t)stream};
+  return recompute_group(c, tokens_dev, P, a, b, a > 0 ? seed : nullptr);
+}
+
+int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, const ds_kv_cache* kv,
+              float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if (n_tokens < 2) return fail(DS_ERR_DEGENERATE, "need at least 2 tokens, got %d", n_tokens);
+  if (n_tokens > d.max_seq) return fail(DS_ERR_INVALID, "sequence length %d exceeds max_seq %d", n_tokens, d.max_seq);
+  if (!tokens_dev || !logits_out) return fail(DS_ERR_INVALID, "tokens_dev and logits_out are required");
+  if ((rc = check_cache(kv, d, n_tokens, "cache"))) return rc;
+  Workspace w = carve(d, n_tokens, workspace);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
+  Ctx c{m, d, w, kv, (cudaStream_t)stream};
+  return anchor_pass(c, tokens_dev, n_tokens - 1, logits_out, token_out);
 }
 
 int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
