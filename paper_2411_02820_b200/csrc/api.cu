@@ -63,6 +63,7 @@ struct Workspace {
   float* part_o;
   float* part_ml;
   unsigned long long* argmax;
+  unsigned int* dec_count;  // [n_kv_heads] split-merge counters (zero between launches)
   size_t bytes;
 };
 
@@ -91,6 +92,7 @@ Workspace carve(const ds_dims& m, int n, void* base) {
   w.part_o = reinterpret_cast<float*>(take(4ull * splits * hd));
   w.part_ml = reinterpret_cast<float*>(take(8ull * splits * m.n_heads));
   w.argmax = reinterpret_cast<unsigned long long*>(take(8));
+  w.dec_count = reinterpret_cast<unsigned int*>(take(4ull * m.n_kv_heads));
   w.bytes = off;
   return w;
 }
@@ -128,6 +130,13 @@ KvAddr layer_addr(const ds_kv_cache& c, int layer, int head_dim) {
   return a;
 }
 
+// Rows of one cache layer viewed as a [rows][head_dim] matrix (the TMA bound).
+long long layer_rows(const ds_kv_cache& c, int n_kv_heads, int head_dim) {
+  if (c.layer_stride > 0) return c.layer_stride / head_dim;
+  const long long pages = (c.positions + kPage - 1) / kPage;
+  return ((n_kv_heads - 1) * c.head_stride + pages * c.page_stride) / head_dim;
+}
+
 struct Ctx {
   const ds_model* m;
   const ds_dims& d;
@@ -161,7 +170,8 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only) {
   DS_TRY(gemm_launch(c.w.a, d.d_model, wqkv, d.d_model, d.d_model, e, c.s), "qkv gemm");
   if (kv_only) return DS_OK;
   const KvAddr ka = layer_addr(*c.kv, l, d.head_dim);
-  DS_TRY(attention_prefill_launch(c.w.q, hd, ka.k, ka.v, ka.head_stride, ka.page_stride, ka.table, rows, 0,
+  DS_TRY(attention_prefill_launch(c.w.q, hd, ka.k, ka.v, ka.head_stride, ka.page_stride,
+                                  layer_rows(*c.kv, d.n_kv_heads, d.head_dim), ka.table, rows, 0,
                                   d.n_heads, d.n_kv_heads, d.head_dim, c.w.o, hd, c.s),
          "attention");
   GemmEpi r{};
@@ -210,7 +220,8 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a) {
   DS_TRY(gemv_launch(g, c.s), "anchor qkv");
   const KvAddr ka = g.kv;
   DS_TRY(decode_attention_launch(c.w.q_a, ka.k, ka.v, ka.head_stride, ka.page_stride, ka.table, pos + 1,
-                                 d.n_heads, d.n_kv_heads, d.head_dim, c.w.part_o, c.w.part_ml, c.w.o_a, c.s),
+                                 d.n_heads, d.n_kv_heads, d.head_dim, c.w.part_o, c.w.part_ml, c.w.dec_count, c.w.o_a,
+                                 c.s),
          "anchor attention");
   GemvArgs o{};
   o.W = static_cast<const bf16*>(W.wo);
@@ -286,8 +297,14 @@ int recompute_group(Ctx& c, const int64_t* tok, int P, int a, int b, const void*
 
 // The anchor position P through every layer, then logits + greedy token
 // (model.py:627-637).
+int reset_counters(Ctx& c) {
+  if (cudaMemsetAsync(c.w.dec_count, 0, 4ull * c.d.n_kv_heads, c.s) != cudaSuccess) return cuda_fail("memset");
+  return DS_OK;
+}
+
 int anchor_pass(Ctx& c, const int64_t* tok, int P, float* logits, int32_t* token) {
   const ds_dims& d = c.d;
+  if (int rc = reset_counters(c)) return rc;
   DS_TRY(rmsnorm_launch(c.m->embed, true, tok + P, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr, 1,
                         c.s),
          "anchor seed");
@@ -384,7 +401,8 @@ int ds_attention_prefill(const void* q, int64_t ldq, const ds_kv_cache* kv, int3
       (head_dim != 64 && head_dim != 128) || layer < 0 || layer >= kv->n_layers || q_pos0 + n_q > kv->positions)
     return fail(DS_ERR_INVALID, "bad attention arguments");
   const KvAddr a = layer_addr(*kv, layer, head_dim);
-  DS_TRY(attention_prefill_launch(static_cast<const bf16*>(q), ldq, a.k, a.v, a.head_stride, a.page_stride, a.table,
+  DS_TRY(attention_prefill_launch(static_cast<const bf16*>(q), ldq, a.k, a.v, a.head_stride, a.page_stride,
+                                  layer_rows(*kv, n_kv_heads, head_dim), a.table,
                                   n_q, q_pos0, n_heads, n_kv_heads, head_dim, static_cast<bf16*>(o), ldo,
                                   (cudaStream_t)stream),
          "attention");
@@ -556,6 +574,7 @@ int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t
       rc = window_layer(c, l, n, false);
     } else {
       rc = window_layer(c, l, P, true);
+      if (!rc) rc = reset_counters(c);
       if (!rc) rc = anchor_layer(c, l, P, w.h + (long long)P * d.d_model);
     }
     if (rc) return rc;

@@ -10,6 +10,8 @@
 // page (a contiguous 64 x D block), double-buffered with cp.async; bf16
 // m16n8k16 tensor-core MMAs with ldmatrix from XOR-swizzled shared memory.
 // Blocks are launched heaviest (latest positions) first.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(128) fa_prefill_kernel(FaArgs a) {
   }
 }
 
-int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
+int attention_prefill_legacy_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
                              long long head_stride, long long page_stride, const int32_t* table, int n_q, int q_pos0,
                              int n_heads, int n_kv_heads, int head_dim, bf16* o, long long ldo, cudaStream_t stream) {
   if (n_q <= 0) return DS_OK;
@@ -267,6 +269,347 @@ int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, 
     return DS_ERR_INVALID;
   }
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+// ======================================================================
+// tcgen05 / TMEM flash-attention prefill (sm_100a)
+//
+// CTA = one head x 256 query rows = two 128-row Q tiles (TMEM lanes = rows).
+// Warp roles (320 threads):
+//   warp 0     TMA producer: Q tiles once; K and V tiles of 128 keys (= two
+//              64-position pages, block-table addressed) through 2-stage rings
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer:
+//                S_i = Q_i K_j^T   (SS, M=128 N=128 K=D)    -> TMEM cols S_i
+//                O_i += P_i V_j    (TS: P from TMEM, V MN-major smem, N=D) -> cols O_i
+//              ping-ponging the two Q tiles so one tile's softmax overlaps the
+//              other tile's MMAs
+//   warps 2-5  softmax of Q tile 0 (thread = row), warps 6-9 of tile 1:
+//              tcgen05.ld S row, causal mask, online max with lazy O rescale
+//              (only when the max grows by > 2^8; exact after the final 1/l),
+//              p = exp2, P as bf16 written back into TMEM over S, l in fp32;
+//              epilogue O / l -> bf16 -> global
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D).
+// ======================================================================
+
+constexpr int FA_BM = 128;
+constexpr int FA_BN = 128;
+constexpr int FA_THREADS = 320;
+
+template <int D>
+struct FaTcSmem {
+  static constexpr int CH = D / 64;
+  static constexpr uint32_t CHUNK = FA_BM * 64 * 2;  // [128][64] bf16, SW128
+  static constexpr uint32_t Q = 0;
+  static constexpr uint32_t K = Q + 2 * CH * CHUNK;
+  static constexpr uint32_t V = K + 2 * CH * CHUNK;
+  static constexpr uint32_t BAR = V + 2 * CH * CHUNK;
+  static constexpr uint32_t TOTAL = BAR + 256 + 1024;
+};
+
+struct FaTcArgs {
+  int n_q, q_pos0, n_heads, n_kv_heads;
+  long long k_head_rows, k_page_rows;
+  const int32_t* table;
+  bf16* o;
+  long long ldo;
+  float scale_log2;
+};
+
+template <int D>
+__global__ void __launch_bounds__(FA_THREADS, 1)
+    fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
+  using L = FaTcSmem<D>;
+  constexpr int CH = L::CH;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 3;
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 7;
+  uint64_t* s_full = bars + 9;
+  uint64_t* p_full = bars + 11;
+  uint64_t* o_done = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  auto sQ = [&](int i, int c) { return smem + L::Q + (i * CH + c) * L::CHUNK; };
+  auto sK = [&](int st, int c) { return smem + L::K + (st * CH + c) * L::CHUNK; };
+  auto sV = [&](int st, int c) { return smem + L::V + (st * CH + c) * L::CHUNK; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x;
+  const int q0 = (gridDim.y - 1 - blockIdx.y) * 2 * FA_BM;  // heaviest (latest) blocks first
+  const int g = h / (a.n_heads / a.n_kv_heads);
+  int n_kv[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int rows = min(FA_BM, a.n_q - (q0 + i * FA_BM));
+    n_kv[i] = rows > 0 ? (a.q_pos0 + q0 + i * FA_BM + rows - 1) / FA_BN + 1 : 0;
+  }
+  const int J = max(n_kv[0], n_kv[1]);
+  const int max_key = a.q_pos0 + min(q0 + 2 * FA_BM, a.n_q) - 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int n_tiles = n_kv[1] > 0 ? 2 : 1;
+      mbar_expect_tx(q_full, n_tiles * CH * L::CHUNK);
+      for (int i = 0; i < n_tiles; ++i)
+        for (int c = 0; c < CH; ++c) tma_load_2d(sQ(i, c), &tmQ, q_full, h * D + c * 64, q0 + i * FA_BM);
+      for (int j = 0; j < J; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        int rows[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          int page = 2 * j + p;
+          if (page * 64 > max_key) page = 2 * j;  // beyond the window: duplicate a valid page (finite, masked)
+          const int tp = a.table ? __ldg(a.table + page) : page;
+          rows[p] = (int)(g * a.k_head_rows + (long long)tp * a.k_page_rows);
+        }
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sK(st, c) + p * 64 * 128, &tmK, &k_full[st], c * 64, rows[p]);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sV(st, c) + p * 64 * 128, &tmV, &v_full[st], c * 64, rows[p]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t IDESC_QK = umma_idesc_bf16(FA_BM, FA_BN);
+    constexpr uint32_t IDESC_PV = umma_idesc_bf16_bmn(FA_BM, D);
+    auto qk = [&](int i, int st) {
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = sdesc_sw128(smem_u32(sQ(i, c)) + k * 32, 16, 1024);
+            const uint64_t bd = sdesc_sw128(smem_u32(sK(st, c)) + k * 32, 16, 1024);
+            umma_bf16(tmem + i * 128, ad, bd, IDESC_QK, (c | k) != 0 ? 1u : 0u);
+          }
+        umma_commit(&s_full[i]);
+      }
+      __syncwarp();
+    };
+    auto pv = [&](int i, int st, int j) {
+      if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < FA_BN / 16; ++s) {
+          const uint64_t bd = sdesc_sw128(smem_u32(sV(st, 0)) + s * 2048, L::CHUNK, 1024);
+          umma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + s * 8, bd, IDESC_PV, (j | s) != 0 ? 1u : 0u);
+        }
+        umma_commit(&o_done[i]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait(&k_full[0], 0);
+    tc_fence_after();
+    if (n_kv[0] > 0) qk(0, 0);
+    if (n_kv[1] > 0) qk(1, 0);
+    if (lane == 0) umma_commit(&k_empty[0]);
+    __syncwarp();
+    for (int j = 0; j < J; ++j) {
+      const int st = j & 1, st1 = (j + 1) & 1;
+      const bool more = j + 1 < J;
+      mbar_wait(&v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (j * FA_BN + FA_BN - 1 > max_key) {
+        // keys past the window end: zero their V rows so p = 0 never meets a
+        // non-finite cache value (a SW128 row's 128 bytes stay within the row)
+        const int first = max_key + 1 - j * FA_BN;
+        for (int c = 0; c < CH; ++c) {
+          const uint32_t base = smem_u32(sV(st, c));
+          for (int off = first * 128 + lane * 16; off < FA_BN * 128; off += 32 * 16)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + off), "r"(0u) : "memory");
+        }
+        fence_async_shared();
+        __syncwarp();
+      }
+      if (j < n_kv[0]) {
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        pv(0, st, j);
+      }
+      if (more) {
+        mbar_wait(&k_full[st1], ((j + 1) >> 1) & 1);
+        tc_fence_after();
+        if (j + 1 < n_kv[0]) qk(0, st1);
+      }
+      if (j < n_kv[1]) {
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        pv(1, st, j);
+      }
+      if (lane == 0) umma_commit(&v_empty[st]);
+      __syncwarp();
+      if (more) {
+        if (j + 1 < n_kv[1]) qk(1, st1);
+        if (lane == 0) umma_commit(&k_empty[st1]);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int i = (warp - 2) >> 2;  // Q tile
+    const int quarter = warp & 3;   // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const int tile_pos0 = a.q_pos0 + q0 + i * FA_BM;
+    const int qpos = tile_pos0 + row;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + i * 128;
+    const uint32_t tO = tmem + lane_base + 256 + i * 128;
+    const float sc = a.scale_log2;
+    const float thr = 8.0f / sc;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv[i]; ++j) {
+      mbar_wait(&s_full[i], j & 1);
+      tc_fence_after();
+      uint32_t sr[FA_BN];
+#pragma unroll
+      for (int c = 0; c < FA_BN / 32; ++c) tmem_ld32_nowait(tS + c * 32, sr + c * 32);
+      tmem_wait_ld();
+      const int kbase = j * FA_BN;
+      if (kbase + FA_BN - 1 > tile_pos0) {
+#pragma unroll
+        for (int c = 0; c < FA_BN; ++c)
+          if (kbase + c > qpos) sr[c] = __float_as_uint(-INFINITY);
+      }
+      float mt = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < FA_BN; ++c) mt = fmaxf(mt, __uint_as_float(sr[c]));
+      const bool need = mt > m_used + thr;
+      float corr = 1.f;
+      if (need) {
+        corr = fast_exp2((m_used - mt) * sc);
+        m_used = mt;
+      }
+      l *= corr;
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        mbar_wait(&o_done[i], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orow[32];
+          tmem_ld32_nowait(tO + c * 32, orow);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * corr);
+          tmem_st32_nowait(tO + c * 32, orow);
+        }
+        tmem_wait_st();
+      }
+      const float msc = m_used * sc;
+      float sum = 0.f;
+      uint32_t pk[FA_BN / 2];
+#pragma unroll
+      for (int c = 0; c < FA_BN / 2; ++c) {
+        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * c]), sc, -msc));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc));
+        sum += p0 + p1;
+        pk[c] = pack_bf16x2(p0, p1);
+      }
+      l += sum;
+      tmem_st32_nowait(tS, pk);
+      tmem_st32_nowait(tS + 32, pk + 32);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[i]);
+    }
+    if (n_kv[i] > 0) {
+      mbar_wait(&o_done[i], (n_kv[i] - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const int qrow = q0 + i * FA_BM + row;
+      bf16* dst = a.o + (long long)qrow * a.ldo + (long long)h * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t orow[32];
+        tmem_ld32_nowait(tO + c * 32, orow);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack_bf16x2(__uint_as_float(orow[2 * e]) * inv, __uint_as_float(orow[2 * e + 1]) * inv);
+        if (qrow < a.n_q) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) st_global_v4(dst + c * 32 + e * 8, pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer, long long head_stride,
+                        long long page_stride, long long layer_rows, const int32_t* table, int n_q, int q_pos0,
+                        int n_heads, int n_kv_heads, bf16* o, long long ldo, cudaStream_t stream) {
+  using L = FaTcSmem<D>;
+  CUtensorMap tq, tk, tv;
+  if (make_tmap_bf16(&tq, q, n_q, (long long)n_heads * D, ldq, FA_BM, 64)) return DS_ERR_CUDA;
+  if (make_tmap_bf16(&tk, k_layer, layer_rows, D, D, 64, 64)) return DS_ERR_CUDA;
+  if (make_tmap_bf16(&tv, v_layer, layer_rows, D, D, 64, 64)) return DS_ERR_CUDA;
+  FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, head_stride / D, page_stride / D, table, o, ldo,
+             (float)(1.4426950408889634 / sqrt((double)D))};
+  static bool set = false;
+  if (!set) {
+    if (cudaFuncSetAttribute(fa_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
+      return DS_ERR_CUDA;
+    set = true;
+  }
+  dim3 grid(n_heads, (n_q + 2 * FA_BM - 1) / (2 * FA_BM));
+  count_launch();
+  fa_tc_kernel<D><<<grid, FA_THREADS, L::TOTAL, stream>>>(tq, tk, tv, a);
+  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+}
+
+int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
+                             long long head_stride, long long page_stride, long long layer_rows, const int32_t* table,
+                             int n_q, int q_pos0, int n_heads, int n_kv_heads, int head_dim, bf16* o, long long ldo,
+                             cudaStream_t stream) {
+  if (n_q <= 0) return DS_OK;
+  static const bool legacy = getenv("DS_FA_LEGACY") != nullptr;
+  if (legacy)
+    return attention_prefill_legacy_launch(q, ldq, k_layer, v_layer, head_stride, page_stride, table, n_q, q_pos0,
+                                           n_heads, n_kv_heads, head_dim, o, ldo, stream);
+  if (head_dim == 128)
+    return fa_tc_launch<128>(q, ldq, k_layer, v_layer, head_stride, page_stride, layer_rows, table, n_q, q_pos0,
+                             n_heads, n_kv_heads, o, ldo, stream);
+  if (head_dim == 64)
+    return fa_tc_launch<64>(q, ldq, k_layer, v_layer, head_stride, page_stride, layer_rows, table, n_q, q_pos0,
+                            n_heads, n_kv_heads, o, ldo, stream);
+  return DS_ERR_INVALID;
 }
 
 }  // namespace ds

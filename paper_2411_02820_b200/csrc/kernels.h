@@ -58,9 +58,13 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
 int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,
                    float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream);
 
+// Causal GQA prefill attention over one cache layer.  layer_rows = rows of the
+// layer region viewed as a [rows][head_dim] matrix (TMA bound).  Cache memory
+// beyond the written positions must hold finite values (allocations are zeroed).
 int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
-                             long long head_stride, long long page_stride, const int32_t* table, int n_q, int q_pos0,
-                             int n_heads, int n_kv_heads, int head_dim, bf16* o, long long ldo, cudaStream_t stream);
+                             long long head_stride, long long page_stride, long long layer_rows, const int32_t* table,
+                             int n_q, int q_pos0, int n_heads, int n_kv_heads, int head_dim, bf16* o, long long ldo,
+                             cudaStream_t stream);
 
 // Single-row GEMV (anchor pass); see anchor.cu.
 struct GemvArgs {
@@ -87,6 +91,7 @@ int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, cud
 int decode_splits(int n_keys);
 int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_layer, long long head_stride,
                             long long page_stride, const int32_t* table, int n_keys, int n_heads, int n_kv_heads,
-                            int head_dim, float* part_o, float* part_ml, bf16* out, cudaStream_t stream);
+                            int head_dim, float* part_o, float* part_ml, unsigned int* counters, bf16* out,
+                            cudaStream_t stream);
 
 }  // namespace ds

@@ -86,9 +86,11 @@ class LayerKV:
 
     @classmethod
     def empty(cls, config: ModelConfig, positions: int, device="cuda") -> "LayerKV":
+        # zero-filled: attention tiles may read (masked) positions beyond the
+        # written ones, and p = 0 must not meet a NaN bit pattern
         shape = (config.n_layers, config.n_kv_heads, positions, config.head_dim)
-        return cls(torch.empty(shape, dtype=torch.bfloat16, device=device),
-                   torch.empty(shape, dtype=torch.bfloat16, device=device))
+        return cls(torch.zeros(shape, dtype=torch.bfloat16, device=device),
+                   torch.zeros(shape, dtype=torch.bfloat16, device=device))
 
 
 @dataclass(eq=False)
@@ -122,8 +124,8 @@ class PagedKV:
         else:
             g = torch.Generator().manual_seed(shuffle_seed)
             table = torch.randperm(pages, generator=g)[:need].to(torch.int32).to(device)
-        return cls(torch.empty(shape, dtype=torch.bfloat16, device=device),
-                   torch.empty(shape, dtype=torch.bfloat16, device=device), table, positions)
+        return cls(torch.zeros(shape, dtype=torch.bfloat16, device=device),
+                   torch.zeros(shape, dtype=torch.bfloat16, device=device), table, positions)
 
     def dense(self) -> LayerKV:
         """Gather into the reference [L, KVH, n, D] layout (tests / export)."""

@@ -91,7 +91,8 @@ def _ref_attention(q, k, v, q_pos0, H, G, D):
     return (torch.softmax(s, -1) @ vv).transpose(0, 1).reshape(n, H * D)
 
 
-@pytest.mark.parametrize("n,H,G,D", [(511, 4, 1, 64), (1000, 8, 2, 128), (64, 4, 4, 128), (2049, 32, 8, 128)])
+@pytest.mark.parametrize("n,H,G,D", [(511, 4, 1, 64), (1000, 8, 2, 128), (64, 4, 4, 128), (2049, 32, 8, 128),
+                                     (1, 4, 1, 64), (257, 8, 8, 128), (8191, 32, 8, 128)])
 def test_attention_prefill_paged(ops, n, H, G, D):
     g = torch.Generator(device="cuda").manual_seed(n + H)
     pages = (n + 63) // 64
@@ -137,3 +138,18 @@ def test_kv_ingest_bit_exact(ops):
             assert (got_k[l, :, P:] == 0).all()  # the anchor position is never copied (model.py:602)
         else:
             assert (got_k[l] == 0).all()
+
+
+@pytest.mark.parametrize("n,q_pos0,D", [(300, 100, 128), (129, 1000, 64), (640, 64, 128)])
+def test_attention_prefill_query_offset(ops, n, q_pos0, D):
+    """Queries at positions q_pos0.. over a cache holding q_pos0 + n keys."""
+    H, G = 8, 2
+    g = torch.Generator(device="cuda").manual_seed(n + q_pos0)
+    total = q_pos0 + n
+    k = torch.randn(1, G, total, D, device="cuda", generator=g).bfloat16()
+    v = torch.randn(1, G, total, D, device="cuda", generator=g).bfloat16()
+    q = torch.randn(n, H * D, device="cuda", generator=g).bfloat16()
+    out = ops.attention_prefill(q, ops.dense_kv_desc(k, v), 0, H, G, D, q_pos0=q_pos0)
+    torch.cuda.synchronize()
+    ref = _ref_attention(q, k[0], v[0], q_pos0, H, G, D)
+    assert _rel(out, ref) < 1.5e-2
