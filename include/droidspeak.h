@@ -154,6 +154,18 @@ DS_API int ds_recompute_group(const ds_model* m, const int64_t* tokens_dev, int3
 DS_API int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, const ds_kv_cache* kv,
                      float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- producer -> consumer over NVLink (P2P pull through CUDA IPC) ----
+ * The producer exports a device buffer once; a consumer process maps it and
+ * hands the mapped pointer to ds_kv_ingest (ds_kv_cache.k/v or layer_k/v) and
+ * to ds_recompute_group (seed): the consumer's kernels then read the
+ * producer's HBM in place over NVLink.  handle = 64 opaque bytes. */
+#define DS_IPC_HANDLE_BYTES 64
+DS_API int ds_ipc_export(const void* device_ptr, void* handle_out, uint64_t* offset_out);
+/* Maps an exported buffer into this process: *base_out = mapping base (pass to
+ * ds_ipc_close), *ptr_out = base + offset. */
+DS_API int ds_ipc_open(const void* handle, uint64_t offset, void** base_out, void** ptr_out);
+DS_API int ds_ipc_close(void* base);
+
 /* ---- single-kernel entry points (used by the parity tests and the scheduler) ---- */
 
 /* C = epilogue(A[M][K] . B[N][K]^T); mode 0 bf16 store, 1 f32 out = resid + acc,

@@ -5,6 +5,7 @@
 // anchor gated on both — the pipelined plan of sched.py:212-263).
 #include <stdarg.h>
 #include <stdio.h>
+#include <string.h>
 
 #include <string>
 #include <vector>
@@ -360,6 +361,52 @@ int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const int32_t* 
   }
   DS_TRY(kv_ingest_launch(*src, *dst, reused, n_reused, n_kv_heads, head_dim, window, (cudaStream_t)stream),
          "kv ingest");
+  return DS_OK;
+}
+
+int ds_ipc_export(const void* device_ptr, void* handle_out, uint64_t* offset_out) {
+  g_err.clear();
+  if (!device_ptr || !handle_out || !offset_out) return fail(DS_ERR_INVALID, "bad ipc export arguments");
+  // driver entry point resolved at run time: the library must load without libcuda (CPU build box)
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(DS_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<RangeFn>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)device_ptr) != CUDA_SUCCESS)
+    return fail(DS_ERR_CUDA, "cuMemGetAddressRange failed for %p", device_ptr);
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) return cuda_fail("cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == DS_IPC_HANDLE_BYTES, "ipc handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (uint64_t)((CUdeviceptr)device_ptr - base);
+  return DS_OK;
+}
+
+int ds_ipc_open(const void* handle, uint64_t offset, void** base_out, void** ptr_out) {
+  g_err.clear();
+  if (!handle || !base_out || !ptr_out) return fail(DS_ERR_INVALID, "bad ipc open arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return cuda_fail("cudaIpcOpenMemHandle");
+  *base_out = base;
+  *ptr_out = static_cast<uint8_t*>(base) + offset;
+  return DS_OK;
+}
+
+int ds_ipc_close(void* base) {
+  g_err.clear();
+  if (!base) return DS_OK;
+  if (cudaIpcCloseMemHandle(base) != cudaSuccess) return cuda_fail("cudaIpcCloseMemHandle");
   return DS_OK;
 }
 
