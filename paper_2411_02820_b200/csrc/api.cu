@@ -144,6 +144,7 @@ struct Ctx {
   Workspace w;
   const ds_kv_cache* kv;
   cudaStream_t s;
+  cudaEvent_t* layer_ready = nullptr;  // recorded once layer l's window K/V are in the cache
 };
 
 // (a = RMSNorm(h) already in the workspace) QKV (+RoPE, K/V into the cache) -> [attention -> o-proj+resid -> RMSNorm -> W1+SiLU -> W2+resid]
@@ -169,6 +170,7 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only) {
   e.rope_sin = c.m->rope_sin;
   const bf16* wqkv = static_cast<const bf16*>(W.wqkv) + (kv_only ? (long long)hd * d.d_model : 0);
   DS_TRY(gemm_launch(c.w.a, d.d_model, wqkv, d.d_model, d.d_model, e, c.s), "qkv gemm");
+  if (c.layer_ready && cudaEventRecord(c.layer_ready[l], c.s) != cudaSuccess) return cuda_fail("event record");
   if (kv_only) return DS_OK;
   const KvAddr ka = layer_addr(*c.kv, l, d.head_dim);
   DS_TRY(attention_prefill_launch(c.w.q, hd, ka.k, ka.v, ka.head_stride, ka.page_stride,
@@ -303,13 +305,17 @@ int reset_counters(Ctx& c) {
   return DS_OK;
 }
 
-int anchor_pass(Ctx& c, const int64_t* tok, int P, float* logits, int32_t* token) {
+// wait_for (optional): per layer, an event the anchor's layer l must wait for
+// (the recompute of l on another stream); NULL entries need no wait.
+int anchor_pass(Ctx& c, const int64_t* tok, int P, float* logits, int32_t* token,
+                const cudaEvent_t* wait_for = nullptr) {
   const ds_dims& d = c.d;
   if (int rc = reset_counters(c)) return rc;
   DS_TRY(rmsnorm_launch(c.m->embed, true, tok + P, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr, 1,
                         c.s),
          "anchor seed");
   for (int l = 0; l < d.n_layers; ++l) {
+    if (wait_for && wait_for[l] && cudaStreamWaitEvent(c.s, wait_for[l], 0) != cudaSuccess) return cuda_fail("wait");
     int rc = anchor_layer(c, l, P, c.w.h_a);
     if (rc) return rc;
   }
@@ -516,30 +522,55 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
   if (!tok) return cuda_fail("token upload");
   Ctx c{m, d, w, out_kv, cs};
 
-  // ---- ingest (copy stream) overlapping recompute (compute stream)
-  // fork/join events, created once per host thread (capturable into CUDA graphs)
-  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (xs != cs) {
-    if (!ev_fork && (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-                     cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess))
-      return cuda_fail("event");
-    cudaEventRecord(ev_fork, cs);
-    cudaStreamWaitEvent(xs, ev_fork, 0);
+  if (xs == cs) {
+    // single stream: ingest, recompute, then the anchor after all KV has landed (sched.py:256)
+    if (!reused.empty())
+      DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P,
+                              cs),
+             "kv ingest");
+    for (int i = 0; i < n_groups; ++i) {
+      rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
+      if (rc) return rc;
+    }
+    return anchor_pass(c, tok, P, logits_out, token_out);
   }
+
+  // Two streams.  Copy stream: KV ingest, then the anchor pass layer by layer;
+  // compute stream: the recompute groups.  The anchor's layer l needs only
+  // layer l's window K/V (model.py:559) and its own layer l-1 output, so it
+  // waits for the recompute of l (an event after l's QKV GEMM) and nothing
+  // else: the HBM-bound anchor streams weights while the tensor-bound
+  // recompute runs.  Same kernels, same results as the single-stream order.
+  // Events are created once per host thread (capturable into CUDA graphs).
+  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  thread_local cudaEvent_t ev_layer[kMaxLayers] = {};
+  if (!ev_fork) {
+    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_fail("event");
+    for (int l = 0; l < kMaxLayers; ++l)
+      if (cudaEventCreateWithFlags(&ev_layer[l], cudaEventDisableTiming) != cudaSuccess) return cuda_fail("event");
+  }
+  cudaEvent_t wait_for[kMaxLayers] = {};
+  for (int l = 0; l < L; ++l) wait_for[l] = covered[l] ? ev_layer[l] : nullptr;
+  cudaEventRecord(ev_fork, cs);
+  cudaStreamWaitEvent(xs, ev_fork, 0);
   if (!reused.empty())
     DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P, xs),
            "kv ingest");
-  if (xs != cs) cudaEventRecord(ev_join, xs);
-
-  // ---- selective recompute of each group over the window
+  c.layer_ready = ev_layer;
+  Ctx cx{m, d, w, out_kv, xs};
+  // enqueue the recompute (which records ev_layer[l]) before the anchor's waits:
+  // a cudaStreamWaitEvent binds to the latest record at enqueue time
   for (int i = 0; i < n_groups; ++i) {
     rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
     if (rc) return rc;
   }
-
-  // ---- anchor pass after all KV has landed (sched.py:256)
-  if (xs != cs) cudaStreamWaitEvent(cs, ev_join, 0);
-  return anchor_pass(c, tok, P, logits_out, token_out);
+  rc = anchor_pass(cx, tok, P, logits_out, token_out, wait_for);
+  if (rc) return rc;
+  cudaEventRecord(ev_join, xs);
+  cudaStreamWaitEvent(cs, ev_join, 0);
+  return DS_OK;
 }
 
 int ds_recompute_group(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, int32_t a, int32_t b,
