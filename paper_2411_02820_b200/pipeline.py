@@ -83,16 +83,17 @@ class ConsumerPipeline:
         n = ids.shape[0]
         P = n - 1
         e_map = _normalize_e(sender_e)
-        # reference error order: KV misses ascending, then E per group (model.py:590-617)
         skv = sender_kv.desc() if sender_kv is not None else None
-        for l in config.reused_layers(cfg.n_layers):
-            if skv is None or l >= skv.n_layers or skv.positions < P or not _present(skv, l):
-                raise CacheMissError(l, "kv")
-        for a, _ in config.groups:
-            if a > 0:
-                e = e_map.get(a)
-                if e is None or e.positions < P or e.hidden.shape[1] != cfg.d_model:
-                    raise CacheMissError(a, "e")
+        if not getattr(self.transport, "provides_all", False):
+            # reference error order: KV misses ascending, then E per group (model.py:590-617)
+            for l in config.reused_layers(cfg.n_layers):
+                if skv is None or l >= skv.n_layers or skv.positions < P or not _present(skv, l):
+                    raise CacheMissError(l, "kv")
+            for a, _ in config.groups:
+                if a > 0:
+                    e = e_map.get(a)
+                    if e is None or e.positions < P or e.hidden.shape[1] != cfg.d_model:
+                        raise CacheMissError(a, "e")
         cache = out if out is not None else PagedKV.allocate(cfg, n, self.device)
         dst = cache.desc()
         logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=self.device)
@@ -118,7 +119,7 @@ class ConsumerPipeline:
             while i < len(jobs):
                 job = jobs[i]
                 if job.kind == "e":
-                    e_ptr[job.layer] = self.transport.e_job(job.layer, e_map[job.layer], self.link)
+                    e_ptr[job.layer] = self.transport.e_job(job.layer, e_map.get(job.layer), self.link)
                     ev = self._event(timing)
                     ev.record(self.link)
                     e_ready[job.layer] = ev
