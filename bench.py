@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=150.0, help="seconds for the CPU reference leg")
     ap.add_argument("--graph", type=int, default=1, help="replay the consumer step as a CUDA graph")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: consumers pull the producer's export over NVLink (CUDA IPC), or NCCL send/recv")
+    ap.add_argument("--same-device", action="store_true",
+                    help="debug: run every rank on cuda:0 with gloo (exercises the N>1 code path on one GPU)")
     return ap.parse_args()
 
 
@@ -117,15 +121,20 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def dist_setup(n_gpus):
+def dist_setup(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:
+        local = 0
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -142,7 +151,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -434,12 +444,177 @@ def run_ours(args, world, rank, local):
         print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# N > 1: one producer fanning out to N-1 consumer fine-tunes (BASELINE configs 3/4)
+# ---------------------------------------------------------------------------
+
+
+def run_fanout(args, world, rank, local):
+    """Rank 0 = producer (GPU 0): prefills the shared context once and keeps the
+    export (KV of every layer + E at the transition layer) resident.  Ranks
+    1..N-1 = consumers, each a different fine-tune (its own perturbation seed),
+    each running the partial prefill while pulling the producer's KV/E over
+    NVLink (p2p: CUDA IPC mapping, the ingest and recompute kernels read peer
+    HBM in place) or receiving it by NCCL send/recv in planner link order.
+    A step = one partial prefill on every consumer; per-step time = max over
+    ranks of the consumer's CUDA-event TTFT; value = consumers x n / TTFT."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_02820_b200 as P
+    from paper_2411_02820_b200 import _lib
+    from paper_2411_02820_b200.pipeline import ConsumerPipeline
+    from paper_2411_02820_b200.transport import NcclSender, NcclTransport, RemoteExport, export_prefill
+
+    lib = _lib.lib()
+    n, k = args.n, args.k
+    cfg = P.ModelConfig(max_seq=max(n, 8192), base_seed=0, **SHAPE)
+    L = cfg.n_layers
+    dev = torch.device("cuda", local)
+    rc = P.RecomputeConfig([(L - k, L - 1)])
+    ids = np.random.default_rng(7).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
+    tok_dev = torch.from_numpy(ids).to(dev)
+    producer = rank == 0
+    A = P.random_model(cfg, seed=1000, device=dev)
+    if producer:
+        prod = P.full_prefill(A, ids, e_layers=rc.transition_layers, tokens_dev=tok_dev)
+        torch.cuda.synchronize()
+        obj = [export_prefill(prod, A.ident, ids) if args.transport == "p2p" else None]
+    else:
+        B = P.random_model(cfg, seed=2000 + rank, device=dev, base=A, perturb_layers=range(L - k, L), eps=0.5)
+        del A
+        obj = [None]
+    dist.broadcast_object_list(obj, src=0)
+    stream = torch.cuda.Stream(device=dev)
+    side = torch.cuda.Stream(device=dev)
+    consumers = list(range(1, world))
+    remote = None
+    if not producer:
+        cache = P.PagedKV.allocate(cfg, n, dev)
+        if args.transport == "p2p":
+            remote = RemoteExport(obj[0])
+            step = lambda: P.partial_prefill(B, ids, rc, remote.kv, remote.e_map, out=cache, stream=stream,  # noqa
+                                             copy_stream=side, tokens_dev=tok_dev)
+        else:
+            pipe = ConsumerPipeline(B, transport=NcclTransport(0, cfg, n, dev))
+            step = lambda: pipe.run(ids, rc, None, None, out=cache, tokens_dev=tok_dev)  # noqa
+    else:
+        sender = NcclSender()
+        step = lambda: sender.serve(prod, [(r, rc, n) for r in consumers], L)  # noqa
+
+    run = step
+    use_graph = args.graph and args.transport == "p2p" and not producer
+    if not producer or args.transport == "nccl":
+        with torch.cuda.stream(stream):
+            step()
+        torch.cuda.synchronize()
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        run = graph.replay
+    for _ in range(args.warmup):
+        if not producer or args.transport == "nccl":
+            with torch.cuda.stream(stream):
+                run()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = lib.ds_launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            starts[i].record(stream)
+            if not producer or args.transport == "nccl":
+                with torch.cuda.stream(stream):
+                    run()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    per = [s.elapsed_time(e) for s, e in zip(starts, ends)] if not producer else [0.0]
+    ttft_ms = max_over_ranks(statistics.median(per), world)
+    total_ms = max_over_ranks(sum(per), world)
+    launches = lib.ds_launch_count() - launches0
+    if use_graph:
+        c0 = lib.ds_launch_count()
+        with torch.cuda.stream(stream):
+            step()
+        torch.cuda.synchronize()
+        launches = (lib.ds_launch_count() - c0) * args.steps
+    launches = int(max_over_ranks(float(launches), world))
+    # end to end through the public API: pinned host ids -> H2D, partial prefill, D2H logits + token
+    e2e = [0.0]
+    if args.transport == "p2p":
+        e2e = []
+        pinned = torch.from_numpy(ids).pin_memory()
+        logits_host = torch.empty(cfg.vocab_size, dtype=torch.float32).pin_memory()
+        tok_host = torch.empty(1, dtype=torch.int32).pin_memory()
+        for i in range(args.warmup + args.steps):
+            barrier(world)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            if not producer:
+                with torch.cuda.stream(stream):
+                    r = P.partial_prefill(B, pinned.numpy(), rc, remote.kv, remote.e_map, out=cache, stream=stream,
+                                          copy_stream=side)
+                    logits_host.copy_(r.logits, non_blocking=True)
+                    tok_host.copy_(r.token_dev, non_blocking=True)
+                stream.synchronize()
+            if i >= args.warmup:
+                e2e.append(time.perf_counter() - w0)
+    e2e_s = max_over_ranks(statistics.median(e2e), world)
+    # NVLink pull rate of the ingest alone (consumer 1): reused KV bytes crossing the link
+    link = None
+    if args.transport == "p2p" and rank == 1:
+        reused = list(range(L - k))
+        xfer = len(reused) * 2 * cfg.n_kv_heads * cfg.head_dim * (n - 1) * 2
+        from paper_2411_02820_b200 import ops
+        d = cache.desc()
+        s = remote.kv.desc()
+        ms = time_kernel(lambda: ops.kv_ingest(s, d, reused, n - 1, cfg.n_kv_heads, cfg.head_dim, stream=stream),
+                         5, stream)
+        link = {"kernel": "kv_ingest (P2P pull over NVLink)", "ms": ms, "bytes": xfer, "gbs": xfer / ms / 1e6}
+    links = [None]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, link)
+        links = [x for x in gathered if x]
+    barrier(world)
+    if remote is not None:
+        remote.close()
+    if rank == 0:
+        nc = len(consumers)
+        line = {
+            "metric": METRIC, "value": nc * n / (ttft_ms / 1e3), "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "ttft_p50_ms": ttft_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (random-init weights generated on GPU, uniform random token ids)",
+            "config": {"workload": f"fan-out: 1 producer (GPU 0) -> {nc} consumer fine-tunes, Llama-3-8B-shaped, "
+                                   f"n={n}, recompute [{L - k},{L - 1}] (BASELINE configs 3/4)",
+                       "n_tokens": n, "recomputed_layers": k, "consumers": nc, "transport": args.transport,
+                       "parallelism": f"1 producer + {nc} consumers", "cuda_graph": bool(use_graph)},
+            "gpu_launches": launches,
+            "e2e": {"value": nc * n / e2e_s if e2e_s > 0 else None, "unit": "tok/s", "ttft_p50_ms": e2e_s * 1e3,
+                    "h2d_bytes_per_step": 8 * n * nc, "d2h_bytes_per_step": (4 * cfg.vocab_size + 4) * nc},
+            "roofline": ({"bound": "nvlink", "kernel": links[0]["kernel"], "achieved": links[0]["gbs"],
+                          "peak": 770.0, "unit": "GB/s", "frac": links[0]["gbs"] / 770.0, "traffic": None,
+                          "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900"}
+                         if links else None),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":
             run_reference(args, world, rank)
+        elif world > 1:
+            run_fanout(args, world, rank, local)
         else:
             run_ours(args, world, rank, local)
     finally:

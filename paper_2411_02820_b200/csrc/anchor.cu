@@ -8,11 +8,8 @@
 //                  RoPE + q / KV-cache write, residual add, SiLU, logits +
 //                  packed argmax (lowest id on ties).  An f32 input is
 //                  RMSNorm'ed in the prologue (model.py:466-468).
-//   decode_attn    split-KV attention of the anchor's query heads: one CTA per
-//                  (kv head, 512-key split) streams 128-key tiles (two K pages and
-//                  two V pages, contiguous 64 x D blocks) through a 2-stage
-//                  bulk-copy ring, online softmax over the R = H/KVH heads, and
-//                  the last CTA of each kv head merges all splits (no second launch).
+//   decode_attn    split-KV attention of the anchor's query heads on the tensor
+//                  pipe (the GQA group is the M of an m16n8k16 tile), see below.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -68,6 +65,14 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
   __shared__ float red[GEMV_WARPS][GEMV_ROWS];
   __shared__ float ssq[GEMV_WARPS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tiles = a.N / GEMV_ROWS;
+
+  // ---- weights do not depend on the predecessor kernel: start streaming this
+  // CTA's first tile into L2, let the successor launch, then wait (PDL)
+  if (blockIdx.x < tiles && tid < GEMV_ROWS)
+    prefetch_l2(a.W + (long long)gemv_row(a, blockIdx.x, tid) * a.ldw, (uint32_t)a.K * 2);
+  pdl_trigger();
+  pdl_wait();
 
   // ---- stage the input vector (bf16) in shared memory, RMSNorm fused
   if (a.x_f32) {
@@ -102,7 +107,6 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
   __syncthreads();
 
   const int nchunk = a.K >> 3;
-  const int tiles = a.mode == EPI_QKV_ROPE ? a.N / a.head_dim * (a.head_dim / 8) : a.N / GEMV_ROWS;
   unsigned long long best = 0ull;
   for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
     const bf16* wr[GEMV_ROWS];
@@ -210,8 +214,8 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
   const int cap = num_sms() * per_sm;
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
-  gemv_kernel<<<grid, GEMV_THREADS, smem, stream>>>(a);
-  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_pdl(gemv_kernel, dim3(grid), dim3(GEMV_THREADS), smem, stream, a) == cudaSuccess ? DS_OK
+                                                                                            : DS_ERR_CUDA;
 }
 
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, cudaStream_t stream) {
@@ -221,12 +225,20 @@ int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, cud
 }
 
 // ---------------------------------------------------------------- decode attention
+//
+// One CTA per (kv head g, split of DEC_SPLIT keys), 4 warps.  The R = H/KVH
+// query heads of the group are the M rows of an m16n8k16 tensor-core tile
+// (rows >= R are zero), so the scores and P.V run on the tensor pipe instead
+// of per-key scalar loops.  Keys stream in 64-key pages (one contiguous 64 x D
+// block per page) through a 2-stage cp.async ring with an XOR swizzle
+// (conflict-free ldmatrix); warp w owns keys [16w, 16w+16) of every page and
+// keeps its own online-softmax state and O accumulator; the 4 warps merge in
+// shared memory, and the last CTA of the kv head merges all splits.
 
 constexpr int DEC_THREADS = 128;
-constexpr int DEC_TILE = 128;                 // keys per shared-memory stage (two 64-position pages)
-constexpr int DEC_TILES_PER_SPLIT = 4;        // 512 keys per CTA
-constexpr int DEC_SPLIT = DEC_TILE * DEC_TILES_PER_SPLIT;
-constexpr int DEC_MAX_R = 8;
+constexpr int DEC_PAGE = 64;
+constexpr int DEC_SPLIT = 256;  // keys per CTA (4 pages)
+constexpr int DEC_MAX_R = 16;
 
 struct DecArgs {
   const bf16* q;  // [H*D]
@@ -245,12 +257,11 @@ struct DecArgs {
 template <int D>
 __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int STAGE = 2 * DEC_TILE * D;                      // bf16 elements per stage (K then V)
-  bf16* ring = reinterpret_cast<bf16*>(smem);                  // [2][K 128xD | V 128xD]
-  float* qs = reinterpret_cast<float*>(ring + 2 * STAGE);      // [R][D]
-  float* sc = qs + DEC_MAX_R * D;                              // [R][128]
-  float* mstat = sc + DEC_MAX_R * DEC_TILE;                    // [R] running max, [R] tile max, [R] sum
-  __shared__ __align__(8) uint64_t bar[2];
+  constexpr int TILE = DEC_PAGE * D * 2;           // bytes of one page (K or V)
+  constexpr int CH = D / 8;                        // 16-byte chunks per row
+  const uint32_t sQ = smem_u32(smem);              // [16][D] bf16 swizzled
+  const uint32_t sKV = sQ + 16 * D * 2;            // [2 stages][K page | V page]
+  float* red = reinterpret_cast<float*>(smem + 16 * D * 2 + 4 * TILE);  // [4 warps][16 rows][D + 2]
   __shared__ unsigned int is_last;
 
   const int g = blockIdx.x, split = blockIdx.y, tid = threadIdx.x;
@@ -258,142 +269,175 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
   const int R = a.n_heads / a.n_kv_heads;
   const int key0 = split * DEC_SPLIT;
   const int nk_split = min(DEC_SPLIT, a.n_keys - key0);
-  const int n_tiles = (nk_split + DEC_TILE - 1) / DEC_TILE;
+  const int n_pages = (nk_split + DEC_PAGE - 1) / DEC_PAGE;
 
-  auto issue = [&](int t) {  // thread 0: bulk-copy tile t's K/V pages into stage t & 1
-    const int st = t & 1;
-    const int k0 = key0 + t * DEC_TILE;
-    const int nk = min(DEC_TILE, a.n_keys - k0);
-    mbar_expect_tx(&bar[st], (uint32_t)nk * D * 2 * 2);
-    for (int p = 0; p * 64 < nk; ++p) {
-      const int pos = k0 + p * 64;
-      const int page = a.table ? __ldg(a.table + (pos >> 6)) : (pos >> 6);
-      const long long off = (long long)g * a.head_stride + (long long)page * a.page_stride;
-      const uint32_t bytes = (uint32_t)min(64, nk - p * 64) * D * 2;
-      bf16* dst = ring + st * STAGE;
-      bulk_g2s(dst + p * 64 * D, a.k + off, bytes, &bar[st]);
-      bulk_g2s(dst + DEC_TILE * D + p * 64 * D, a.v + off, bytes, &bar[st]);
+  // the split's cache pages (except the anchor's own row, written by the
+  // predecessor) are already in HBM: stream them toward L2, then wait (PDL)
+  if (tid < n_pages) {
+    const int pos = key0 + tid * DEC_PAGE;
+    const int page = a.table ? __ldg(a.table + (pos >> 6)) : (pos >> 6);
+    const long long off = (long long)g * a.head_stride + (long long)page * a.page_stride;
+    const uint32_t bytes = (uint32_t)min(DEC_PAGE, a.n_keys - pos) * D * 2;
+    prefetch_l2(a.k + off, bytes);
+    prefetch_l2(a.v + off, bytes);
+  }
+  pdl_trigger();
+  pdl_wait();
+  // Q rows 0..R-1 = the group's heads, rows R..15 zero
+  for (int i = tid; i < 16 * CH; i += DEC_THREADS) {
+    const int r = i / CH, c = i % CH;
+    const bool ok = r < R;
+    cp_async16(sQ + swz<D>(r, c), a.q + (ok ? ((long long)(g * R + r) * D + c * 8) : 0), ok);
+  }
+  auto load_page = [&](int t) {
+    const int pos = key0 + t * DEC_PAGE;
+    const int rows = min(DEC_PAGE, a.n_keys - pos);
+    const int page = a.table ? __ldg(a.table + (pos >> 6)) : (pos >> 6);
+    const long long off = (long long)g * a.head_stride + (long long)page * a.page_stride;
+    const uint32_t base = sKV + (t & 1) * 2 * TILE;
+    for (int i = tid; i < DEC_PAGE * CH; i += DEC_THREADS) {
+      const int r = i / CH, c = i % CH;
+      const bool ok = r < rows;  // rows past the last key are zero-filled
+      const long long src = ok ? (long long)r * D + c * 8 : 0;
+      cp_async16(base + swz<D>(r, c), a.k + off + src, ok);
+      cp_async16(base + TILE + swz<D>(r, c), a.v + off + src, ok);
     }
   };
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-    issue(0);
-    if (n_tiles > 1) issue(1);
+  load_page(0);
+  cp_async_commit();
+
+  uint32_t qf[D / 16][4];
+  float acc_o[D / 8][4];
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) acc_o[i][0] = acc_o[i][1] = acc_o[i][2] = acc_o[i][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+  const int t4 = lane & 3;
+
+  for (int t = 0; t < n_pages; ++t) {
+    if (t + 1 < n_pages) load_page(t + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        ldsm_x4(sQ + swz<D>(lane & 15, ks * 2 + (lane >> 4)), qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
+    }
+    const uint32_t sK = sKV + (t & 1) * 2 * TILE, sV = sK + TILE;
+    // S = Q K^T over this warp's 16 keys (two n-tiles of 8)
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      uint32_t b0, b1, b2, b3;
+      const int r = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
+      ldsm_x4(sK + swz<D>(r, ks * 2 + ((lane >> 3) & 1)), b0, b1, b2, b3);
+      mma_bf16_16816(s[0], qf[ks], b0, b1);
+      mma_bf16_16816(s[1], qf[ks], b2, b3);
+    }
+    // keys past the end of the window -> -inf
+    const int kbase = key0 + t * DEC_PAGE + warp * 16;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int kp = kbase + nt * 8 + 2 * t4;
+      if (kp >= a.n_keys) s[nt][0] = s[nt][2] = -INFINITY;
+      if (kp + 1 >= a.n_keys) s[nt][1] = s[nt][3] = -INFINITY;
+    }
+    // online softmax (row g in [0], [1]; row g + 8 in [2], [3])
+    float mx[2] = {m_r[0], m_r[1]};
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      mx[0] = fmaxf(mx[0], fmaxf(s[nt][0], s[nt][1]));
+      mx[1] = fmaxf(mx[1], fmaxf(s[nt][2], s[nt][3]));
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+    }
+    float corr[2], msc[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      // a warp whose keys are all past the end keeps -inf: guard exp2(-inf - -inf)
+      corr[r] = mx[r] == -INFINITY ? 1.f : exp2f((m_r[r] - mx[r]) * a.scale_log2);
+      m_r[r] = mx[r];
+      msc[r] = mx[r] == -INFINITY ? 0.f : mx[r] * a.scale_log2;
+    }
+    uint32_t pa[4];
+    float rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const float p0 = exp2f(s[nt][0] * a.scale_log2 - msc[0]);
+      const float p1 = exp2f(s[nt][1] * a.scale_log2 - msc[0]);
+      const float p2 = exp2f(s[nt][2] * a.scale_log2 - msc[1]);
+      const float p3 = exp2f(s[nt][3] * a.scale_log2 - msc[1]);
+      rs[0] += p0 + p1;
+      rs[1] += p2 + p3;
+      pa[nt * 2 + 0] = pack_bf16x2(p0, p1);
+      pa[nt * 2 + 1] = pack_bf16x2(p2, p3);
+    }
+    l_r[0] = l_r[0] * corr[0] + rs[0];
+    l_r[1] = l_r[1] * corr[1] + rs[1];
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      acc_o[i][0] *= corr[0];
+      acc_o[i][1] *= corr[0];
+      acc_o[i][2] *= corr[1];
+      acc_o[i][3] *= corr[1];
+    }
+    // O += P V over the warp's 16 keys (one k-step)
+#pragma unroll
+    for (int i = 0; i < D / 16; ++i) {
+      uint32_t b0, b1, b2, b3;
+      const int r = warp * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+      ldsm_x4_t(sV + swz<D>(r, i * 2 + (lane >> 4)), b0, b1, b2, b3);
+      mma_bf16_16816(acc_o[2 * i], pa, b0, b1);
+      mma_bf16_16816(acc_o[2 * i + 1], pa, b2, b3);
+    }
+    __syncthreads();
   }
-  for (int i = tid; i < R * D; i += DEC_THREADS) qs[i] = __bfloat162float(a.q[(long long)g * R * D + i]);
-  if (tid < DEC_MAX_R) {
-    mstat[tid] = -INFINITY;
-    mstat[2 * DEC_MAX_R + tid] = 0.f;
+  cp_async_wait<0>();
+
+  // ---- merge the 4 warps: per row m, l and the unnormalised O
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
+  }
+  constexpr int RS = D + 2;  // [m, l, O...] per (warp, row)
+  const int gr = lane >> 2;
+  float* mine = red + (warp * 16) * RS;
+#pragma unroll
+  for (int i = 0; i < D / 8; ++i) {
+    const int col = i * 8 + 2 * t4;
+    mine[gr * RS + 2 + col] = acc_o[i][0];
+    mine[gr * RS + 2 + col + 1] = acc_o[i][1];
+    mine[(gr + 8) * RS + 2 + col] = acc_o[i][2];
+    mine[(gr + 8) * RS + 2 + col + 1] = acc_o[i][3];
+  }
+  if (t4 == 0) {
+    mine[gr * RS] = m_r[0];
+    mine[gr * RS + 1] = l_r[0];
+    mine[(gr + 8) * RS] = m_r[1];
+    mine[(gr + 8) * RS + 1] = l_r[1];
   }
   __syncthreads();
-
-  constexpr int KG = DEC_THREADS / D;  // key groups in the P.V loop (2 for D = 64)
-  const int d = tid % D, kg = tid / D;
-  float o[DEC_MAX_R];
+  for (int idx = tid; idx < R * D; idx += DEC_THREADS) {
+    const int r = idx / D, d = idx % D, h = g * R + r;
+    float M = -INFINITY;
 #pragma unroll
-  for (int r = 0; r < DEC_MAX_R; ++r) o[r] = 0.f;
-
-  for (int t = 0; t < n_tiles; ++t) {
-    const int st = t & 1;
-    const int nk = min(DEC_TILE, nk_split - t * DEC_TILE);
-    mbar_wait(&bar[st], (uint32_t)(t >> 1) & 1u);
-    const bf16* sk = ring + st * STAGE;
-    const bf16* sv = sk + DEC_TILE * D;
-    // scores: thread = key; 16-byte chunks read staggered by key (bank-conflict free)
-    if (tid < nk) {
-      float acc[DEC_MAX_R];
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * 16 + r) * RS]);
+    float o = 0.f, lsum = 0.f;
 #pragma unroll
-      for (int r = 0; r < DEC_MAX_R; ++r) acc[r] = 0.f;
-      const bf16* kr = sk + tid * D;
-#pragma unroll 4
-      for (int cc = 0; cc < D / 8; ++cc) {
-        const int c = (cc + tid) & (D / 8 - 1);
-        const uint4 u = *reinterpret_cast<const uint4*>(kr + c * 8);
-        const float2 e0 = unpack_bf16x2(u.x), e1 = unpack_bf16x2(u.y), e2 = unpack_bf16x2(u.z),
-                     e3 = unpack_bf16x2(u.w);
-        const float kv8[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
-#pragma unroll
-        for (int r = 0; r < DEC_MAX_R; ++r) {
-          if (r < R) {
-            const float4 q0 = *reinterpret_cast<const float4*>(qs + r * D + c * 8);
-            const float4 q1 = *reinterpret_cast<const float4*>(qs + r * D + c * 8 + 4);
-            acc[r] = fmaf(q0.x, kv8[0], acc[r]);
-            acc[r] = fmaf(q0.y, kv8[1], acc[r]);
-            acc[r] = fmaf(q0.z, kv8[2], acc[r]);
-            acc[r] = fmaf(q0.w, kv8[3], acc[r]);
-            acc[r] = fmaf(q1.x, kv8[4], acc[r]);
-            acc[r] = fmaf(q1.y, kv8[5], acc[r]);
-            acc[r] = fmaf(q1.z, kv8[6], acc[r]);
-            acc[r] = fmaf(q1.w, kv8[7], acc[r]);
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < DEC_MAX_R; ++r)
-        if (r < R) sc[r * DEC_TILE + tid] = acc[r] * a.scale_log2;
+    for (int w = 0; w < 4; ++w) {
+      const float mw = red[(w * 16 + r) * RS];
+      const float wt = mw == -INFINITY ? 0.f : exp2f((mw - M) * a.scale_log2);
+      o += wt * red[(w * 16 + r) * RS + 2 + d];
+      lsum += wt * red[(w * 16 + r) * RS + 1];
     }
-    __syncthreads();
-    // online softmax per head (warp w -> heads w, w+4): new running max, p, tile sum
-    for (int r = warp; r < R; r += DEC_THREADS / 32) {
-      float m = -INFINITY;
-      for (int i = lane; i < nk; i += 32) m = fmaxf(m, sc[r * DEC_TILE + i]);
-#pragma unroll
-      for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-      const float m_old = mstat[r];
-      const float m_new = fmaxf(m_old, m);
-      float l = 0.f;
-      for (int i = lane; i < nk; i += 32) {
-        const float p = exp2f(sc[r * DEC_TILE + i] - m_new);
-        sc[r * DEC_TILE + i] = p;
-        l += p;
-      }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-      __syncwarp();
-      if (lane == 0) {
-        const float corr = exp2f(m_old - m_new);  // 0 on the first tile
-        mstat[DEC_MAX_R + r] = corr;
-        mstat[2 * DEC_MAX_R + r] = mstat[2 * DEC_MAX_R + r] * corr + l;
-        mstat[r] = m_new;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < DEC_MAX_R; ++r)
-      if (r < R) o[r] *= mstat[DEC_MAX_R + r];
-    for (int kk = kg; kk < nk; kk += KG) {
-      const float vv = __bfloat162float(sv[kk * D + d]);
-#pragma unroll
-      for (int r = 0; r < DEC_MAX_R; ++r)
-        if (r < R) o[r] = fmaf(sc[r * DEC_TILE + kk], vv, o[r]);
-    }
-    __syncthreads();  // stage st and sc are free
-    if (tid == 0 && t + 2 < n_tiles) issue(t + 2);
-  }
-  if (KG > 1) {
-    float* ored = sc;  // [R][D]
-    if (kg == 1) {
-#pragma unroll
-      for (int r = 0; r < DEC_MAX_R; ++r)
-        if (r < R) ored[r * D + d] = o[r];
-    }
-    __syncthreads();
-    if (kg == 0) {
-#pragma unroll
-      for (int r = 0; r < DEC_MAX_R; ++r)
-        if (r < R) o[r] += ored[r * D + d];
-    }
-  }
-  if (kg == 0) {
-    for (int r = 0; r < R; ++r) {
-      const int h = g * R + r;
-      a.part_o[((long long)h * a.splits + split) * D + d] = o[r];
-      if (d == 0) {
-        a.part_ml[((long long)h * a.splits + split) * 2] = mstat[r];
-        a.part_ml[((long long)h * a.splits + split) * 2 + 1] = mstat[2 * DEC_MAX_R + r];
-      }
+    a.part_o[((long long)h * a.splits + split) * D + d] = o;
+    if (d == 0) {
+      a.part_ml[((long long)h * a.splits + split) * 2] = M * a.scale_log2;  // log2 domain
+      a.part_ml[((long long)h * a.splits + split) * 2 + 1] = lsum;
     }
   }
   // ---- the last CTA of this kv head merges every split (threadfence reduction)
@@ -403,20 +447,19 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // split weights per head in shared memory: w[r][s] = exp2(m_s - M_r), den_r = sum w l
-  float* wts = reinterpret_cast<float*>(smem);  // the ring is dead: [R][splits]
+  float* wts = red;  // [R][splits]
   float* den = wts + DEC_MAX_R * a.splits;
   for (int r = warp; r < R; r += DEC_THREADS / 32) {
     const float* ml = a.part_ml + (long long)(g * R + r) * a.splits * 2;
     float M = -INFINITY;
-    for (int s = lane; s < a.splits; s += 32) M = fmaxf(M, __ldcg(ml + 2 * s));
+    for (int s2 = lane; s2 < a.splits; s2 += 32) M = fmaxf(M, __ldcg(ml + 2 * s2));
 #pragma unroll
     for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
     float dn = 0.f;
-    for (int s = lane; s < a.splits; s += 32) {
-      const float w = exp2f(__ldcg(ml + 2 * s) - M);
-      wts[r * a.splits + s] = w;
-      dn += w * __ldcg(ml + 2 * s + 1);
+    for (int s2 = lane; s2 < a.splits; s2 += 32) {
+      const float w = exp2f(__ldcg(ml + 2 * s2) - M);
+      wts[r * a.splits + s2] = w;
+      dn += w * __ldcg(ml + 2 * s2 + 1);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
@@ -428,13 +471,18 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
     const float* po = a.part_o + (long long)h * a.splits * D + dd;
     float num = 0.f;
 #pragma unroll 8
-    for (int s = 0; s < a.splits; ++s) num = fmaf(wts[r * a.splits + s], __ldcg(po + (long long)s * D), num);
+    for (int s2 = 0; s2 < a.splits; ++s2) num = fmaf(wts[r * a.splits + s2], __ldcg(po + (long long)s2 * D), num);
     a.out[(long long)h * D + dd] = __float2bfloat16_rn(num / den[r]);
   }
   if (tid == 0) a.counters[g] = 0u;
 }
 
 int decode_splits(int n_keys) { return (n_keys + DEC_SPLIT - 1) / DEC_SPLIT; }
+
+template <int D>
+static int dec_smem() {
+  return 16 * D * 2 + 4 * DEC_PAGE * D * 2 + 4 * 16 * (D + 2) * 4;
+}
 
 int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_layer, long long head_stride,
                             long long page_stride, const int32_t* table, int n_keys, int n_heads, int n_kv_heads,
@@ -443,11 +491,10 @@ int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_la
   const int R = n_heads / n_kv_heads;
   if (R > DEC_MAX_R || (head_dim != 64 && head_dim != 128)) return DS_ERR_INVALID;
   const int splits = decode_splits(n_keys);
-  if (splits * (DEC_MAX_R + 1) * 4 > 2 * 2 * DEC_TILE * head_dim * 2) return DS_ERR_INVALID;  // merge scratch
+  const int smem = head_dim == 128 ? dec_smem<128>() : dec_smem<64>();
+  if ((DEC_MAX_R + 1) * splits * 4 > 4 * 16 * (head_dim + 2) * 4) return DS_ERR_INVALID;  // merge scratch
   DecArgs a{q, k_layer, v_layer, head_stride, page_stride, table, n_keys, n_heads, n_kv_heads, head_dim, splits,
             part_o, part_ml, counters, out, (float)(1.4426950408889634 / sqrt((double)head_dim))};
-  const int smem = 2 * 2 * DEC_TILE * head_dim * 2 + DEC_MAX_R * head_dim * 4 + DEC_MAX_R * DEC_TILE * 4 +
-                   3 * DEC_MAX_R * 4;
   count_launch();
   if (head_dim == 128) {
     static bool set = false;
@@ -457,7 +504,9 @@ int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_la
         return DS_ERR_CUDA;
       set = true;
     }
-    decode_attn_kernel<128><<<dim3(n_kv_heads, splits), DEC_THREADS, smem, stream>>>(a);
+    if (launch_pdl(decode_attn_kernel<128>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a) !=
+        cudaSuccess)
+      return DS_ERR_CUDA;
   } else {
     static bool set = false;
     if (!set) {
@@ -466,7 +515,9 @@ int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_la
         return DS_ERR_CUDA;
       set = true;
     }
-    decode_attn_kernel<64><<<dim3(n_kv_heads, splits), DEC_THREADS, smem, stream>>>(a);
+    if (launch_pdl(decode_attn_kernel<64>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a) !=
+        cudaSuccess)
+      return DS_ERR_CUDA;
   }
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }

@@ -42,6 +42,25 @@ inline bool kv_layer_present(const ds_kv_cache& c, int layer) {
   return layer >= 0 && layer < c.n_layers && kv_layer_base(c, layer, false) && kv_layer_base(c, layer, true);
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while the previous kernel in the stream drains; it must call pdl_wait()
+// before touching anything the predecessor writes or reads.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Every kernel launch of this library bumps this counter (ds_launch_count()).
 extern unsigned long long g_launches;
 inline void count_launch(int n = 1) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
