@@ -154,6 +154,15 @@ DS_API int ds_recompute_group(const ds_model* m, const int64_t* tokens_dev, int3
 DS_API int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, const ds_kv_cache* kv,
                      float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Greedy decode (decode_greedy, model.py:751-788): tokens_out[0] = *first_token
+ * (argmax of the prefill logits); each further step runs the previous token at
+ * the next position through every layer over kv (appending its K/V at
+ * positions, positions+1, ... -- the cache needs that capacity) and takes the
+ * argmax (lowest id on ties).  Device int32 in/out. */
+DS_API int ds_decode_greedy(const ds_model* m, const ds_kv_cache* kv, int32_t positions, const int32_t* first_token,
+                            int32_t steps, int32_t* tokens_out, void* workspace, size_t workspace_bytes,
+                            void* stream);
+
 /* ---- producer -> consumer over NVLink (P2P pull through CUDA IPC) ----
  * The producer exports a device buffer once; a consumer process maps it and
  * hands the mapped pointer to ds_kv_ingest (ds_kv_cache.k/v or layer_k/v) and

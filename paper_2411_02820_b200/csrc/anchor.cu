@@ -59,7 +59,7 @@ DS_DEV int gemv_row(const GemvArgs& a, int t, int r) {
   return head * a.head_dim + (r < 4 ? j0 + r : half + j0 + r - 4);
 }
 
-__global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
+__global__ void __launch_bounds__(GEMV_THREADS, 4) gemv_kernel(GemvArgs a) {
   extern __shared__ __align__(16) uint8_t smem_x[];
   bf16* xs = reinterpret_cast<bf16*>(smem_x);
   __shared__ float red[GEMV_WARPS][GEMV_ROWS];
@@ -194,8 +194,23 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
   }
 }
 
-__global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t* token) {
-  *token = (int32_t)(0xFFFFFFFFu - (uint32_t)(*packed & 0xFFFFFFFFull));
+__global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t* token, int64_t* token64) {
+  const int32_t t = (int32_t)(0xFFFFFFFFu - (uint32_t)(*packed & 0xFFFFFFFFull));
+  if (token) *token = t;
+  if (token64) *token64 = t;
+}
+
+// Decode bookkeeping: dst32 = dst64 = *src (the greedy token that seeds the next step).
+__global__ void token_copy_kernel(const int32_t* src, int32_t* dst32, int64_t* dst64) {
+  const int32_t t = *src;
+  if (dst32) *dst32 = t;
+  if (dst64) *dst64 = t;
+}
+
+int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaStream_t stream) {
+  count_launch();
+  token_copy_kernel<<<1, 1, 0, stream>>>(src, dst32, dst64);
+  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
 int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
@@ -218,9 +233,9 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
                                                                                             : DS_ERR_CUDA;
 }
 
-int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, cudaStream_t stream) {
+int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream) {
   count_launch();
-  argmax_finalize_kernel<<<1, 1, 0, stream>>>(packed, token);
+  argmax_finalize_kernel<<<1, 1, 0, stream>>>(packed, token, token64);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 

@@ -64,6 +64,8 @@ struct Workspace {
   float* part_o;
   float* part_ml;
   unsigned long long* argmax;
+  int64_t* tok64;     // greedy token feeding the next decode step's embedding gather
+  float* logits_dec;  // [V] decode-step logits
   unsigned int* dec_count;  // [n_kv_heads] split-merge counters (zero between launches)
   size_t bytes;
 };
@@ -93,6 +95,8 @@ Workspace carve(const ds_dims& m, int n, void* base) {
   w.part_o = reinterpret_cast<float*>(take(4ull * splits * hd));
   w.part_ml = reinterpret_cast<float*>(take(8ull * splits * m.n_heads));
   w.argmax = reinterpret_cast<unsigned long long*>(take(8));
+  w.tok64 = reinterpret_cast<int64_t*>(take(8));
+  w.logits_dec = reinterpret_cast<float*>(take(4ull * m.vocab_size));
   w.dec_count = reinterpret_cast<unsigned int*>(take(4ull * m.n_kv_heads));
   w.bytes = off;
   return w;
@@ -260,7 +264,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a) {
 }
 
 // _final_logits + greedy first token (model.py:565-566, 779).
-int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token) {
+int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token, int64_t* token64 = nullptr) {
   const ds_dims& d = c.d;
   if (cudaMemsetAsync(c.w.argmax, 0, 8, c.s) != cudaSuccess) return cuda_fail("memset");
   GemvArgs g{};
@@ -274,7 +278,7 @@ int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token) {
   g.out_f32 = logits;
   g.argmax = c.w.argmax;
   DS_TRY(gemv_launch(g, c.s), "lm head");
-  if (token) DS_TRY(argmax_finalize_launch(c.w.argmax, token, c.s), "argmax");
+  if (token || token64) DS_TRY(argmax_finalize_launch(c.w.argmax, token, token64, c.s), "argmax");
   return DS_OK;
 }
 
@@ -307,19 +311,20 @@ int reset_counters(Ctx& c) {
 
 // wait_for (optional): per layer, an event the anchor's layer l must wait for
 // (the recompute of l on another stream); NULL entries need no wait.
-int anchor_pass(Ctx& c, const int64_t* tok, int P, float* logits, int32_t* token,
-                const cudaEvent_t* wait_for = nullptr) {
+// token_id: device pointer to the row's token id; P: its position.
+int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* token,
+                const cudaEvent_t* wait_for = nullptr, int64_t* token64 = nullptr) {
   const ds_dims& d = c.d;
   if (int rc = reset_counters(c)) return rc;
-  DS_TRY(rmsnorm_launch(c.m->embed, true, tok + P, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr, 1,
-                        c.s),
+  DS_TRY(rmsnorm_launch(c.m->embed, true, token_id, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr,
+                        1, c.s),
          "anchor seed");
   for (int l = 0; l < d.n_layers; ++l) {
     if (wait_for && wait_for[l] && cudaStreamWaitEvent(c.s, wait_for[l], 0) != cudaSuccess) return cuda_fail("wait");
     int rc = anchor_layer(c, l, P, c.w.h_a);
     if (rc) return rc;
   }
-  return lm_head(c, c.w.h_a, logits, token);
+  return lm_head(c, c.w.h_a, logits, token, token64);
 }
 
 const int64_t* stage_tokens(const int64_t* host, const int64_t* dev, int n, Workspace& w, cudaStream_t s) {
@@ -367,6 +372,33 @@ int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const int32_t* 
   }
   DS_TRY(kv_ingest_launch(*src, *dst, reused, n_reused, n_kv_heads, head_dim, window, (cudaStream_t)stream),
          "kv ingest");
+  return DS_OK;
+}
+
+int ds_decode_greedy(const ds_model* m, const ds_kv_cache* kv, int32_t positions, const int32_t* first_token,
+                     int32_t steps, int32_t* tokens_out, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if (steps < 1) return fail(DS_ERR_INVALID, "steps must be at least 1");
+  if (positions < 1) return fail(DS_ERR_INVALID, "cache must hold at least one position");
+  if ((long long)positions + steps > d.max_seq)
+    return fail(DS_ERR_INVALID, "decoding %d steps from %d positions exceeds max_seq %d", steps, positions, d.max_seq);
+  if (!first_token || !tokens_out) return fail(DS_ERR_INVALID, "first_token and tokens_out are required");
+  if ((rc = check_cache(kv, d, positions + steps - 1, "cache"))) return rc;
+  Workspace w = carve(d, positions + steps, workspace);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
+  Ctx c{m, d, w, kv, (cudaStream_t)stream};
+  // step 0's token is argmax of the prefill logits; each further step runs that
+  // token through every layer at the next position (model.py:771-787)
+  DS_TRY(token_copy_launch(first_token, tokens_out, w.tok64, c.s), "token copy");
+  for (int s = 1; s < steps; ++s) {
+    rc = anchor_pass(c, w.tok64, positions + s - 1, w.logits_dec, tokens_out + s, nullptr, w.tok64);
+    if (rc) return rc;
+  }
   return DS_OK;
 }
 
@@ -532,7 +564,7 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
       rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
       if (rc) return rc;
     }
-    return anchor_pass(c, tok, P, logits_out, token_out);
+    return anchor_pass(c, tok + P, P, logits_out, token_out);
   }
 
   // Two streams.  Copy stream: KV ingest, then the anchor pass layer by layer;
@@ -566,7 +598,7 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
     rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
     if (rc) return rc;
   }
-  rc = anchor_pass(cx, tok, P, logits_out, token_out, wait_for);
+  rc = anchor_pass(cx, tok + P, P, logits_out, token_out, wait_for);
   if (rc) return rc;
   cudaEventRecord(ev_join, xs);
   cudaStreamWaitEvent(cs, ev_join, 0);
@@ -610,7 +642,7 @@ int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, co
   if (!workspace || workspace_bytes < w.bytes)
     return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
   Ctx c{m, d, w, kv, (cudaStream_t)stream};
-  return anchor_pass(c, tokens_dev, n_tokens - 1, logits_out, token_out);
+  return anchor_pass(c, tokens_dev + (n_tokens - 1), n_tokens - 1, logits_out, token_out);
 }
 
 int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,

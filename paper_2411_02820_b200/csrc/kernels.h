@@ -106,7 +106,8 @@ struct GemvArgs {
 };
 
 int gemv_launch(const GemvArgs& a, cudaStream_t stream);
-int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, cudaStream_t stream);
+int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream);
+int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaStream_t stream);
 int decode_splits(int n_keys);
 int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_layer, long long head_stride,
                             long long page_stride, const int32_t* table, int n_keys, int n_heads, int n_kv_heads,
