@@ -504,7 +504,8 @@ def run_fanout(args, world, rank, local):
         step = lambda: sender.serve(prod, [(r, rc, n) for r in consumers], L)  # noqa
 
     run = step
-    use_graph = args.graph and args.transport == "p2p" and not producer
+    use_graph = bool(args.graph) and args.transport == "p2p" and not producer
+    graphed = bool(args.graph) and args.transport == "p2p"  # what the consumers do
     if not producer or args.transport == "nccl":
         with torch.cuda.stream(stream):
             step()
@@ -594,11 +595,14 @@ def run_fanout(args, world, rank, local):
             "config": {"workload": f"fan-out: 1 producer (GPU 0) -> {nc} consumer fine-tunes, Llama-3-8B-shaped, "
                                    f"n={n}, recompute [{L - k},{L - 1}] (BASELINE configs 3/4)",
                        "n_tokens": n, "recomputed_layers": k, "consumers": nc, "transport": args.transport,
-                       "parallelism": f"1 producer + {nc} consumers", "cuda_graph": bool(use_graph)},
+                       "parallelism": f"1 producer + {nc} consumers", "cuda_graph": graphed},
             "gpu_launches": launches,
             "e2e": {"value": nc * n / e2e_s if e2e_s > 0 else None, "unit": "tok/s", "ttft_p50_ms": e2e_s * 1e3,
                     "h2d_bytes_per_step": 8 * n * nc, "d2h_bytes_per_step": (4 * cfg.vocab_size + 4) * nc},
-            "roofline": ({"bound": "nvlink", "kernel": links[0]["kernel"], "achieved": links[0]["gbs"],
+            "roofline": ({"bound": "hbm" if args.same_device else "nvlink",
+                          "kernel": links[0]["kernel"] + (" (same device: debug run, not NVLink)"
+                                                          if args.same_device else ""),
+                          "achieved": links[0]["gbs"],
                           "peak": 770.0, "unit": "GB/s", "frac": links[0]["gbs"] / 770.0, "traffic": None,
                           "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900"}
                          if links else None),

@@ -59,7 +59,7 @@ DS_DEV int gemv_row(const GemvArgs& a, int t, int r) {
   return head * a.head_dim + (r < 4 ? j0 + r : half + j0 + r - 4);
 }
 
-__global__ void __launch_bounds__(GEMV_THREADS, 4) gemv_kernel(GemvArgs a) {
+__global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
   extern __shared__ __align__(16) uint8_t smem_x[];
   bf16* xs = reinterpret_cast<bf16*>(smem_x);
   __shared__ float red[GEMV_WARPS][GEMV_ROWS];
@@ -243,16 +243,19 @@ int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int
 //
 // One CTA per (kv head g, split of DEC_SPLIT keys), 4 warps.  The R = H/KVH
 // query heads of the group are the M rows of an m16n8k16 tensor-core tile
-// (rows >= R are zero), so the scores and P.V run on the tensor pipe instead
-// of per-key scalar loops.  Keys stream in 64-key pages (one contiguous 64 x D
-// block per page) through a 2-stage cp.async ring with an XOR swizzle
-// (conflict-free ldmatrix); warp w owns keys [16w, 16w+16) of every page and
-// keeps its own online-softmax state and O accumulator; the 4 warps merge in
-// shared memory, and the last CTA of the kv head merges all splits.
+// (rows >= R are zero), so scores and P.V run on the tensor pipe.  Operand
+// fragments are loaded straight from global memory into registers (K rows are
+// already in the B-fragment order; V fragments are transposed in registers
+// with movmatrix), so the kernel needs no shared memory for K/V: it co-resides
+// with the persistent tcgen05 GEMMs of the recompute running on the other
+// stream (their 194 KB shared-memory rings leave ~30 KB per SM).  Warp w owns
+// 16-key blocks w, w+4, ... of the split with its own online softmax; the 4
+// warps merge through a small shared buffer, and the last CTA of the kv head
+// merges all splits.
 
 constexpr int DEC_THREADS = 128;
-constexpr int DEC_PAGE = 64;
-constexpr int DEC_SPLIT = 256;  // keys per CTA (4 pages)
+constexpr int DEC_BLOCK = 16;    // keys per warp step (one mma k-step for P.V)
+constexpr int DEC_SPLIT = 256;   // keys per CTA
 constexpr int DEC_MAX_R = 16;
 
 struct DecArgs {
@@ -269,95 +272,107 @@ struct DecArgs {
   float scale_log2;
 };
 
+DS_DEV uint32_t ld_b32(const bf16* p, bool ok) {
+  uint32_t r = 0;
+  if (ok) r = __ldg(reinterpret_cast<const unsigned int*>(p));
+  return r;
+}
+DS_DEV uint32_t movm_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 template <int D>
 __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int TILE = DEC_PAGE * D * 2;           // bytes of one page (K or V)
-  constexpr int CH = D / 8;                        // 16-byte chunks per row
-  const uint32_t sQ = smem_u32(smem);              // [16][D] bf16 swizzled
-  const uint32_t sKV = sQ + 16 * D * 2;            // [2 stages][K page | V page]
-  float* red = reinterpret_cast<float*>(smem + 16 * D * 2 + 4 * TILE);  // [4 warps][16 rows][D + 2]
+  extern __shared__ __align__(16) float red[];  // [4 warps][R][D + 2]
   __shared__ unsigned int is_last;
-
   const int g = blockIdx.x, split = blockIdx.y, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const int gr = lane >> 2, t4 = lane & 3;
   const int R = a.n_heads / a.n_kv_heads;
   const int key0 = split * DEC_SPLIT;
   const int nk_split = min(DEC_SPLIT, a.n_keys - key0);
-  const int n_pages = (nk_split + DEC_PAGE - 1) / DEC_PAGE;
+  const int n_blocks = (nk_split + DEC_BLOCK - 1) / DEC_BLOCK;
+  const bf16* kh = a.k + (long long)g * a.head_stride;
+  const bf16* vh = a.v + (long long)g * a.head_stride;
 
-  // the split's cache pages (except the anchor's own row, written by the
-  // predecessor) are already in HBM: stream them toward L2, then wait (PDL)
-  if (tid < n_pages) {
-    const int pos = key0 + tid * DEC_PAGE;
+  // the split's cache rows (except the anchor's own, written by the predecessor)
+  // are in HBM already: stream them toward L2, then wait for the predecessor (PDL)
+  if (tid < (nk_split + 63) / 64) {
+    const int pos = key0 + tid * 64;
     const int page = a.table ? __ldg(a.table + (pos >> 6)) : (pos >> 6);
-    const long long off = (long long)g * a.head_stride + (long long)page * a.page_stride;
-    const uint32_t bytes = (uint32_t)min(DEC_PAGE, a.n_keys - pos) * D * 2;
-    prefetch_l2(a.k + off, bytes);
-    prefetch_l2(a.v + off, bytes);
+    const long long off = (long long)page * a.page_stride;
+    const uint32_t bytes = (uint32_t)min(64, a.n_keys - pos) * D * 2;
+    prefetch_l2(kh + off, bytes);
+    prefetch_l2(vh + off, bytes);
   }
   pdl_trigger();
   pdl_wait();
-  // Q rows 0..R-1 = the group's heads, rows R..15 zero
-  for (int i = tid; i < 16 * CH; i += DEC_THREADS) {
-    const int r = i / CH, c = i % CH;
-    const bool ok = r < R;
-    cp_async16(sQ + swz<D>(r, c), a.q + (ok ? ((long long)(g * R + r) * D + c * 8) : 0), ok);
-  }
-  auto load_page = [&](int t) {
-    const int pos = key0 + t * DEC_PAGE;
-    const int rows = min(DEC_PAGE, a.n_keys - pos);
-    const int page = a.table ? __ldg(a.table + (pos >> 6)) : (pos >> 6);
-    const long long off = (long long)g * a.head_stride + (long long)page * a.page_stride;
-    const uint32_t base = sKV + (t & 1) * 2 * TILE;
-    for (int i = tid; i < DEC_PAGE * CH; i += DEC_THREADS) {
-      const int r = i / CH, c = i % CH;
-      const bool ok = r < rows;  // rows past the last key are zero-filled
-      const long long src = ok ? (long long)r * D + c * 8 : 0;
-      cp_async16(base + swz<D>(r, c), a.k + off + src, ok);
-      cp_async16(base + TILE + swz<D>(r, c), a.v + off + src, ok);
-    }
-  };
-  load_page(0);
-  cp_async_commit();
 
+  // Q as A fragments: rows 0..R-1 = the group's heads, rows >= R zero
   uint32_t qf[D / 16][4];
+  {
+    const bf16* qg = a.q + (long long)g * R * D;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks) {
+      const int c = ks * 16 + 2 * t4;
+      qf[ks][0] = ld_b32(qg + gr * D + c, gr < R);
+      qf[ks][1] = ld_b32(qg + (gr + 8) * D + c, gr + 8 < R);
+      qf[ks][2] = ld_b32(qg + gr * D + c + 8, gr < R);
+      qf[ks][3] = ld_b32(qg + (gr + 8) * D + c + 8, gr + 8 < R);
+    }
+  }
   float acc_o[D / 8][4];
 #pragma unroll
   for (int i = 0; i < D / 8; ++i) acc_o[i][0] = acc_o[i][1] = acc_o[i][2] = acc_o[i][3] = 0.f;
   float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
-  const int t4 = lane & 3;
 
-  for (int t = 0; t < n_pages; ++t) {
-    if (t + 1 < n_pages) load_page(t + 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    if (t == 0) {
+  auto row_ptr = [&](const bf16* base, int key) {
+    const int page = a.table ? __ldg(a.table + (key >> 6)) : (key >> 6);
+    return base + (long long)page * a.page_stride + (long long)(key & 63) * D;
+  };
+
+  for (int b = warp; b < n_blocks; b += 4) {
+    const int kb = key0 + b * DEC_BLOCK;
+    // K fragments (B of S = Q K^T, n = key): key kb + 8nt + gr, dims 16ks + 2t4 (+8)
+    uint32_t kf[2][D / 16][2];
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks)
-        ldsm_x4(sQ + swz<D>(lane & 15, ks * 2 + (lane >> 4)), qf[ks][0], qf[ks][1], qf[ks][2], qf[ks][3]);
+    for (int nt = 0; nt < 2; ++nt) {
+      const int key = kb + nt * 8 + gr;
+      const bool ok = key < a.n_keys;
+      const bf16* kr = row_ptr(kh, ok ? key : kb);
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        kf[nt][ks][0] = ld_b32(kr + ks * 16 + 2 * t4, ok);
+        kf[nt][ks][1] = ld_b32(kr + ks * 16 + 8 + 2 * t4, ok);
+      }
     }
-    const uint32_t sK = sKV + (t & 1) * 2 * TILE, sV = sK + TILE;
-    // S = Q K^T over this warp's 16 keys (two n-tiles of 8)
+    // V rows (key kb + gr and kb + 8 + gr, dims 8i + 2t4), transposed below
+    uint32_t vr[D / 8][2];
+    {
+      const int k0 = kb + gr, k1 = kb + 8 + gr;
+      const bool ok0 = k0 < a.n_keys, ok1 = k1 < a.n_keys;
+      const bf16* v0 = row_ptr(vh, ok0 ? k0 : kb);
+      const bf16* v1 = row_ptr(vh, ok1 ? k1 : kb);
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        vr[i][0] = ld_b32(v0 + i * 8 + 2 * t4, ok0);
+        vr[i][1] = ld_b32(v1 + i * 8 + 2 * t4, ok1);
+      }
+    }
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
     for (int ks = 0; ks < D / 16; ++ks) {
-      uint32_t b0, b1, b2, b3;
-      const int r = warp * 16 + (lane & 7) + ((lane >> 4) << 3);
-      ldsm_x4(sK + swz<D>(r, ks * 2 + ((lane >> 3) & 1)), b0, b1, b2, b3);
-      mma_bf16_16816(s[0], qf[ks], b0, b1);
-      mma_bf16_16816(s[1], qf[ks], b2, b3);
+      mma_bf16_16816(s[0], qf[ks], kf[0][ks][0], kf[0][ks][1]);
+      mma_bf16_16816(s[1], qf[ks], kf[1][ks][0], kf[1][ks][1]);
     }
-    // keys past the end of the window -> -inf
-    const int kbase = key0 + t * DEC_PAGE + warp * 16;
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      const int kp = kbase + nt * 8 + 2 * t4;
+      const int kp = kb + nt * 8 + 2 * t4;
       if (kp >= a.n_keys) s[nt][0] = s[nt][2] = -INFINITY;
       if (kp + 1 >= a.n_keys) s[nt][1] = s[nt][3] = -INFINITY;
     }
-    // online softmax (row g in [0], [1]; row g + 8 in [2], [3])
     float mx[2] = {m_r[0], m_r[1]};
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -372,7 +387,6 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
     float corr[2], msc[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      // a warp whose keys are all past the end keeps -inf: guard exp2(-inf - -inf)
       corr[r] = mx[r] == -INFINITY ? 1.f : exp2f((m_r[r] - mx[r]) * a.scale_log2);
       m_r[r] = mx[r];
       msc[r] = mx[r] == -INFINITY ? 0.f : mx[r] * a.scale_log2;
@@ -398,56 +412,47 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
       acc_o[i][1] *= corr[0];
       acc_o[i][2] *= corr[1];
       acc_o[i][3] *= corr[1];
+      // B of O += P V (k = key, n = dim): transpose the two 8x8 row tiles
+      mma_bf16_16816(acc_o[i], pa, movm_trans(vr[i][0]), movm_trans(vr[i][1]));
     }
-    // O += P V over the warp's 16 keys (one k-step)
-#pragma unroll
-    for (int i = 0; i < D / 16; ++i) {
-      uint32_t b0, b1, b2, b3;
-      const int r = warp * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
-      ldsm_x4_t(sV + swz<D>(r, i * 2 + (lane >> 4)), b0, b1, b2, b3);
-      mma_bf16_16816(acc_o[2 * i], pa, b0, b1);
-      mma_bf16_16816(acc_o[2 * i + 1], pa, b2, b3);
-    }
-    __syncthreads();
   }
-  cp_async_wait<0>();
 
-  // ---- merge the 4 warps: per row m, l and the unnormalised O
+  // ---- merge the 4 warps (rows < R only): m, l and the unnormalised O
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
     l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
   }
-  constexpr int RS = D + 2;  // [m, l, O...] per (warp, row)
-  const int gr = lane >> 2;
-  float* mine = red + (warp * 16) * RS;
+  constexpr int RS = D + 2;
+  float* mine = red + warp * R * RS;
 #pragma unroll
-  for (int i = 0; i < D / 8; ++i) {
-    const int col = i * 8 + 2 * t4;
-    mine[gr * RS + 2 + col] = acc_o[i][0];
-    mine[gr * RS + 2 + col + 1] = acc_o[i][1];
-    mine[(gr + 8) * RS + 2 + col] = acc_o[i][2];
-    mine[(gr + 8) * RS + 2 + col + 1] = acc_o[i][3];
-  }
-  if (t4 == 0) {
-    mine[gr * RS] = m_r[0];
-    mine[gr * RS + 1] = l_r[0];
-    mine[(gr + 8) * RS] = m_r[1];
-    mine[(gr + 8) * RS + 1] = l_r[1];
+  for (int half = 0; half < 2; ++half) {
+    const int row = gr + 8 * half;
+    if (row < R) {
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) {
+        mine[row * RS + 2 + i * 8 + 2 * t4] = acc_o[i][2 * half];
+        mine[row * RS + 2 + i * 8 + 2 * t4 + 1] = acc_o[i][2 * half + 1];
+      }
+      if (t4 == 0) {
+        mine[row * RS] = m_r[half];
+        mine[row * RS + 1] = l_r[half];
+      }
+    }
   }
   __syncthreads();
   for (int idx = tid; idx < R * D; idx += DEC_THREADS) {
     const int r = idx / D, d = idx % D, h = g * R + r;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * 16 + r) * RS]);
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * R + r) * RS]);
     float o = 0.f, lsum = 0.f;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      const float mw = red[(w * 16 + r) * RS];
+      const float mw = red[(w * R + r) * RS];
       const float wt = mw == -INFINITY ? 0.f : exp2f((mw - M) * a.scale_log2);
-      o += wt * red[(w * 16 + r) * RS + 2 + d];
-      lsum += wt * red[(w * 16 + r) * RS + 1];
+      o += wt * red[(w * R + r) * RS + 2 + d];
+      lsum += wt * red[(w * R + r) * RS + 1];
     }
     a.part_o[((long long)h * a.splits + split) * D + d] = o;
     if (d == 0) {
@@ -462,8 +467,8 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  float* wts = red;  // [R][splits]
-  float* den = wts + DEC_MAX_R * a.splits;
+  float* wts = red;  // [R][splits] then den[R]
+  float* den = wts + R * a.splits;
   for (int r = warp; r < R; r += DEC_THREADS / 32) {
     const float* ml = a.part_ml + (long long)(g * R + r) * a.splits * 2;
     float M = -INFINITY;
@@ -494,11 +499,6 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
 
 int decode_splits(int n_keys) { return (n_keys + DEC_SPLIT - 1) / DEC_SPLIT; }
 
-template <int D>
-static int dec_smem() {
-  return 16 * D * 2 + 4 * DEC_PAGE * D * 2 + 4 * 16 * (D + 2) * 4;
-}
-
 int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_layer, long long head_stride,
                             long long page_stride, const int32_t* table, int n_keys, int n_heads, int n_kv_heads,
                             int head_dim, float* part_o, float* part_ml, unsigned int* counters, bf16* out,
@@ -506,35 +506,23 @@ int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_la
   const int R = n_heads / n_kv_heads;
   if (R > DEC_MAX_R || (head_dim != 64 && head_dim != 128)) return DS_ERR_INVALID;
   const int splits = decode_splits(n_keys);
-  const int smem = head_dim == 128 ? dec_smem<128>() : dec_smem<64>();
-  if ((DEC_MAX_R + 1) * splits * 4 > 4 * 16 * (head_dim + 2) * 4) return DS_ERR_INVALID;  // merge scratch
+  // shared memory: the 4-warp merge [4][R][D+2], reused for the split merge [R][splits] + [R]
+  int smem = 4 * R * (head_dim + 2) * 4;
+  const int merge = (R * splits + R) * 4;
+  if (merge > smem) smem = merge;
+  if (smem > 200 * 1024) return DS_ERR_INVALID;
   DecArgs a{q, k_layer, v_layer, head_stride, page_stride, table, n_keys, n_heads, n_kv_heads, head_dim, splits,
             part_o, part_ml, counters, out, (float)(1.4426950408889634 / sqrt((double)head_dim))};
   count_launch();
+  cudaError_t e;
   if (head_dim == 128) {
-    static bool set = false;
-    if (!set) {
-      if (cudaFuncSetAttribute(decode_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-          cudaSuccess)
-        return DS_ERR_CUDA;
-      set = true;
-    }
-    if (launch_pdl(decode_attn_kernel<128>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a) !=
-        cudaSuccess)
-      return DS_ERR_CUDA;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(decode_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = launch_pdl(decode_attn_kernel<128>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a);
   } else {
-    static bool set = false;
-    if (!set) {
-      if (cudaFuncSetAttribute(decode_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-          cudaSuccess)
-        return DS_ERR_CUDA;
-      set = true;
-    }
-    if (launch_pdl(decode_attn_kernel<64>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a) !=
-        cudaSuccess)
-      return DS_ERR_CUDA;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(decode_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = launch_pdl(decode_attn_kernel<64>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a);
   }
-  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return e == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
 }  // namespace ds
