@@ -209,6 +209,8 @@ __global__ void token_copy_kernel(const int32_t* src, int32_t* dst32, int64_t* d
 
 int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaStream_t stream) {
   count_launch();
+  static const bool c0 = prefer_max_smem(token_copy_kernel);
+  (void)c0;
   token_copy_kernel<<<1, 1, 0, stream>>>(src, dst32, dst64);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
@@ -229,12 +231,16 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
   const int cap = num_sms() * per_sm;
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
+  static const bool c0 = prefer_max_smem(gemv_kernel);
+  (void)c0;
   return launch_pdl(gemv_kernel, dim3(grid), dim3(GEMV_THREADS), smem, stream, a) == cudaSuccess ? DS_OK
                                                                                             : DS_ERR_CUDA;
 }
 
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream) {
   count_launch();
+  static const bool c0 = prefer_max_smem(argmax_finalize_kernel);
+  (void)c0;
   argmax_finalize_kernel<<<1, 1, 0, stream>>>(packed, token, token64);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
@@ -515,6 +521,8 @@ int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_la
             part_o, part_ml, counters, out, (float)(1.4426950408889634 / sqrt((double)head_dim))};
   count_launch();
   cudaError_t e;
+  static const bool c0 = prefer_max_smem(decode_attn_kernel<128>) && prefer_max_smem(decode_attn_kernel<64>);
+  (void)c0;
   if (head_dim == 128) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(decode_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     e = launch_pdl(decode_attn_kernel<128>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a);

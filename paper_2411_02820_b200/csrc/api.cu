@@ -588,7 +588,8 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
   cudaEventRecord(ev_fork, cs);
   cudaStreamWaitEvent(xs, ev_fork, 0);
   if (!reused.empty())
-    DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P, xs),
+    DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P, xs,
+                            /*background=*/true),
            "kv ingest");
   c.layer_ready = ev_layer;
   Ctx cx{m, d, w, out_kv, xs};

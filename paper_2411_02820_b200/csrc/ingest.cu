@@ -14,7 +14,7 @@
 
 namespace ds {
 
-constexpr int INGEST_STAGES = 4;
+constexpr int INGEST_STAGES_MAX = 4;
 
 // Per-(reused layer) K/V bases travel by value (graph-capturable, 4 KB of
 // kernel parameters); they may point into a peer GPU's HBM (P2P pull).
@@ -46,13 +46,14 @@ DS_DEV void ingest_unit(const IngestArgs& a, int u, const uint8_t*& src, uint8_t
   dst = (kv ? a.dst_v[li] : a.dst_k[li]) + h * a.dst_head_stride + dp * a.dst_page_stride;
 }
 
-__global__ void __launch_bounds__(32) kv_ingest_kernel(const __grid_constant__ IngestArgs a, int total_units, int stage_bytes) {
+__global__ void __launch_bounds__(32) kv_ingest_kernel(const __grid_constant__ IngestArgs a, int total_units, int stage_bytes,
+                                                       int stages) {
   extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t bars[INGEST_STAGES];
+  __shared__ __align__(8) uint64_t bars[INGEST_STAGES_MAX];
   if (threadIdx.x != 0) return;
   const int n_my = (total_units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   if (n_my <= 0) return;
-  for (int s = 0; s < INGEST_STAGES; ++s) mbar_init(&bars[s], 1);
+  for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
   fence_mbar_init();
 
   auto issue_load = [&](int i) {
@@ -60,23 +61,23 @@ __global__ void __launch_bounds__(32) kv_ingest_kernel(const __grid_constant__ I
     uint8_t* dst;
     uint32_t bytes;
     ingest_unit(a, (int)blockIdx.x + i * (int)gridDim.x, src, dst, bytes);
-    const int s = i % INGEST_STAGES;
+    const int s = i % stages;
     mbar_expect_tx(&bars[s], bytes);
     bulk_g2s(ring + s * stage_bytes, src, bytes, &bars[s]);
   };
 
-  const int pro = n_my < INGEST_STAGES ? n_my : INGEST_STAGES;
+  const int pro = n_my < stages ? n_my : stages;
   for (int i = 0; i < pro; ++i) issue_load(i);
   for (int i = 0; i < n_my; ++i) {
-    const int s = i % INGEST_STAGES;
-    mbar_wait(&bars[s], (uint32_t)(i / INGEST_STAGES) & 1u);
+    const int s = i % stages;
+    mbar_wait(&bars[s], (uint32_t)(i / stages) & 1u);
     const uint8_t* src;
     uint8_t* dst;
     uint32_t bytes;
     ingest_unit(a, (int)blockIdx.x + i * (int)gridDim.x, src, dst, bytes);
     bulk_s2g(dst, ring + s * stage_bytes, bytes);
     bulk_commit();
-    const int refill = i - 1 + INGEST_STAGES;
+    const int refill = i - 1 + stages;
     if (i >= 1 && refill < n_my) {
       bulk_wait_read<1>();  // the store of unit i-1 has finished reading its stage
       issue_load(refill);
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(32) kv_ingest_kernel(const __grid_constant__ I
 }
 
 int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
-                     int n_kv_heads, int head_dim, int window, cudaStream_t stream) {
+                     int n_kv_heads, int head_dim, int window, cudaStream_t stream, bool background) {
   if (n_layers <= 0 || window <= 0) return DS_OK;
   IngestArgs a;
   a.src_head_stride = src.head_stride * 2;
@@ -109,7 +110,11 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   a.window = window;
   a.n_pages = (window + kPage - 1) / kPage;
   const int stage_bytes = kPage * head_dim * 2;
-  const int smem = INGEST_STAGES * stage_bytes;
+  // foreground: 4-stage rings, up to 8 CTAs per SM (HBM roofline when alone);
+  // background: one 2-stage CTA per SM, small enough to share every SM with
+  // a persistent tcgen05 GEMM of the concurrent recompute
+  const int stages = background ? 2 : INGEST_STAGES_MAX;
+  const int smem = stages * stage_bytes;
   static int attr_smem = 0;
   if (smem > attr_smem) {
     if (cudaFuncSetAttribute(kv_ingest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -118,13 +123,15 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   }
   const long long total = (long long)n_layers * 2 * n_kv_heads * a.n_pages;
   if (total > 0x7fffffffLL) return DS_ERR_INVALID;
-  int per_sm = (200 * 1024) / (smem + 1024);
+  int per_sm = background ? 1 : (200 * 1024) / (smem + 1024);
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 8) per_sm = 8;
   long long grid = (long long)num_sms() * per_sm;
   if (grid > total) grid = total;
   count_launch();
-  kv_ingest_kernel<<<(int)grid, 32, smem, stream>>>(a, (int)total, stage_bytes);
+  static const bool c0 = prefer_max_smem(kv_ingest_kernel);
+  (void)c0;
+  kv_ingest_kernel<<<(int)grid, 32, smem, stream>>>(a, (int)total, stage_bytes, stages);
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 

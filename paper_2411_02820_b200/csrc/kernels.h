@@ -42,6 +42,15 @@ inline bool kv_layer_present(const ds_kv_cache& c, int layer) {
   return layer >= 0 && layer < c.n_layers && kv_layer_base(c, layer, false) && kv_layer_base(c, layer, true);
 }
 
+// Kernels of the two streams only share an SM when their shared-memory
+// carveouts agree: the tcgen05 GEMM / attention need the maximum, so every
+// kernel asks for it (otherwise an anchor GEMV waits for an SM to drain).
+template <typename F>
+inline bool prefer_max_smem(F* kern) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared) ==
+         cudaSuccess;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while the previous kernel in the stream drains; it must call pdl_wait()
 // before touching anything the predecessor writes or reads.
@@ -72,7 +81,7 @@ int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int 
                 cudaStream_t stream, int force_bn = 0, int max_ctas = 0);
 
 int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
-                     int n_kv_heads, int head_dim, int window, cudaStream_t stream);
+                     int n_kv_heads, int head_dim, int window, cudaStream_t stream, bool background = false);
 
 int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,
                    float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream);

@@ -78,6 +78,8 @@ int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int
                    float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream) {
   if (M <= 0) return DS_OK;
   count_launch();
+  static const bool c0 = prefer_max_smem(rmsnorm_kernel<true>) && prefer_max_smem(rmsnorm_kernel<false>);
+  (void)c0;
   if (x_bf16)
     rmsnorm_kernel<true><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
   else
