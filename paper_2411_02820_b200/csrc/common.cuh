@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -268,6 +269,15 @@ DS_DEV void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1
 template <int D>
 DS_DEV uint32_t swz(int r, int c) {
   return (uint32_t)(r * D * 2 + ((c ^ (r & 7)) << 4));
+}
+
+// (2^a, 2^b) with one packed half-precision MUFU op.
+DS_DEV float2 exp2_f16x2(float a, float b) {
+  uint32_t h, e;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));  // low half = a
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+  __half2 v = *reinterpret_cast<__half2*>(&e);
+  return __half22float2(v);
 }
 
 // ---------------------------------------------------------------- bf16 packing

@@ -53,28 +53,38 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
   const bool row_ok = row < e.M;
   const int col0 = nb * BN;
   if (e.mode == EPI_QKV_ROPE) {
+    // j outer, heads inner: one row's cos/sin chunk (16-byte vector loads of
+    // the f32 tables) serves every head of the tile
     const int D = e.head_dim;
     const int half = D >> 1;
     const int pos = e.pos0 + row;
-    for (int cb = 0; cb < BN; cb += D) {
-      const int gcol = col0 + cb;  // column within this launch's N range
-      if (gcol >= e.N) break;      // uniform across the warp
-      const int head = (gcol + e.n_offset) / D;
-      const bool is_q = head < e.n_heads;
-      const bool is_k = !is_q && head < e.n_heads + e.n_kv_heads;
-      for (int j = 0; j < half; j += 16) {
+    for (int j = 0; j < half; j += 16) {
+      float cs[16], sn[16];
+      if (row_ok) {
+        const float4* c4 = reinterpret_cast<const float4*>(e.rope_cos + (long long)pos * half + j);
+        const float4* s4 = reinterpret_cast<const float4*>(e.rope_sin + (long long)pos * half + j);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 c = __ldg(c4 + i), t = __ldg(s4 + i);
+          cs[4 * i] = c.x; cs[4 * i + 1] = c.y; cs[4 * i + 2] = c.z; cs[4 * i + 3] = c.w;
+          sn[4 * i] = t.x; sn[4 * i + 1] = t.y; sn[4 * i + 2] = t.z; sn[4 * i + 3] = t.w;
+        }
+      }
+      for (int cb = 0; cb < BN; cb += D) {
+        const int gcol = col0 + cb;  // column within this launch's N range
+        if (gcol >= e.N) break;      // uniform across the warp
+        const int head = (gcol + e.n_offset) / D;
+        const bool is_q = head < e.n_heads;
+        const bool is_k = !is_q && head < e.n_heads + e.n_kv_heads;
         float lo[16], hi[16];
         tmem_ld16x2(tbase + cb + j, tbase + cb + half + j, lo, hi);
         if (!row_ok) continue;
         if (is_q || is_k) {
-          const float* cs = e.rope_cos + (long long)pos * half + j;
-          const float* sn = e.rope_sin + (long long)pos * half + j;
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            float c = __ldg(cs + i), s = __ldg(sn + i);
-            float x1 = lo[i], x2 = hi[i];
-            lo[i] = x1 * c - x2 * s;
-            hi[i] = x1 * s + x2 * c;
+            const float x1 = lo[i], x2 = hi[i];
+            lo[i] = x1 * cs[i] - x2 * sn[i];
+            hi[i] = x1 * sn[i] + x2 * cs[i];
           }
         }
         uint32_t pl[8], ph[8];
