@@ -18,7 +18,7 @@ namespace ds {
 constexpr int GEMV_THREADS = 256;
 constexpr int GEMV_WARPS = GEMV_THREADS / 32;
 constexpr int GEMV_ROWS = 8;    // weight rows per tile
-constexpr int GEMV_UNROLL = 2;  // 16-byte chunks per row per thread in flight
+constexpr int GEMV_UNROLL = 1;  // 16-byte chunks per row per thread per pipeline unit
 
 DS_DEV uint4 ld_stream16(const void* p) {
   uint4 r;
@@ -59,7 +59,7 @@ DS_DEV int gemv_row(const GemvArgs& a, int t, int r) {
   return head * a.head_dim + (r < 4 ? j0 + r : half + j0 + r - 4);
 }
 
-__global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
+__global__ void __launch_bounds__(GEMV_THREADS, 1) gemv_kernel(GemvArgs a) {
   extern __shared__ __align__(16) uint8_t smem_x[];
   bf16* xs = reinterpret_cast<bf16*>(smem_x);
   __shared__ float red[GEMV_WARPS][GEMV_ROWS];
@@ -106,33 +106,54 @@ __global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
   }
   __syncthreads();
 
+  // ---- software-pipelined weight stream: a unit = (tile, k-block of
+  // 2 x 256 16-byte chunks per row); the next unit's 16 loads per thread are in
+  // flight while the current unit is reduced (registers, no shared staging)
   const int nchunk = a.K >> 3;
+  constexpr int KB = GEMV_UNROLL * GEMV_THREADS;  // chunks per k-block
+  const int kblocks = (nchunk + KB - 1) / KB;
   unsigned long long best = 0ull;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const bf16* wr[GEMV_ROWS];
+  uint4 cur[GEMV_UNROLL][GEMV_ROWS], nxt[GEMV_UNROLL][GEMV_ROWS];
+  auto load_unit = [&](int t, int kb, uint4 (&w)[GEMV_UNROLL][GEMV_ROWS]) {
 #pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) wr[r] = a.W + (long long)gemv_row(a, t, r) * a.ldw;
-    float s[GEMV_ROWS];
-#pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
-    int c = tid;
-    for (; c + (GEMV_UNROLL - 1) * GEMV_THREADS < nchunk; c += GEMV_UNROLL * GEMV_THREADS) {
-      uint4 w[GEMV_UNROLL][GEMV_ROWS];
-#pragma unroll
-      for (int u = 0; u < GEMV_UNROLL; ++u)
-#pragma unroll
-        for (int r = 0; r < GEMV_ROWS; ++r) w[u][r] = ld_stream16(wr[r] + (c + u * GEMV_THREADS) * 8);
+    for (int r = 0; r < GEMV_ROWS; ++r) {
+      const bf16* wr = a.W + (long long)gemv_row(a, t, r) * a.ldw;
 #pragma unroll
       for (int u = 0; u < GEMV_UNROLL; ++u) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(xs + (c + u * GEMV_THREADS) * 8);
-#pragma unroll
-        for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(w[u][r], xv);
+        const int c = kb * KB + u * GEMV_THREADS + tid;
+        w[u][r] = c < nchunk ? ld_stream16(wr + c * 8) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
-    for (; c < nchunk; c += GEMV_THREADS) {
-      const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
+  };
+  int t = blockIdx.x, kb = 0;
+  if (t < tiles) load_unit(t, 0, cur);
+  float s[GEMV_ROWS];
 #pragma unroll
-      for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(ld_stream16(wr[r] + c * 8), xv);
+  for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
+  while (t < tiles) {
+    int t2 = t, kb2 = kb + 1;
+    if (kb2 == kblocks) {
+      kb2 = 0;
+      t2 = t + gridDim.x;
+    }
+    if (t2 < tiles) load_unit(t2, kb2, nxt);
+#pragma unroll
+    for (int u = 0; u < GEMV_UNROLL; ++u) {
+      const int c = kb * KB + u * GEMV_THREADS + tid;
+      if (c < nchunk) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
+#pragma unroll
+        for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(cur[u][r], xv);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < GEMV_UNROLL; ++u)
+#pragma unroll
+      for (int r = 0; r < GEMV_ROWS; ++r) cur[u][r] = nxt[u][r];
+    if (kb != kblocks - 1) {
+      t = t2;
+      kb = kb2;
+      continue;
     }
 #pragma unroll
     for (int r = 0; r < GEMV_ROWS; ++r) {
@@ -183,6 +204,10 @@ __global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
       }
     }
     __syncthreads();  // red[] reused by the next tile
+#pragma unroll
+    for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
+    t = t2;
+    kb = kb2;
   }
   if (a.mode == EPI_STORE_F32 && a.argmax && tid < GEMV_ROWS) {
 #pragma unroll
@@ -226,9 +251,9 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
       return DS_ERR_CUDA;
     attr = smem;
   }
-  int per_sm = (200 * 1024) / (smem + 2048);
-  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
-  const int cap = num_sms() * per_sm;
+  // one CTA per SM: its registers hold two units of loads in flight, and it
+  // fits beside a persistent tcgen05 GEMM CTA of the concurrent recompute
+  const int cap = num_sms();
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
   static const bool c0 = prefer_max_smem(gemv_kernel);
