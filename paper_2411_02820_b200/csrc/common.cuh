@@ -271,6 +271,17 @@ DS_DEV uint32_t swz(int r, int c) {
   return (uint32_t)(r * D * 2 + ((c ^ (r & 7)) << 4));
 }
 
+// 2^x on the FMA pipe (Cody-Waite split + degree-3 polynomial, max relative
+// error 1.7e-4, far below the bf16 rounding of P): used for a fraction of the
+// softmax exponentials so the MUFU unit is not the attention bottleneck.
+DS_DEV float exp2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float xi = floorf(x);
+  const float f = x - xi;
+  const float p = fmaf(fmaf(fmaf(0.07632546f, f, 0.22830825f), f, 0.69503617f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((int)xi << 23));
+}
+
 // (2^a, 2^b) with one packed half-precision MUFU op.
 DS_DEV float2 exp2_f16x2(float a, float b) {
   uint32_t h, e;
