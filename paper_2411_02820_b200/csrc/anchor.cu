@@ -2,9 +2,9 @@
 // (_layer_single, model.py:547-562) and the first-token logits
 // (_final_logits + argmax, model.py:565-566, 779).  All HBM-bound:
 //
-//   gemv_kernel    y = W[N][K] . x over tiles of ROWS weight rows per CTA; the
-//                  128 threads split K (16-byte coalesced row chunks, all 16
-//                  loads per thread issued before anything else), fused epilogue:
+//   gemv_kernel    y = W[N][K] . x over tiles of 8 weight rows per CTA; the 256
+//                  threads split K (16-byte coalesced row chunks, 16 loads in
+//                  flight per thread), block-reduce, fused epilogue:
 //                  RoPE + q / KV-cache write, residual add, SiLU, logits +
 //                  packed argmax (lowest id on ties).  An f32 input is
 //                  RMSNorm'ed in the prologue (model.py:466-468).
@@ -15,9 +15,10 @@
 
 namespace ds {
 
-constexpr int GEMV_THREADS = 128;
+constexpr int GEMV_THREADS = 256;
 constexpr int GEMV_WARPS = GEMV_THREADS / 32;
-constexpr int GEMV_LOADS = 16;  // 16-byte weight chunks per thread per tile (all in flight at once)
+constexpr int GEMV_ROWS = 8;    // weight rows per tile
+constexpr int GEMV_UNROLL = 2;  // 16-byte chunks per row per thread in flight
 
 DS_DEV uint4 ld_stream16(const void* p) {
   uint4 r;
@@ -47,49 +48,29 @@ DS_DEV unsigned long long pack_argmax(float v, int idx) {
   return ((unsigned long long)key << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)idx);
 }
 
-// Global row of slot r of tile t (ROWS rows per tile).  QKV tiles hold ROWS/2
-// RoPE pairs (rows head*D + j0 + i and head*D + half + j0 + i) so the rotation
-// happens in the epilogue; other modes take ROWS consecutive rows.
-template <int ROWS>
+// Global row of slot r (0..7) of tile t.  QKV tiles hold 4 RoPE pairs
+// (rows head*D + j0 + i and head*D + half + j0 + i, i < 4) so the rotation
+// happens in the epilogue; other modes take 8 consecutive rows.
 DS_DEV int gemv_row(const GemvArgs& a, int t, int r) {
-  if (a.mode != EPI_QKV_ROPE) return t * ROWS + r;
-  constexpr int P2 = ROWS / 2;
+  if (a.mode != EPI_QKV_ROPE) return t * GEMV_ROWS + r;
   const int half = a.head_dim >> 1;
-  const int per_head = half / P2;
-  const int head = t / per_head, j0 = (t - head * per_head) * P2;
-  return head * a.head_dim + (r < P2 ? j0 + r : half + j0 + r - P2);
+  const int per_head = half / 4;
+  const int head = t / per_head, j0 = (t - head * per_head) * 4;
+  return head * a.head_dim + (r < 4 ? j0 + r : half + j0 + r - 4);
 }
 
-// One tile = ROWS weight rows x the whole K.  Every thread issues its
-// GEMV_LOADS 16-byte weight loads FIRST (they depend on nothing), then waits
-// for the predecessor kernel (PDL) and stages the (RMSNorm'ed) input vector in
-// shared memory while the loads are in flight, then reduces.  Many small CTAs
-// keep ~GEMV_LOADS x 16 B x threads of HBM requests in flight per SM.
-template <int ROWS>
-__global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
-  constexpr int CPT = GEMV_LOADS / ROWS;  // chunks per row per thread
+__global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
   extern __shared__ __align__(16) uint8_t smem_x[];
   bf16* xs = reinterpret_cast<bf16*>(smem_x);
-  __shared__ float red[GEMV_WARPS][ROWS];
+  __shared__ float red[GEMV_WARPS][GEMV_ROWS];
   __shared__ float ssq[GEMV_WARPS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tiles = a.N / ROWS;
-  const int nchunk = a.K >> 3;
+  const int tiles = a.N / GEMV_ROWS;
 
-  uint4 w[ROWS][CPT];
-  auto load_tile = [&](int t) {
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      const bf16* wr = a.W + (long long)gemv_row<ROWS>(a, t, r) * a.ldw;
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const int c = tid + i * GEMV_THREADS;
-        w[r][i] = c < nchunk ? ld_stream16(wr + c * 8) : make_uint4(0u, 0u, 0u, 0u);
-      }
-    }
-  };
-  int t = blockIdx.x;
-  if (t < tiles) load_tile(t);
+  // ---- weights do not depend on the predecessor kernel: start streaming this
+  // CTA's first tile into L2, let the successor launch, then wait (PDL)
+  if (blockIdx.x < tiles && tid < GEMV_ROWS)
+    prefetch_l2(a.W + (long long)gemv_row(a, blockIdx.x, tid) * a.ldw, (uint32_t)a.K * 2);
   pdl_trigger();
   pdl_wait();
 
@@ -106,10 +87,10 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
       for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       if (lane == 0) ssq[warp] = ss;
       __syncthreads();
-      float tot = 0.f;
+      float t = 0.f;
 #pragma unroll
-      for (int q = 0; q < GEMV_WARPS; ++q) tot += ssq[q];
-      inv = 1.0f / sqrtf(tot / (float)a.K + 1e-6f);
+      for (int w = 0; w < GEMV_WARPS; ++w) t += ssq[w];
+      inv = 1.0f / sqrtf(t / (float)a.K + 1e-6f);
     }
     for (int k = tid * 4; k < a.K; k += GEMV_THREADS * 4) {
       float4 v = *reinterpret_cast<const float4*>(a.x_f32 + k);
@@ -125,52 +106,56 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
   }
   __syncthreads();
 
+  const int nchunk = a.K >> 3;
   unsigned long long best = 0ull;
-  while (t < tiles) {
-    float s[ROWS];
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const bf16* wr[GEMV_ROWS];
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) s[r] = 0.f;
+    for (int r = 0; r < GEMV_ROWS; ++r) wr[r] = a.W + (long long)gemv_row(a, t, r) * a.ldw;
+    float s[GEMV_ROWS];
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      const int c = tid + i * GEMV_THREADS;
-      if (c < nchunk) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
+    for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
+    int c = tid;
+    for (; c + (GEMV_UNROLL - 1) * GEMV_THREADS < nchunk; c += GEMV_UNROLL * GEMV_THREADS) {
+      uint4 w[GEMV_UNROLL][GEMV_ROWS];
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r) s[r] += dot8(w[r][i], xv);
+      for (int u = 0; u < GEMV_UNROLL; ++u)
+#pragma unroll
+        for (int r = 0; r < GEMV_ROWS; ++r) w[u][r] = ld_stream16(wr[r] + (c + u * GEMV_THREADS) * 8);
+#pragma unroll
+      for (int u = 0; u < GEMV_UNROLL; ++u) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(xs + (c + u * GEMV_THREADS) * 8);
+#pragma unroll
+        for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(w[u][r], xv);
       }
     }
-    // rows longer than CPT x 128 chunks (not used by the 8B shapes): serial tail
-    for (int c = tid + CPT * GEMV_THREADS; c < nchunk; c += GEMV_THREADS) {
+    for (; c < nchunk; c += GEMV_THREADS) {
       const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r)
-        s[r] += dot8(ld_stream16(a.W + (long long)gemv_row<ROWS>(a, t, r) * a.ldw + c * 8), xv);
+      for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(ld_stream16(wr[r] + c * 8), xv);
     }
-    const int t_next = t + gridDim.x;
-    if (t_next < tiles) load_tile(t_next);  // next tile's loads overlap this tile's reduction
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
+    for (int r = 0; r < GEMV_ROWS; ++r) {
 #pragma unroll
       for (int o = 16; o; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
     }
     if (lane == 0) {
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r) red[warp][r] = s[r];
+      for (int r = 0; r < GEMV_ROWS; ++r) red[warp][r] = s[r];
     }
     __syncthreads();
-    if (tid < ROWS) {
+    if (tid < GEMV_ROWS) {
       float v = 0.f;
 #pragma unroll
-      for (int q = 0; q < GEMV_WARPS; ++q) v += red[q][tid];
+      for (int w = 0; w < GEMV_WARPS; ++w) v += red[w][tid];
       red[0][tid] = v;  // only thread tid touches column tid
     }
     __syncthreads();
     if (a.mode == EPI_QKV_ROPE) {
-      constexpr int P2 = ROWS / 2;
-      if (tid < P2) {
-        const int r0 = gemv_row<ROWS>(a, t, tid);
+      if (tid < 4) {
+        const int r0 = gemv_row(a, t, tid);
         const int head = r0 / a.head_dim, j = r0 - head * a.head_dim, half = a.head_dim >> 1;
-        float lo = red[0][tid], hi = red[0][tid + P2];
+        float lo = red[0][tid], hi = red[0][tid + 4];
         const bool is_q = head < a.n_heads, is_k = !is_q && head < a.n_heads + a.n_kv_heads;
         if (is_q || is_k) {
           const float cs = a.rope_cos[(long long)a.pos * half + j], sn = a.rope_sin[(long long)a.pos * half + j];
@@ -184,8 +169,8 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
         dst[j] = __float2bfloat16_rn(lo);
         dst[j + half] = __float2bfloat16_rn(hi);
       }
-    } else if (tid < ROWS) {
-      const int row = t * ROWS + tid;
+    } else if (tid < GEMV_ROWS) {
+      const int row = t * GEMV_ROWS + tid;
       const float v = red[0][tid];
       if (a.mode == EPI_RESID_F32) {
         a.out_f32[row] = a.resid[row] + v;
@@ -198,15 +183,14 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
       }
     }
     __syncthreads();  // red[] reused by the next tile
-    t = t_next;
   }
-  if (a.mode == EPI_STORE_F32 && a.argmax && warp == 0) {
+  if (a.mode == EPI_STORE_F32 && a.argmax && tid < GEMV_ROWS) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+    for (int o = 4; o; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0x000000ffu, best, o);
       best = other > best ? other : best;
     }
-    if (lane == 0 && best) atomicMax(a.argmax, best);
+    if (tid == 0 && best) atomicMax(a.argmax, best);
   }
 }
 
@@ -231,43 +215,26 @@ int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaSt
   return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
 }
 
-template <int ROWS>
-static int gemv_launch_t(const GemvArgs& a, cudaStream_t stream) {
-  const int tiles = a.N / ROWS;
+int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
+  if ((a.N % GEMV_ROWS) || (a.K & 7)) return DS_ERR_INVALID;
+  if (a.mode == EPI_QKV_ROPE && (a.head_dim % 8 || a.N % a.head_dim)) return DS_ERR_INVALID;
+  const int tiles = a.N / GEMV_ROWS;
   const int smem = a.K * 2;
   static int attr = 0;
-  static const bool c0 = prefer_max_smem(gemv_kernel<ROWS>);
-  (void)c0;
   if (smem > 48 * 1024 && smem > attr) {
-    if (cudaFuncSetAttribute(gemv_kernel<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return DS_ERR_CUDA;
     attr = smem;
   }
-  // one tile per CTA for the layer projections; the lm head (V/ROWS tiles)
-  // loops, staging x once per CTA
-  const int cap = num_sms() * 16;
+  int per_sm = (200 * 1024) / (smem + 2048);
+  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+  const int cap = num_sms() * per_sm;
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
-  return launch_pdl(gemv_kernel<ROWS>, dim3(grid), dim3(GEMV_THREADS), smem, stream, a) == cudaSuccess
-             ? DS_OK
-             : DS_ERR_CUDA;
-}
-
-int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
-  if (a.K & 7) return DS_ERR_INVALID;
-  // rows per tile: keep ~GEMV_LOADS chunks per thread for one full row pass
-  const int cpt = (a.K / 8 + GEMV_THREADS - 1) / GEMV_THREADS;
-  int rows = GEMV_LOADS / (cpt < 1 ? 1 : cpt);
-  rows = rows >= 8 ? 8 : rows >= 4 ? 4 : rows >= 2 ? 2 : 1;
-  if (a.mode == EPI_QKV_ROPE && rows < 2) rows = 2;
-  while (rows > 1 && (a.N % rows || (a.mode == EPI_QKV_ROPE && (a.head_dim / 2) % (rows / 2)))) rows >>= 1;
-  if (a.N % rows || (a.mode == EPI_QKV_ROPE && rows < 2)) return DS_ERR_INVALID;
-  switch (rows) {
-    case 8: return gemv_launch_t<8>(a, stream);
-    case 4: return gemv_launch_t<4>(a, stream);
-    case 2: return gemv_launch_t<2>(a, stream);
-    default: return gemv_launch_t<1>(a, stream);
-  }
+  static const bool c0 = prefer_max_smem(gemv_kernel);
+  (void)c0;
+  return launch_pdl(gemv_kernel, dim3(grid), dim3(GEMV_THREADS), smem, stream, a) == cudaSuccess ? DS_OK
+                                                                                            : DS_ERR_CUDA;
 }
 
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream) {

@@ -267,11 +267,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       uint32_t pk[FA_BN / 2];
 #pragma unroll
       for (int c = 0; c < FA_BN / 2; ++c) {
-        // one pair in four on the FMA pipe, the rest on MUFU
-        const float x0 = fmaf(__uint_as_float(sr[2 * c]), sc, -msc);
-        const float x1 = fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc);
-        const float p0 = (c & 3) == 3 ? exp2_poly(x0) : fast_exp2(x0);
-        const float p1 = (c & 3) == 3 ? exp2_poly(x1) : fast_exp2(x1);
+        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * c]), sc, -msc));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc));
         sum += p0 + p1;
         pk[c] = pack_bf16x2(p0, p1);
       }

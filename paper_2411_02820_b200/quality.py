@@ -81,6 +81,17 @@ def greedy_agreement(reference, candidate) -> Agreement:
                      tuple(int(t) for t in cand))
 
 
+def _receiver_reference(receiver, ids, horizon: int) -> np.ndarray:
+    """The receiver's own greedy stream: a recompute-all partial prefill (the
+    receiver's full prefill computed by the same kernels the candidates use, so
+    recompute-all agrees with it bit for bit, as model.py guarantees for the
+    reference: test_model.py:156-161) followed by ``horizon`` decode steps."""
+    cfg = receiver.config
+    cache = PagedKV.allocate(cfg, len(ids) + horizon, receiver.device)
+    own = partial_prefill(receiver, ids, RecomputeConfig.full(cfg.n_layers), None, out=cache)
+    return decode_greedy(receiver, cache, own.token_dev, horizon, positions=len(ids))
+
+
 def _prefill_with_capacity(model, ids, reserve: int, e_layers=None):
     kv = LayerKV.empty(model.config, len(ids) + reserve, model.device)
     res = full_prefill(model, ids, e_layers=e_layers, out=kv)
@@ -94,8 +105,7 @@ def agreement_score(sender, receiver, tokens, config: RecomputeConfig, horizon: 
     if horizon < 1:
         raise ValueError("horizon must be at least 1")
     ids = check_tokens(tokens, receiver.config)
-    ref = _prefill_with_capacity(receiver, ids, horizon)
-    ref_tokens = decode_greedy(receiver, ref.kv, ref, horizon)
+    ref_tokens = _receiver_reference(receiver, ids, horizon)
     sent = full_prefill(sender, ids, e_layers=config.transition_layers)
     cand_tokens = _mixed_decode(receiver, ids, config, sent, horizon)
     return greedy_agreement(ref_tokens, cand_tokens)
@@ -121,9 +131,7 @@ class PairEvaluator:
         self.items = []
         for seq in train_set:
             ids = check_tokens(seq, receiver.config)
-            ref = _prefill_with_capacity(receiver, ids, horizon)
-            ref_tokens = decode_greedy(receiver, ref.kv, ref, horizon)
-            del ref
+            ref_tokens = _receiver_reference(receiver, ids, horizon)
             sent = full_prefill(sender, ids)  # profiling mode: E at every layer
             self.items.append((ids, sent, ref_tokens))
 

@@ -95,7 +95,10 @@ def test_agreement_score_first_token_identity(pair):
     # within the logit tolerance (this prefix has a 0.005 top-2 gap, so they may differ)
     _, _, _, lg = O.full_prefill(oB, toks)
     assert lg.max() - lg[ag.reference[0]] < TOL and lg.max() - lg[ag.candidate[0]] < TOL
-    print(f"recompute-all self agreement over 8 tokens: {ag.score}")
+    # the receiver's reference stream and the recompute-all candidate run the same
+    # deterministic kernels: identical streams (the reference's recompute-all
+    # bitwise-equals-full invariant, test_model.py:156-161)
+    assert ag.score == 1.0 and ag.first_divergence is None
     g = greedy_agreement([1, 2, 3, 4], [1, 2, 9, 4])
     assert g.score == 0.75 and g.first_divergence == 2
     with pytest.raises(ValueError):
