@@ -366,6 +366,18 @@ def run_ours(args, world, rank, local):
             full_ms.append(s_ev.elapsed_time(e_ev))
     full_ttft = max_over_ranks(statistics.median(full_ms), world)
 
+    # ---- greedy first-token agreement, consumer partial prefill vs its own full
+    # prefill, over a few 8K prefixes (outside the timed region)
+    agree, n_pref = 0, 4
+    for i in range(n_pref):
+        ids_i = np.random.default_rng(100 + i).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
+        t_i = torch.from_numpy(ids_i).to(dev)
+        prod_i = P.full_prefill(A, ids_i, e_layers=rc.transition_layers, tokens_dev=t_i)
+        mixed_i = P.partial_prefill(B, ids_i, rc, prod_i.kv, prod_i.e_map(), tokens_dev=t_i)
+        own_i = P.full_prefill(B, ids_i, e_layers=(), tokens_dev=t_i)
+        agree += int(mixed_i.token == own_i.token)
+        del prod_i, mixed_i, own_i
+
     # ---- per-kernel rooflines (CUDA events on the launching stream, same shapes as the step)
     Pn = n - 1
     d, F, HD, KVD = cfg.d_model, cfg.d_ff, cfg.n_heads * cfg.head_dim, cfg.n_kv_heads * cfg.head_dim
@@ -418,6 +430,8 @@ def run_ours(args, world, rank, local):
             "full_prefill": {"ttft_p50_ms": full_ttft, "tok_s": n / (full_ttft / 1e3),
                              "speedup_reuse_vs_full": full_ttft / ttft_ms},
             "first_token": token,
+            "first_token_agreement": {"partial_vs_own_full_prefill": agree, "prefixes": n_pref,
+                                      "note": "random-init pair: B = A + noise on the recomputed suffix"},
             "gpu_launches": int(launches),
             "e2e": {"value": world * n / e2e_ttft, "unit": "tok/s", "ttft_p50_ms": e2e_ttft * 1e3,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * cfg.vocab_size + 4},

@@ -212,7 +212,7 @@ int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaSt
   static const bool c0 = prefer_max_smem(token_copy_kernel);
   (void)c0;
   token_copy_kernel<<<1, 1, 0, stream>>>(src, dst32, dst64);
-  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_status();
 }
 
 int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
@@ -222,8 +222,7 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
   const int smem = a.K * 2;
   static int attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
-    if (cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return DS_ERR_CUDA;
+    if (int rc_ = launch_status(cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return rc_;
     attr = smem;
   }
   int per_sm = (200 * 1024) / (smem + 2048);
@@ -233,8 +232,7 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
   count_launch();
   static const bool c0 = prefer_max_smem(gemv_kernel);
   (void)c0;
-  return launch_pdl(gemv_kernel, dim3(grid), dim3(GEMV_THREADS), smem, stream, a) == cudaSuccess ? DS_OK
-                                                                                            : DS_ERR_CUDA;
+  return launch_status(launch_pdl(gemv_kernel, dim3(grid), dim3(GEMV_THREADS), smem, stream, a));
 }
 
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream) {
@@ -242,7 +240,7 @@ int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int
   static const bool c0 = prefer_max_smem(argmax_finalize_kernel);
   (void)c0;
   argmax_finalize_kernel<<<1, 1, 0, stream>>>(packed, token, token64);
-  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_status();
 }
 
 // ---------------------------------------------------------------- decode attention
@@ -530,7 +528,7 @@ int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_la
     if (smem > 48 * 1024) cudaFuncSetAttribute(decode_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     e = launch_pdl(decode_attn_kernel<64>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a);
   }
-  return e == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_status(e);
 }
 
 }  // namespace ds

@@ -316,21 +316,20 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
                         int n_heads, int n_kv_heads, bf16* o, long long ldo, cudaStream_t stream) {
   using L = FaTcSmem<D>;
   CUtensorMap tq, tk, tv;
-  if (make_tmap_bf16(&tq, q, n_q, (long long)n_heads * D, ldq, FA_BM, 64)) return DS_ERR_CUDA;
-  if (make_tmap_bf16(&tk, k_layer, layer_rows, D, D, 64, 64)) return DS_ERR_CUDA;
-  if (make_tmap_bf16(&tv, v_layer, layer_rows, D, D, 64, 64)) return DS_ERR_CUDA;
+  if (make_tmap_bf16(&tq, q, n_q, (long long)n_heads * D, ldq, FA_BM, 64) ||
+      make_tmap_bf16(&tk, k_layer, layer_rows, D, D, 64, 64) || make_tmap_bf16(&tv, v_layer, layer_rows, D, D, 64, 64))
+    return launch_status(cudaErrorInvalidValue);
   FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, head_stride / D, page_stride / D, table, o, ldo,
              (float)(1.4426950408889634 / sqrt((double)D))};
   static bool set = false;
   if (!set) {
-    if (cudaFuncSetAttribute(fa_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
-      return DS_ERR_CUDA;
+    if (int rc_ = launch_status(cudaFuncSetAttribute(fa_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL))) return rc_;
     set = true;
   }
   dim3 grid(n_heads, (n_q + 2 * FA_BM - 1) / (2 * FA_BM));
   count_launch();
   fa_tc_kernel<D><<<grid, FA_THREADS, L::TOTAL, stream>>>(tq, tk, tv, a);
-  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_status();
 }
 
 int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,

@@ -50,6 +50,20 @@ DS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Same, with a suspend-time hint: the waiting warp sleeps in hardware until the
+// phase completes (or the hint expires) instead of re-issuing the try_wait, so
+// long waits do not steal issue slots from the warps doing the work.
+DS_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
 DS_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -228,6 +242,14 @@ DS_DEV void tmem_st32_nowait(uint32_t taddr, const uint32_t* r) {
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+DS_DEV void tmem_st16_nowait(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 DS_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 DS_DEV float fast_exp2(float x) {
@@ -269,26 +291,6 @@ DS_DEV void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1
 template <int D>
 DS_DEV uint32_t swz(int r, int c) {
   return (uint32_t)(r * D * 2 + ((c ^ (r & 7)) << 4));
-}
-
-// 2^x on the FMA pipe (Cody-Waite split + degree-3 polynomial, max relative
-// error 1.7e-4, far below the bf16 rounding of P): used for a fraction of the
-// softmax exponentials so the MUFU unit is not the attention bottleneck.
-DS_DEV float exp2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float xi = floorf(x);
-  const float f = x - xi;
-  const float p = fmaf(fmaf(fmaf(0.07632546f, f, 0.22830825f), f, 0.69503617f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + ((int)xi << 23));
-}
-
-// (2^a, 2^b) with one packed half-precision MUFU op.
-DS_DEV float2 exp2_f16x2(float a, float b) {
-  uint32_t h, e;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(b), "f"(a));  // low half = a
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
-  __half2 v = *reinterpret_cast<__half2*>(&e);
-  return __half22float2(v);
 }
 
 // ---------------------------------------------------------------- bf16 packing

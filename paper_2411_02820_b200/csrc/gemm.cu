@@ -17,6 +17,8 @@
 //   EPI_RESID_F32 out = resid + acc                (x = h + attn@wo, out = x + mlp)
 //   EPI_SILU_BF16 out = bf16(silu(acc))            (silu(rms(x)*g @ w1))
 //   EPI_STORE_*   plain stores (tests / lm head)
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -109,21 +111,45 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
     }
     return;
   }
+  if (e.mode == EPI_RESID_F32) {
+    // f32 residual add, 32 columns per step with the next step's residual loads
+    // already in flight (the residual stream comes from HBM: hide its latency)
+    const int ncols = min(BN, e.N - col0);  // multiple of 32 (N % 32 == 0)
+    const float4* r = reinterpret_cast<const float4*>(e.resid + (long long)row * e.ld_resid + col0);
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col0);
+    float4 cur[8], nxt[8];
+    if (row_ok) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cur[i] = r[i];
+    }
+    for (int c = 0; c < ncols; c += 32) {
+      const bool more = c + 32 < ncols;
+      if (row_ok && more) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) nxt[i] = r[(c + 32) / 4 + i];
+      }
+      float v[32];
+      tmem_ld16x2(tbase + c, tbase + c + 16, v, v + 16);
+      if (row_ok) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          o[c / 4 + i] = make_float4(cur[i].x + v[4 * i], cur[i].y + v[4 * i + 1], cur[i].z + v[4 * i + 2],
+                                     cur[i].w + v[4 * i + 3]);
+      }
+      if (more) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+      }
+    }
+    return;
+  }
   for (int c = 0; c < BN; c += 16) {
     const int col = col0 + c;
     if (col >= e.N) break;
     float v[16];
     tmem_ld16(tbase + c, v);
     if (!row_ok) continue;
-    if (e.mode == EPI_RESID_F32) {
-      const float4* r = reinterpret_cast<const float4*>(e.resid + (long long)row * e.ld_resid + col);
-      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float4 a = r[i];
-        o[i] = make_float4(a.x + v[4 * i], a.y + v[4 * i + 1], a.z + v[4 * i + 2], a.w + v[4 * i + 3]);
-      }
-    } else if (e.mode == EPI_STORE_F32) {
+    if (e.mode == EPI_STORE_F32) {
       float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col);
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -330,13 +356,14 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
 // A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks BN from N.
 int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
                 cudaStream_t stream, int force_bn, int max_ctas) {
-  int bn = force_bn ? force_bn : (epi.N >= 1024 ? 256 : 128);
+  static const int env_bn = getenv("DS_GEMM_BN") ? atoi(getenv("DS_GEMM_BN")) : 0;  // temporary A/B switch
+  int bn = force_bn ? force_bn : env_bn ? env_bn : (epi.N >= 1024 ? 256 : 128);
   CUtensorMap ta, tb;
-  if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK)) return DS_ERR_CUDA;
-  if (make_tmap_bf16(&tb, B, epi.N, K, ldb, bn, GEMM_BK)) return DS_ERR_CUDA;
+  if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK) || make_tmap_bf16(&tb, B, epi.N, K, ldb, bn, GEMM_BK))
+    return launch_status(cudaErrorInvalidValue);
   cudaError_t e = bn == 256 ? launch_gemm_t<256, 4>(ta, tb, K, epi, stream, max_ctas)
                             : launch_gemm_t<128, 6>(ta, tb, K, epi, stream, max_ctas);
-  return e == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_status(e);
 }
 
 }  // namespace ds

@@ -117,8 +117,7 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   const int smem = stages * stage_bytes;
   static int attr_smem = 0;
   if (smem > attr_smem) {
-    if (cudaFuncSetAttribute(kv_ingest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return DS_ERR_CUDA;
+    if (int rc_ = launch_status(cudaFuncSetAttribute(kv_ingest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return rc_;
     attr_smem = smem;
   }
   const long long total = (long long)n_layers * 2 * n_kv_heads * a.n_pages;
@@ -132,7 +131,7 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   static const bool c0 = prefer_max_smem(kv_ingest_kernel);
   (void)c0;
   kv_ingest_kernel<<<(int)grid, 32, smem, stream>>>(a, (int)total, stage_bytes, stages);
-  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_status();
 }
 
 }  // namespace ds

@@ -70,6 +70,15 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// Status of the launch just made; the CUDA error is kept for ds_last_error()
+// (cudaGetLastError clears it, so the C ABI layer reads it from here).
+extern thread_local cudaError_t g_cuda_err;
+inline int launch_status(cudaError_t e = cudaGetLastError()) {
+  if (e == cudaSuccess) return DS_OK;
+  g_cuda_err = e;
+  return DS_ERR_CUDA;
+}
+
 // Every kernel launch of this library bumps this counter (ds_launch_count()).
 extern unsigned long long g_launches;
 inline void count_launch(int n = 1) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }

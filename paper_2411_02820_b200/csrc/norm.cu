@@ -84,7 +84,7 @@ int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int
     rmsnorm_kernel<true><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
   else
     rmsnorm_kernel<false><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
-  return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ERR_CUDA;
+  return launch_status();
 }
 
 }  // namespace ds

@@ -1,0 +1,8 @@
+python -m paper_2411_02820_b200._build > /dev/null 2>&1
+mkdir -p gpurun_out/ab2
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x > gpurun_out/ab2/kern.log 2>&1
+timeout 120 python tools/attn_bench.py > gpurun_out/ab2/attn.log 2>&1
+timeout 120 python tools/gemm_bench.py > gpurun_out/ab2/gemm256.log 2>&1
+DS_GEMM_BN=128 timeout 120 python tools/gemm_bench.py > gpurun_out/ab2/gemm128.log 2>&1
+timeout 400 python -m pytest tests -m gpu -q -x > gpurun_out/ab2/pytest.log 2>&1
+timeout 300 python tools/overlap_probe.py > gpurun_out/ab2/probe.json 2>&1
