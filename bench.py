@@ -627,6 +627,9 @@ def run_fanout(args, world, rank, local):
 
 def main():
     args = parse()
+    if args.impl != "reference" and not (ROOT / "paper_2411_02820_b200" / "libdroidspeak.so").exists():
+        from paper_2411_02820_b200 import _build  # the CUDA path is the only path: build it in-tree
+        _build.build()
     world, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":

@@ -13,6 +13,19 @@ for p in (str(ROOT),):
         sys.path.insert(0, p)
 
 
+def pytest_sessionstart(session):
+    """Build the sm_100a library in-tree if it is missing (nvcc cross-compiles on
+    the CPU box; the GPU box image has it too).  Building is not a fallback: the
+    CUDA path is still the only one."""
+    lib = ROOT / "paper_2411_02820_b200" / "libdroidspeak.so"
+    if not lib.exists():
+        try:
+            from paper_2411_02820_b200 import _build
+            _build.build()
+        except Exception as exc:  # the ABI tests report the missing library
+            print(f"library build failed: {exc}")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200, sm_100a) device")
     config.addinivalue_line("markers", "reference: needs the read-only reference checkout (build container only)")

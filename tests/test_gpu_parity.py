@@ -190,3 +190,41 @@ def test_paged_cache_with_shuffled_pages(pkg, tiny):
     torch.cuda.synchronize()
     assert torch.equal(ref.logits, got.logits)
     assert torch.equal(ref.kv.dense().v, got.kv.dense().v)
+
+
+@pytest.mark.parametrize("n", [2, 3, 65, 1024])
+def test_edge_lengths(pkg, tiny, n):
+    """Shortest window (n = 2: one reused position + the anchor), page boundaries,
+    and n = max_seq (model.py:425-437 bounds)."""
+    cfg, A, B, oA, oB = tiny
+    toks = O.synthetic_tokens(50 + n, 1, n, 4096)[0]
+    prod = pkg.full_prefill(A, toks)
+    cons = pkg.partial_prefill(B, toks, pkg.RecomputeConfig([(2, 3)]), prod.kv, prod.e_map())
+    torch.cuda.synchronize()
+    k, v, e, lp = O.full_prefill(oA, toks)
+    _, _, lc = O.partial_prefill(oB, toks, [(2, 3)], k, v, e)
+    assert np.abs(_host(prod.logits) - lp).max() < 0.1
+    assert np.abs(_host(cons.logits) - lc).max() < 0.1
+    d = cons.kv.dense()
+    assert torch.equal(d.k[:2, :, :n - 1], prod.kv.k[:2, :, :n - 1])
+    with pytest.raises(ValueError):
+        pkg.partial_prefill(B, O.synthetic_tokens(1, 1, 1025, 4096)[0], pkg.RecomputeConfig([(2, 3)]), prod.kv,
+                            prod.e_map())
+
+
+def test_multiple_groups_and_layer0_group(pkg, tiny):
+    cfg, A, B, oA, oB = tiny
+    toks = O.synthetic_tokens(61, 1, 257, 4096)[0]
+    groups = [(0, 0), (2, 2)]
+    prod = pkg.full_prefill(A, toks)
+    cons = pkg.partial_prefill(B, toks, pkg.RecomputeConfig(groups), prod.kv, prod.e_map())
+    torch.cuda.synchronize()
+    k, v, e, _ = O.full_prefill(oA, toks)
+    ck, cv, lc = O.partial_prefill(oB, toks, groups, k, v, e)
+    assert np.abs(_host(cons.logits) - lc).max() < 0.1
+    d = cons.kv.dense()
+    P_ = len(toks) - 1
+    for l in (1, 3):
+        assert torch.equal(d.k[l, :, :P_], prod.kv.k[l, :, :P_])
+    for l in (0, 2):
+        assert rel(_host(d.k)[l, :, :P_], ck[l, :, :P_]) < 2e-2
