@@ -458,7 +458,7 @@ int ds_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int
     return fail(DS_ERR_INVALID, "bad gemm shape M=%d N=%d K=%d", M, N, K);
   if (mode != EPI_STORE_BF16 && mode != EPI_RESID_F32 && mode != EPI_SILU_BF16 && mode != EPI_STORE_F32)
     return fail(DS_ERR_INVALID, "bad epilogue mode %d", mode);
-  if (mode == EPI_RESID_F32 && (!resid || (N % 32))) return fail(DS_ERR_INVALID, "resid required, N % 32 == 0");
+  if (mode == EPI_RESID_F32 && !resid) return fail(DS_ERR_INVALID, "resid required");
   GemmEpi e{};
   e.mode = mode;
   e.M = M;

@@ -238,9 +238,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         for (int c = 0; c < FA_BN; ++c)
           if (kbase + c > qpos) sr[c] = __float_as_uint(-INFINITY);
       }
-      float mt = -INFINITY;
+      // row max as 8 independent chains (a single 128-long fmax chain is
+      // ~4 cycles per link on the softmax critical path)
+      float mx8[8];
 #pragma unroll
-      for (int c = 0; c < FA_BN; ++c) mt = fmaxf(mt, __uint_as_float(sr[c]));
+      for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(sr[q]);
+#pragma unroll
+      for (int c = 8; c < FA_BN; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+      const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const bool need = mt > m_used + thr;
       float corr = 1.f;
       if (need) {
@@ -263,16 +269,16 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         tmem_wait_st();
       }
       const float msc = m_used * sc;
-      float sum = 0.f;
+      float sum4[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
       uint32_t pk[FA_BN / 2];
 #pragma unroll
       for (int c = 0; c < FA_BN / 2; ++c) {
         const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * c]), sc, -msc));
         const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc));
-        sum += p0 + p1;
+        sum4[c & 3] += p0 + p1;
         pk[c] = pack_bf16x2(p0, p1);
       }
-      l += sum;
+      l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       tmem_st32_nowait(tS, pk);
       tmem_st32_nowait(tS + 32, pk + 32);
       tmem_wait_st();

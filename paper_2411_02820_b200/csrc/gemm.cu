@@ -17,8 +17,6 @@
 //   EPI_RESID_F32 out = resid + acc                (x = h + attn@wo, out = x + mlp)
 //   EPI_SILU_BF16 out = bf16(silu(acc))            (silu(rms(x)*g @ w1))
 //   EPI_STORE_*   plain stores (tests / lm head)
-#include <stdlib.h>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -37,14 +35,13 @@ struct GemmSmem {
   static constexpr uint32_t TOTAL = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
 };
 
-DS_DEV void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  // Grouped raster: GROUP m-blocks sweep all n-blocks before moving on, so the
+DS_DEV void tile_coords(int t, int num_m, int num_n, int group, int& mb, int& nb) {
+  // Grouped raster: `group` m-blocks sweep all n-blocks before moving on, so the
   // ~148 concurrently resident tiles share A rows and B columns in L2.
-  constexpr int GROUP = 16;
-  int per_group = GROUP * num_n;
+  int per_group = group * num_n;
   int g = t / per_group;
-  int first_m = g * GROUP;
-  int gsize = min(num_m - first_m, GROUP);
+  int first_m = g * group;
+  int gsize = min(num_m - first_m, group);
   int r = t - g * per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
@@ -112,34 +109,32 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
     return;
   }
   if (e.mode == EPI_RESID_F32) {
-    // f32 residual add, 32 columns per step with the next step's residual loads
+    // f32 residual add, 16 columns per step with the next step's residual loads
     // already in flight (the residual stream comes from HBM: hide its latency)
-    const int ncols = min(BN, e.N - col0);  // multiple of 32 (N % 32 == 0)
+    const int ncols = min(BN, e.N - col0);  // multiple of 16
     const float4* r = reinterpret_cast<const float4*>(e.resid + (long long)row * e.ld_resid + col0);
     float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col0);
-    float4 cur[8], nxt[8];
+    float4 cur[4], nxt[4];
     if (row_ok) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) cur[i] = r[i];
+      for (int i = 0; i < 4; ++i) cur[i] = r[i];
     }
-    for (int c = 0; c < ncols; c += 32) {
-      const bool more = c + 32 < ncols;
+    for (int c = 0; c < ncols; c += 16) {
+      const bool more = c + 16 < ncols;
       if (row_ok && more) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) nxt[i] = r[(c + 32) / 4 + i];
+        for (int i = 0; i < 4; ++i) nxt[i] = r[(c + 16) / 4 + i];
       }
-      float v[32];
-      tmem_ld16x2(tbase + c, tbase + c + 16, v, v + 16);
+      float v[16];
+      tmem_ld16(tbase + c, v);
       if (row_ok) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 4; ++i)
           o[c / 4 + i] = make_float4(cur[i].x + v[4 * i], cur[i].y + v[4 * i + 1], cur[i].z + v[4 * i + 2],
                                      cur[i].w + v[4 * i + 3]);
       }
-      if (more) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
-      }
+      for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
     }
     return;
   }
@@ -168,8 +163,11 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
   }
 }
 
+// At most 128 registers per thread: a warp then holds 4096 of its SM
+// sub-partition's 16K registers, which leaves room for an anchor GEMV or decode
+// CTA of the other stream to share the SM with this persistent kernel.
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __maxnreg__(128)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                         GemmEpi epi) {
   using L = GemmSmem<BN, STAGES>;
@@ -216,7 +214,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t, num_m, num_n, mb, nb);
+        tile_coords(t, num_m, num_n, epi.group, mb, nb);
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], L::STAGE_BYTES);
@@ -269,7 +267,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      tile_coords(t, num_m, num_n, epi.group, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
@@ -356,13 +354,14 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
 // A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks BN from N.
 int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
                 cudaStream_t stream, int force_bn, int max_ctas) {
-  static const int env_bn = getenv("DS_GEMM_BN") ? atoi(getenv("DS_GEMM_BN")) : 0;  // temporary A/B switch
-  int bn = force_bn ? force_bn : env_bn ? env_bn : (epi.N >= 1024 ? 256 : 128);
+  int bn = force_bn ? force_bn : (epi.N >= 1024 ? 256 : 128);
+  GemmEpi e2 = epi;
+  e2.group = 16;  // measured best of 8 / 16 / 64 for the recompute shapes
   CUtensorMap ta, tb;
   if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK) || make_tmap_bf16(&tb, B, epi.N, K, ldb, bn, GEMM_BK))
     return launch_status(cudaErrorInvalidValue);
-  cudaError_t e = bn == 256 ? launch_gemm_t<256, 4>(ta, tb, K, epi, stream, max_ctas)
-                            : launch_gemm_t<128, 6>(ta, tb, K, epi, stream, max_ctas);
+  cudaError_t e = bn == 256 ? launch_gemm_t<256, 4>(ta, tb, K, e2, stream, max_ctas)
+                            : launch_gemm_t<128, 6>(ta, tb, K, e2, stream, max_ctas);
   return launch_status(e);
 }
 

@@ -27,6 +27,7 @@ struct GemmEpi {
   long long ld_q;
   KvAddr kv;
   int pos0;             // absolute position of row 0
+  int group;            // raster: m-blocks per group (set by gemm_launch)
   const float* rope_cos;  // [max_seq][head_dim/2]
   const float* rope_sin;
 };
