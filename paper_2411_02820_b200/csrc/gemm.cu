@@ -109,32 +109,37 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
     return;
   }
   if (e.mode == EPI_RESID_F32) {
-    // f32 residual add, 16 columns per step with the next step's residual loads
-    // already in flight (the residual stream comes from HBM: hide its latency)
+    // f32 residual add, 16 columns per step with the residual loads of the next
+    // two steps already in flight (the residual stream comes from HBM)
     const int ncols = min(BN, e.N - col0);  // multiple of 16
     const float4* r = reinterpret_cast<const float4*>(e.resid + (long long)row * e.ld_resid + col0);
     float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col0);
-    float4 cur[4], nxt[4];
+    float4 r0[4], r1[4], r2[4];
     if (row_ok) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) cur[i] = r[i];
+      for (int i = 0; i < 4; ++i) {
+        r0[i] = r[i];
+        if (ncols > 16) r1[i] = r[4 + i];
+      }
     }
     for (int c = 0; c < ncols; c += 16) {
-      const bool more = c + 16 < ncols;
-      if (row_ok && more) {
+      if (row_ok && c + 32 < ncols) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) nxt[i] = r[(c + 16) / 4 + i];
+        for (int i = 0; i < 4; ++i) r2[i] = r[(c + 32) / 4 + i];
       }
       float v[16];
       tmem_ld16(tbase + c, v);
       if (row_ok) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          o[c / 4 + i] = make_float4(cur[i].x + v[4 * i], cur[i].y + v[4 * i + 1], cur[i].z + v[4 * i + 2],
-                                     cur[i].w + v[4 * i + 3]);
+          o[c / 4 + i] = make_float4(r0[i].x + v[4 * i], r0[i].y + v[4 * i + 1], r0[i].z + v[4 * i + 2],
+                                     r0[i].w + v[4 * i + 3]);
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+      for (int i = 0; i < 4; ++i) {
+        r0[i] = r1[i];
+        r1[i] = r2[i];
+      }
     }
     return;
   }
