@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--graph", type=int, default=1, help="replay the consumer step as a CUDA graph")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1: consumers pull the producer's export over NVLink (CUDA IPC), or NCCL send/recv")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="N>1: requests per consumer per step (config 4 batched requests; each its own prefix)")
     ap.add_argument("--same-device", action="store_true",
                     help="debug: run every rank on cuda:0 with gloo (exercises the N>1 code path on one GPU)")
     return ap.parse_args()
@@ -487,14 +489,20 @@ def run_fanout(args, world, rank, local):
     L = cfg.n_layers
     dev = torch.device("cuda", local)
     rc = P.RecomputeConfig([(L - k, L - 1)])
-    ids = np.random.default_rng(7).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
+    nb = max(1, args.batch) if args.transport == "p2p" else 1
+    batch_ids = [np.random.default_rng(7 + b).integers(0, cfg.vocab_size, size=n, dtype=np.int64) for b in range(nb)]
+    ids = batch_ids[0]
     tok_dev = torch.from_numpy(ids).to(dev)
+    batch_tok = [torch.from_numpy(x).to(dev) for x in batch_ids]
     producer = rank == 0
     A = P.random_model(cfg, seed=1000, device=dev)
     if producer:
-        prod = P.full_prefill(A, ids, e_layers=rc.transition_layers, tokens_dev=tok_dev)
+        # the shared contexts are prefilled once and stay resident
+        prods = [P.full_prefill(A, x, e_layers=rc.transition_layers, tokens_dev=t) for x, t in zip(batch_ids, batch_tok)]
+        prod = prods[0]
         torch.cuda.synchronize()
-        obj = [export_prefill(prod, A.ident, ids) if args.transport == "p2p" else None]
+        obj = [[export_prefill(p_, A.ident, x) for p_, x in zip(prods, batch_ids)] if args.transport == "p2p"
+               else None]
     else:
         B = P.random_model(cfg, seed=2000 + rank, device=dev, base=A, perturb_layers=range(L - k, L), eps=0.5)
         del A
@@ -507,9 +515,15 @@ def run_fanout(args, world, rank, local):
     if not producer:
         cache = P.PagedKV.allocate(cfg, n, dev)
         if args.transport == "p2p":
-            remote = RemoteExport(obj[0])
-            step = lambda: P.partial_prefill(B, ids, rc, remote.kv, remote.e_map, out=cache, stream=stream,  # noqa
-                                             copy_stream=side, tokens_dev=tok_dev)
+            remotes = [RemoteExport(h_) for h_ in obj[0]]
+            remote = remotes[0]
+            caches = [cache] + [P.PagedKV.allocate(cfg, n, dev) for _ in range(nb - 1)]
+
+            def step():
+                for b in range(nb):  # the consumer's batch of requests, back to back in one graph
+                    r_ = P.partial_prefill(B, batch_ids[b], rc, remotes[b].kv, remotes[b].e_map, out=caches[b],
+                                           stream=stream, copy_stream=side, tokens_dev=batch_tok[b])
+                return r_
         else:
             pipe = ConsumerPipeline(B, transport=NcclTransport(0, cfg, n, dev))
             step = lambda: pipe.run(ids, rc, None, None, out=cache, tokens_dev=tok_dev)  # noqa
@@ -598,17 +612,19 @@ def run_fanout(args, world, rank, local):
         links = [x for x in gathered if x]
     barrier(world)
     if remote is not None:
-        remote.close()
+        for r_ in remotes:
+            r_.close()
     if rank == 0:
         nc = len(consumers)
         line = {
-            "metric": METRIC, "value": nc * n / (ttft_ms / 1e3), "unit": "tok/s", "n_gpus": world,
+            "metric": METRIC, "value": nc * nb * n / (ttft_ms / 1e3), "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "ttft_p50_ms": ttft_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (random-init weights generated on GPU, uniform random token ids)",
             "config": {"workload": f"fan-out: 1 producer (GPU 0) -> {nc} consumer fine-tunes, Llama-3-8B-shaped, "
                                    f"n={n}, recompute [{L - k},{L - 1}] (BASELINE configs 3/4)",
-                       "n_tokens": n, "recomputed_layers": k, "consumers": nc, "transport": args.transport,
+                       "n_tokens": n, "recomputed_layers": k, "consumers": nc, "requests_per_consumer": nb,
+                       "transport": args.transport,
                        "parallelism": f"1 producer + {nc} consumers", "cuda_graph": graphed},
             "gpu_launches": launches,
             "e2e": {"value": nc * n / e2e_s if e2e_s > 0 else None, "unit": "tok/s", "ttft_p50_ms": e2e_s * 1e3,

@@ -22,6 +22,11 @@ DS_DEV void load8(const void* x, long long idx, float* v) {
   }
 }
 
+// One CTA per row.  Rows up to NORM_THREADS * 8 * NORM_REG values are read
+// once into registers (sum of squares, then scale from registers); longer rows
+// take a second (L2-resident) pass.
+constexpr int NORM_REG = 4;
+
 template <bool IN_BF16>
 __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, const int64_t* gather, int d,
                                                                const float* gain, bf16* out, float* copy_f32,
@@ -29,12 +34,26 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, co
   const int r = blockIdx.x;
   const long long src = gather ? (long long)__ldg(gather + r) : (long long)r;
   const long long base = src * d;
+  const bool in_regs = d <= NORM_THREADS * 8 * NORM_REG;
+  float v[NORM_REG][8];
   float ss = 0.f;
-  for (int c = threadIdx.x * 8; c < d; c += NORM_THREADS * 8) {
-    float v[8];
-    load8<IN_BF16>(x, base + c, v);
+  if (in_regs) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
+    for (int i = 0; i < NORM_REG; ++i) {
+      const int c = (threadIdx.x + i * NORM_THREADS) * 8;
+      if (c < d) {
+        load8<IN_BF16>(x, base + c, v[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ss += v[i][e] * v[i][e];
+      }
+    }
+  } else {
+    for (int c = threadIdx.x * 8; c < d; c += NORM_THREADS * 8) {
+      float t[8];
+      load8<IN_BF16>(x, base + c, t);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += t[e] * t[e];
+    }
   }
   __shared__ float red[NORM_THREADS / 32];
 #pragma unroll
@@ -50,26 +69,37 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, co
   __syncthreads();
   const float inv = 1.0f / sqrtf(red[0] / (float)d + 1e-6f);
   const long long obase = (long long)r * d;
-  for (int c = threadIdx.x * 8; c < d; c += NORM_THREADS * 8) {
-    float v[8];
-    load8<IN_BF16>(x, base + c, v);
+  auto emit = [&](int c, const float* w) {
     const float4 g0 = *reinterpret_cast<const float4*>(gain + c);
     const float4 g1 = *reinterpret_cast<const float4*>(gain + c + 4);
     const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
     uint32_t p[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) p[i] = pack_bf16x2(v[2 * i] * inv * g[2 * i], v[2 * i + 1] * inv * g[2 * i + 1]);
+    for (int i = 0; i < 4; ++i) p[i] = pack_bf16x2(w[2 * i] * inv * g[2 * i], w[2 * i + 1] * inv * g[2 * i + 1]);
     *reinterpret_cast<uint4*>(out + obase + c) = make_uint4(p[0], p[1], p[2], p[3]);
     if (copy_f32) {
       float4* o = reinterpret_cast<float4*>(copy_f32 + obase + c);
-      o[0] = make_float4(v[0], v[1], v[2], v[3]);
-      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+      o[0] = make_float4(w[0], w[1], w[2], w[3]);
+      o[1] = make_float4(w[4], w[5], w[6], w[7]);
     }
     if (copy_bf16 && r < copy_rows) {
       uint32_t q[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) q[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+      for (int i = 0; i < 4; ++i) q[i] = pack_bf16x2(w[2 * i], w[2 * i + 1]);
       *reinterpret_cast<uint4*>(copy_bf16 + obase + c) = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+  };
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < NORM_REG; ++i) {
+      const int c = (threadIdx.x + i * NORM_THREADS) * 8;
+      if (c < d) emit(c, v[i]);
+    }
+  } else {
+    for (int c = threadIdx.x * 8; c < d; c += NORM_THREADS * 8) {
+      float t[8];
+      load8<IN_BF16>(x, base + c, t);
+      emit(c, t);
     }
   }
 }
