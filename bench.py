@@ -629,12 +629,14 @@ def run_fanout(args, world, rank, local):
             "gpu_launches": launches,
             "e2e": {"value": nc * n / e2e_s if e2e_s > 0 else None, "unit": "tok/s", "ttft_p50_ms": e2e_s * 1e3,
                     "h2d_bytes_per_step": 8 * n * nc, "d2h_bytes_per_step": (4 * cfg.vocab_size + 4) * nc},
-            "roofline": ({"bound": "hbm" if args.same_device else "nvlink",
-                          "kernel": links[0]["kernel"] + (" (same device: debug run, not NVLink)"
-                                                          if args.same_device else ""),
-                          "achieved": links[0]["gbs"],
-                          "peak": 770.0, "unit": "GB/s", "frac": links[0]["gbs"] / 770.0, "traffic": None,
-                          "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900"}
+            "roofline": (({"bound": "hbm", "kernel": links[0]["kernel"] + " (same device: debug run, not NVLink)",
+                           "achieved": 2 * links[0]["gbs"], "peak": peaks()["hbm"], "unit": "GB/s",
+                           "frac": 2 * links[0]["gbs"] / peaks()["hbm"], "traffic": None,
+                           "peak_source": f"{peaks()['src']} HBM copy (read + write counted)"}
+                          if args.same_device else
+                          {"bound": "nvlink", "kernel": links[0]["kernel"], "achieved": links[0]["gbs"],
+                           "peak": 770.0, "unit": "GB/s", "frac": links[0]["gbs"] / 770.0, "traffic": None,
+                           "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900"})
                          if links else None),
             "clocks": clocks.summary(),
         }

@@ -81,7 +81,8 @@ class LayerKV:
 
     def desc(self) -> L.KvCache:
         Ln, G, n, D = self.k.shape
-        assert self.k.is_contiguous() and self.v.is_contiguous()
+        if not (self.k.is_contiguous() and self.v.is_contiguous()):
+            raise ValueError("LayerKV tensors must be contiguous")
         return L.KvCache(self.k.data_ptr(), self.v.data_ptr(), G * n * D, n * D, PAGE * D, None, Ln, n)
 
     @classmethod
@@ -196,9 +197,14 @@ def workspace_bytes(config: ModelConfig, n_tokens: int) -> int:
     return int(L.lib().ds_workspace_size(C.byref(dims), n_tokens))
 
 
-def _workspace(model: ModelWeights, n: int) -> torch.Tensor:
+def _workspace(model: ModelWeights, n: int, stream=None) -> torch.Tensor:
+    """Scratch for one call, cached per (device, model, stream): calls on the
+    same stream are ordered, so they may share it; calls on different streams
+    (a producer and a consumer prefilling concurrently) get their own.  The
+    pointer stays stable across calls, which CUDA-graph capture relies on."""
     need = workspace_bytes(model.config, n)
-    key = (model.device, id(model.config))
+    s = stream if stream is not None else torch.cuda.current_stream(model.device)
+    key = (model.device, id(model), s.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=model.device)
@@ -233,8 +239,8 @@ def full_prefill(model: ModelWeights, tokens, e_layers: Iterable[int] | None = N
     e_bufs = [torch.empty(n - 1, cfg.d_model, dtype=torch.bfloat16, device=model.device) for _ in layers]
     logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=model.device)
     tok = torch.empty(1, dtype=torch.int32, device=model.device)
-    ws = _workspace(model, n)
     s = stream if stream is not None else torch.cuda.current_stream(model.device)
+    ws = _workspace(model, n, s)
     la = (C.c_int32 * max(1, len(layers)))(*layers)
     ptrs = (C.c_void_p * max(1, len(layers)))(*[b.data_ptr() for b in e_bufs])
     desc = kv.desc()
@@ -263,13 +269,14 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
     cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
     logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
     tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
-    ws = _workspace(receiver, n)
     s = stream if stream is not None else torch.cuda.current_stream(receiver.device)
+    ws = _workspace(receiver, n, s)
     groups = [x for g in config.groups for x in g]
     ga = (C.c_int32 * max(1, len(groups)))(*groups)
-    e_list = [L.ECacheDesc(l, e.positions, e.hidden.shape[1], e.hidden.data_ptr())
-              for l, e in sorted(e_map.items()) if e.hidden.dtype == torch.bfloat16 and e.hidden.is_cuda
-              and e.hidden.is_contiguous()]
+    for l, e in e_map.items():
+        if e.hidden.dtype != torch.bfloat16 or not e.hidden.is_cuda or not e.hidden.is_contiguous():
+            raise ValueError(f"E cache of layer {l} must be a contiguous bf16 device tensor")
+    e_list = [L.ECacheDesc(l, e.positions, e.hidden.shape[1], e.hidden.data_ptr()) for l, e in sorted(e_map.items())]
     ea = (L.ECacheDesc * max(1, len(e_list)))(*e_list)
     skv = sender_kv.desc() if sender_kv is not None else None
     odesc = cache.desc()

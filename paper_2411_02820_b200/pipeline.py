@@ -98,7 +98,7 @@ class ConsumerPipeline:
         dst = cache.desc()
         logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=self.device)
         tok = torch.empty(1, dtype=torch.int32, device=self.device)
-        ws = _workspace(self.receiver, n)
+        ws = _workspace(self.receiver, n, self.compute)
         if tokens_dev is None:
             tokens_dev = torch.from_numpy(ids).to(self.device, non_blocking=True)
         cur = torch.cuda.current_stream(self.device)
