@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // PDL: barrier init, TMEM alloc and descriptor prefetch overlapped the
+  // predecessor's tail; its outputs are read only after this point
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -334,8 +338,7 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
   }
   dim3 grid(n_heads, (n_q + 2 * FA_BM - 1) / (2 * FA_BM));
   count_launch();
-  fa_tc_kernel<D><<<grid, FA_THREADS, L::TOTAL, stream>>>(tq, tk, tv, a);
-  return launch_status();
+  return launch_status(launch_pdl(fa_tc_kernel<D>, grid, dim3(FA_THREADS), L::TOTAL, stream, tq, tk, tv, a));
 }
 
 int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,

@@ -212,6 +212,10 @@ __global__ void __maxnreg__(128)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: barrier init, TMEM alloc and descriptor prefetch overlapped the
+  // predecessor's tail; its outputs are read only after this point
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -352,8 +356,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   count_launch();
-  kern<<<grid, GEMM_THREADS, L::TOTAL, stream>>>(ta, tb, K, epi);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(GEMM_THREADS), L::TOTAL, stream, ta, tb, K, epi);
 }
 
 // A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks BN from N.

@@ -31,6 +31,8 @@ template <bool IN_BF16>
 __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, const int64_t* gather, int d,
                                                                const float* gain, bf16* out, float* copy_f32,
                                                                bf16* copy_bf16, int copy_rows) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const long long src = gather ? (long long)__ldg(gather + r) : (long long)r;
   const long long base = src * d;
@@ -111,10 +113,10 @@ int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int
   static const bool c0 = prefer_max_smem(rmsnorm_kernel<true>) && prefer_max_smem(rmsnorm_kernel<false>);
   (void)c0;
   if (x_bf16)
-    rmsnorm_kernel<true><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
-  else
-    rmsnorm_kernel<false><<<M, NORM_THREADS, 0, stream>>>(x, gather, d, gain, out, copy_f32, copy_bf16, copy_rows);
-  return launch_status();
+    return launch_status(launch_pdl(rmsnorm_kernel<true>, dim3(M), dim3(NORM_THREADS), 0, stream, x, gather, d, gain,
+                                    out, copy_f32, copy_bf16, copy_rows));
+  return launch_status(launch_pdl(rmsnorm_kernel<false>, dim3(M), dim3(NORM_THREADS), 0, stream, x, gather, d, gain,
+                                  out, copy_f32, copy_bf16, copy_rows));
 }
 
 }  // namespace ds

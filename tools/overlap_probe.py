@@ -34,17 +34,21 @@ ids = np.random.default_rng(7).integers(0, cfg.vocab_size, size=n, dtype=np.int6
 tok = torch.from_numpy(ids).cuda()
 prod = P.full_prefill(A, ids, e_layers=rc.transition_layers, tokens_dev=tok)
 cache = P.PagedKV.allocate(cfg, n)
-s, side = torch.cuda.Stream(), torch.cuda.Stream()
+s = torch.cuda.Stream()
+side_hi = torch.cuda.Stream(priority=-1)   # high priority copy/anchor stream
+side_lo = torch.cuda.Stream(priority=0)
+side = side_lo
 ws = _workspace(B, n)
 lib = L.lib()
 
 
-def graph_time(fn, reps=10):
-    with torch.cuda.stream(s):
+def graph_time(fn, reps=10, cs=None):
+    cs = cs or s
+    with torch.cuda.stream(cs):
         fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=s):
+    with torch.cuda.graph(g, stream=cs):
         fn()
     for _ in range(3):
         g.replay()
@@ -52,10 +56,10 @@ def graph_time(fn, reps=10):
     ts = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        with torch.cuda.stream(s):
+        a.record(cs)
+        with torch.cuda.stream(cs):
             g.replay()
-        b.record(s)
+        b.record(cs)
         b.synchronize()
         ts.append(a.elapsed_time(b))
     return statistics.median(ts)
@@ -64,6 +68,12 @@ def graph_time(fn, reps=10):
 out = {}
 out["fused_two_stream_ms"] = graph_time(lambda: P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), out=cache, stream=s,
                                                                   copy_stream=side, tokens_dev=tok))
+out["fused_two_stream_hiprio_ms"] = graph_time(lambda: P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), out=cache,
+                                                                         stream=s, copy_stream=side_hi, tokens_dev=tok))
+s_hi = torch.cuda.Stream(priority=-1)
+out["fused_two_stream_compute_hiprio_ms"] = graph_time(
+    lambda: P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), out=cache, stream=s_hi, copy_stream=side_lo,
+                              tokens_dev=tok), cs=s_hi)
 out["fused_single_stream_ms"] = graph_time(lambda: P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), out=cache,
                                                                      stream=s, tokens_dev=tok))
 reused = list(range(L_ - k))
