@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--graph", type=int, default=1, help="replay the consumer step as a CUDA graph")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1: consumers pull the producer's export over NVLink (CUDA IPC), or NCCL send/recv")
+    ap.add_argument("--mlp", default="ungated", choices=["ungated", "swiglu"],
+                    help="ungated = the reference block (headline); swiglu = real Llama-3-8B MLP (second row)")
+    ap.add_argument("--vocab", type=int, default=128256, help="32000 = Mistral-7B shape (config 3)")
     ap.add_argument("--batch", type=int, default=1,
                     help="N>1: requests per consumer per step (config 4 batched requests; each its own prefix)")
     ap.add_argument("--same-device", action="store_true",
@@ -268,7 +271,7 @@ def run_ours(args, world, rank, local):
     lib = _lib.lib()
     pk = peaks()
     n, k = args.n, args.k
-    cfg = P.ModelConfig(max_seq=max(n, 8192), base_seed=0, **SHAPE)
+    cfg = P.ModelConfig(max_seq=max(n, 8192), base_seed=0, mlp_kind=args.mlp, **dict(SHAPE, vocab_size=args.vocab))
     L = cfg.n_layers
     dev = torch.device("cuda", local)
     A = P.random_model(cfg, seed=1000 + rank, device=dev)
@@ -388,9 +391,9 @@ def run_ours(args, world, rank, local):
     lw = B.layers[L - 1]
     kern = {}
     with torch.cuda.stream(stream):
-        ms = time_kernel(lambda: ops.gemm(a_act, lw["w1"], mode=_lib.EPI_SILU_BF16, out=u_act, stream=stream), 10,
-                         stream)
-        kern["gemm_w1_silu"] = {"ms": ms, "tflops": 2 * Pn * d * F / ms / 1e9}
+        w1_mode = _lib.EPI_SWIGLU_BF16 if args.mlp == "swiglu" else _lib.EPI_SILU_BF16
+        ms = time_kernel(lambda: ops.gemm(a_act, lw["w1"], mode=w1_mode, out=u_act, stream=stream), 10, stream)
+        kern["gemm_w1_silu"] = {"ms": ms, "tflops": 2 * Pn * d * lw["w1"].shape[0] / ms / 1e9}
         hbuf = torch.randn(Pn, d, device=dev)
         ms = time_kernel(lambda: ops.gemm(u_act, lw["w2"], mode=_lib.EPI_RESID_F32, resid=hbuf, out=hbuf,
                                           stream=stream), 10, stream)
@@ -413,16 +416,17 @@ def run_ours(args, world, rank, local):
     gemm = kern["gemm_w1_silu"]
     traffic = None
     tpath = ROOT / "profiles" / "ncu_traffic.json"
-    if tpath.exists():
-        traffic = json.loads(tpath.read_text()).get("gemm_w1_silu")
-    flops_layer = 2 * Pn * d * (HD + 2 * KVD) + 2 * Pn * HD * d + 2 * 2 * Pn * d * F + 2 * 2 * HD * Pn * (Pn + 1) / 2
+    if tpath.exists() and args.mlp == "ungated" and n == 8192:
+        traffic = json.loads(tpath.read_text()).get("gemm_w1_silu")  # measured for this shape only
+    m_mlp = 3 if args.mlp == "swiglu" else 2
+    flops_layer = 2 * Pn * d * (HD + 2 * KVD) + 2 * Pn * HD * d + m_mlp * 2 * Pn * d * F + 2 * 2 * HD * Pn * (Pn + 1) / 2
     if rank == 0:
         line = {
             "metric": METRIC, "value": world * n / (ttft_ms / 1e3), "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "ttft_p50_ms": ttft_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (random-init weights generated on GPU, uniform random token ids)",
-            "config": {"workload": f"consumer partial prefill, Llama-3-8B-shaped pair (ungated MLP), n={n}, "
+            "config": {"workload": f"consumer partial prefill, Llama-3-8B-shaped pair ({args.mlp} MLP, V={args.vocab}), n={n}, "
                                    f"recompute [{L - k},{L - 1}] (k={k}/32), producer export resident "
                                    "(BASELINE config 2)",
                        "n_tokens": n, "recomputed_layers": k, "reused_layers": L - k,
@@ -437,7 +441,8 @@ def run_ours(args, world, rank, local):
             "gpu_launches": int(launches),
             "e2e": {"value": world * n / e2e_ttft, "unit": "tok/s", "ttft_p50_ms": e2e_ttft * 1e3,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * cfg.vocab_size + 4},
-            "roofline": {"bound": "tensor", "kernel": "gemm_tcgen05 (W1+SiLU, M=%d N=%d K=%d)" % (Pn, F, d),
+            "roofline": {"bound": "tensor", "kernel": "gemm_tcgen05 (W1+%s, M=%d N=%d K=%d)" % (
+                "SwiGLU" if args.mlp == "swiglu" else "SiLU", Pn, lw["w1"].shape[0], d),
                          "achieved": gemm["tflops"], "peak": pk["bf16"], "unit": "TFLOP/s",
                          "frac": gemm["tflops"] / pk["bf16"], "traffic": traffic,
                          "peak_source": f"{pk['src']} bf16 burst (kernel timed alone)"},
@@ -485,7 +490,7 @@ def run_fanout(args, world, rank, local):
 
     lib = _lib.lib()
     n, k = args.n, args.k
-    cfg = P.ModelConfig(max_seq=max(n, 8192), base_seed=0, **SHAPE)
+    cfg = P.ModelConfig(max_seq=max(n, 8192), base_seed=0, mlp_kind=args.mlp, **dict(SHAPE, vocab_size=args.vocab))
     L = cfg.n_layers
     dev = torch.device("cuda", local)
     rc = P.RecomputeConfig([(L - k, L - 1)])

@@ -36,9 +36,14 @@ extern "C" {
 enum ds_status { DS_OK = 0, DS_ERR_INVALID = 1, DS_ERR_CACHE_MISS = 2, DS_ERR_DEGENERATE = 3, DS_ERR_CUDA = 4 };
 enum ds_miss_kind { DS_MISS_NONE = 0, DS_MISS_KV = 1, DS_MISS_E = 2 };
 
-/* ModelConfig (model.py:70-124) minus the seed. */
+/* ModelConfig (model.py:70-124) minus the seed.  mlp_kind: DS_MLP_UNGATED is the
+ * reference block (silu(x W1) W2, model.py:532-533); DS_MLP_SWIGLU is the
+ * Llama-3 MLP (silu(x Wg) * (x Wu)) W2 with W1 = [2*d_ff][d] holding gate and
+ * up rows interleaved in blocks of 16 (rows 32b..32b+15 gate, 32b+16..32b+31 up). */
+enum ds_mlp_kind { DS_MLP_UNGATED = 0, DS_MLP_SWIGLU = 1 };
 typedef struct ds_dims {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab_size, max_seq;
+  int32_t mlp_kind;
 } ds_dims;
 
 /* One layer's weights on device.  Matrices are the reference's [in,out]
@@ -46,7 +51,7 @@ typedef struct ds_dims {
 typedef struct ds_layer_weights {
   const void* wqkv;    /* bf16 [(H+2*KVH)*D][d] = concat(wq, wk, wv)^T */
   const void* wo;      /* bf16 [d][H*D]          = wo^T */
-  const void* w1;      /* bf16 [d_ff][d]         = w1^T */
+  const void* w1;      /* bf16 [d_ff][d] = w1^T (ungated) or [2*d_ff][d] interleaved gate/up (SwiGLU) */
   const void* w2;      /* bf16 [d][d_ff]         = w2^T */
   const float* g_attn; /* f32 [d] */
   const float* g_mlp;  /* f32 [d] */

@@ -17,12 +17,14 @@ DS_OK, DS_ERR_INVALID, DS_ERR_CACHE_MISS, DS_ERR_DEGENERATE, DS_ERR_CUDA = range
 MISS_KIND = {1: "kv", 2: "e"}
 
 # epilogue modes of ds_gemm
-EPI_STORE_BF16, EPI_RESID_F32, EPI_SILU_BF16, EPI_QKV_ROPE, EPI_STORE_F32 = range(5)
+EPI_STORE_BF16, EPI_RESID_F32, EPI_SILU_BF16, EPI_QKV_ROPE, EPI_STORE_F32, EPI_SWIGLU_BF16 = range(6)
+MLP_KINDS = {"ungated": 0, "swiglu": 1}
 
 
 class Dims(C.Structure):
     _fields_ = [(n, C.c_int32) for n in
-                ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab_size", "max_seq")]
+                ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab_size", "max_seq",
+                 "mlp_kind")]
 
 
 class LayerWeights(C.Structure):

@@ -23,8 +23,13 @@ class ModelConfig:
     vocab_size: int
     max_seq: int
     base_seed: int
+    # "ungated" = the reference block (model.py:532-533); "swiglu" = the Llama-3
+    # MLP (a B200-path extension: the second row of config 2)
+    mlp_kind: str = "ungated"
 
     def __post_init__(self) -> None:
+        if self.mlp_kind not in ("ungated", "swiglu"):
+            raise ValueError(f"unknown mlp_kind {self.mlp_kind!r}")
         for name in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab_size"):
             if getattr(self, name) < 1:
                 raise ValueError(f"{name} must be positive, got {getattr(self, name)}")

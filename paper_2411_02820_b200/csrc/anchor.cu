@@ -52,6 +52,11 @@ DS_DEV unsigned long long pack_argmax(float v, int idx) {
 // (rows head*D + j0 + i and head*D + half + j0 + i, i < 4) so the rotation
 // happens in the epilogue; other modes take 8 consecutive rows.
 DS_DEV int gemv_row(const GemvArgs& a, int t, int r) {
+  if (a.mode == EPI_SWIGLU_BF16) {
+    // 4 gate rows and the 4 up rows that pair with them (blocks of 16, see ds_dims)
+    const int blk = t >> 2, q = t & 3;
+    return blk * 32 + (r < 4 ? q * 4 + r : 16 + q * 4 + r - 4);
+  }
   if (a.mode != EPI_QKV_ROPE) return t * GEMV_ROWS + r;
   const int half = a.head_dim >> 1;
   const int per_head = half / 4;
@@ -169,6 +174,11 @@ __global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
         dst[j] = __float2bfloat16_rn(lo);
         dst[j + half] = __float2bfloat16_rn(hi);
       }
+    } else if (a.mode == EPI_SWIGLU_BF16) {
+      if (tid < 4) {
+        const int o = (t >> 2) * 16 + (t & 3) * 4 + tid;
+        a.out_bf16[o] = __float2bfloat16_rn(silu(red[0][tid]) * red[0][tid + 4]);
+      }
     } else if (tid < GEMV_ROWS) {
       const int row = t * GEMV_ROWS + tid;
       const float v = red[0][tid];
@@ -216,7 +226,7 @@ int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaSt
 }
 
 int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
-  if ((a.N % GEMV_ROWS) || (a.K & 7)) return DS_ERR_INVALID;
+  if ((a.N % GEMV_ROWS) || (a.K & 7) || (a.mode == EPI_SWIGLU_BF16 && a.N % 32)) return DS_ERR_INVALID;
   if (a.mode == EPI_QKV_ROPE && (a.head_dim % 8 || a.N % a.head_dim)) return DS_ERR_INVALID;
   const int tiles = a.N / GEMV_ROWS;
   const int smem = a.K * 2;

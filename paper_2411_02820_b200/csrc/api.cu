@@ -114,6 +114,7 @@ int check_dims(const ds_dims& d) {
   if (d.d_model % 64 || d.d_ff % 64) return fail(DS_ERR_INVALID, "d_model and d_ff must be multiples of 64");
   if (d.vocab_size < 2 || d.vocab_size % 2) return fail(DS_ERR_INVALID, "vocab_size must be even");
   if (d.max_seq < 2) return fail(DS_ERR_INVALID, "max_seq must be >= 2");
+  if (d.mlp_kind != DS_MLP_UNGATED && d.mlp_kind != DS_MLP_SWIGLU) return fail(DS_ERR_INVALID, "unknown mlp_kind %d", d.mlp_kind);
   return DS_OK;
 }
 
@@ -196,9 +197,10 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only) {
   DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, rows, d.d_model, W.g_mlp, c.w.a, nullptr, nullptr, 0, c.s),
          "rmsnorm");
   GemmEpi f{};
-  f.mode = EPI_SILU_BF16;
+  const bool swiglu = d.mlp_kind == DS_MLP_SWIGLU;
+  f.mode = swiglu ? EPI_SWIGLU_BF16 : EPI_SILU_BF16;
   f.M = rows;
-  f.N = d.d_ff;
+  f.N = swiglu ? 2 * d.d_ff : d.d_ff;
   f.out = c.w.u;
   f.ld_out = d.d_ff;
   DS_TRY(gemm_launch(c.w.a, d.d_model, W.w1, d.d_model, d.d_model, f, c.s), "w1 gemm");
@@ -246,11 +248,11 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a) {
   GemvArgs f{};
   f.W = static_cast<const bf16*>(W.w1);
   f.ldw = d.d_model;
-  f.N = d.d_ff;
+  f.N = d.mlp_kind == DS_MLP_SWIGLU ? 2 * d.d_ff : d.d_ff;
   f.K = d.d_model;
   f.x_f32 = h_a;
   f.gain = W.g_mlp;
-  f.mode = EPI_SILU_BF16;
+  f.mode = d.mlp_kind == DS_MLP_SWIGLU ? EPI_SWIGLU_BF16 : EPI_SILU_BF16;
   f.out_bf16 = c.w.u_a;
   DS_TRY(gemv_launch(f, c.s), "anchor w1");
   GemvArgs s2{};
@@ -456,7 +458,8 @@ int ds_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int
   g_err.clear();
   if (!A || !B || !C || M < 1 || N < 16 || K < 8 || (N % 16) || (K % 8))
     return fail(DS_ERR_INVALID, "bad gemm shape M=%d N=%d K=%d", M, N, K);
-  if (mode != EPI_STORE_BF16 && mode != EPI_RESID_F32 && mode != EPI_SILU_BF16 && mode != EPI_STORE_F32)
+  if (mode != EPI_STORE_BF16 && mode != EPI_RESID_F32 && mode != EPI_SILU_BF16 && mode != EPI_STORE_F32 &&
+      !(mode == EPI_SWIGLU_BF16 && N % 32 == 0))
     return fail(DS_ERR_INVALID, "bad epilogue mode %d", mode);
   if (mode == EPI_RESID_F32 && !resid) return fail(DS_ERR_INVALID, "resid required");
   GemmEpi e{};

@@ -16,6 +16,7 @@
 //                 k/v -> bf16 KV cache through KvAddr (paged or dense export layout)
 //   EPI_RESID_F32 out = resid + acc                (x = h + attn@wo, out = x + mlp)
 //   EPI_SILU_BF16 out = bf16(silu(acc))            (silu(rms(x)*g @ w1))
+//   EPI_SWIGLU_BF16 out = bf16(silu(gate) * up)    (Llama-3 MLP, interleaved gate/up columns)
 //   EPI_STORE_*   plain stores (tests / lm head)
 #include "common.cuh"
 #include "kernels.h"
@@ -140,6 +141,24 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
         r0[i] = r1[i];
         r1[i] = r2[i];
       }
+    }
+    return;
+  }
+  if (e.mode == EPI_SWIGLU_BF16) {
+    // W1 rows interleave gate / up in blocks of 16: accumulator columns
+    // [32b, 32b+16) are gate, [32b+16, 32b+32) up; output column 16b + i
+    for (int c = 0; c < BN; c += 32) {
+      const int col = col0 + c;
+      if (col >= e.N) break;
+      float gt[16], up[16];
+      tmem_ld16x2(tbase + c, tbase + c + 16, gt, up);
+      if (!row_ok) continue;
+      uint32_t p[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p[i] = pack_bf16x2(silu(gt[2 * i]) * up[2 * i], silu(gt[2 * i + 1]) * up[2 * i + 1]);
+      bf16* o = reinterpret_cast<bf16*>(e.out) + (long long)row * e.ld_out + col / 2;
+      st_global_v4(o, p[0], p[1], p[2], p[3]);
+      st_global_v4(o + 8, p[4], p[5], p[6], p[7]);
     }
     return;
   }

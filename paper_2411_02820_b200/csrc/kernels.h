@@ -11,7 +11,8 @@
 
 namespace ds {
 
-enum EpiMode { EPI_STORE_BF16 = 0, EPI_RESID_F32 = 1, EPI_SILU_BF16 = 2, EPI_QKV_ROPE = 3, EPI_STORE_F32 = 4 };
+enum EpiMode { EPI_STORE_BF16 = 0, EPI_RESID_F32 = 1, EPI_SILU_BF16 = 2, EPI_QKV_ROPE = 3, EPI_STORE_F32 = 4,
+               EPI_SWIGLU_BF16 = 5 };
 
 struct GemmEpi {
   int mode;
@@ -112,7 +113,7 @@ struct GemvArgs {
   const float* x_f32;   // normalised when gain != nullptr
   const float* gain;
   const bf16* x_bf16;   // used when x_f32 == nullptr
-  int mode;             // EPI_QKV_ROPE / EPI_RESID_F32 / EPI_SILU_BF16 / EPI_STORE_F32
+  int mode;             // EPI_QKV_ROPE / EPI_RESID_F32 / EPI_SILU_BF16 / EPI_SWIGLU_BF16 / EPI_STORE_F32
   float* out_f32;
   const float* resid;
   bf16* out_bf16;

@@ -193,7 +193,7 @@ _WS: dict = {}
 
 def workspace_bytes(config: ModelConfig, n_tokens: int) -> int:
     dims = L.Dims(config.n_layers, config.d_model, config.n_heads, config.n_kv_heads, config.head_dim,
-                  config.d_ff, config.vocab_size, config.max_seq)
+                  config.d_ff, config.vocab_size, config.max_seq, L.MLP_KINDS[config.mlp_kind])
     return int(L.lib().ds_workspace_size(C.byref(dims), n_tokens))
 
 

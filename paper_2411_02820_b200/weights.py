@@ -115,7 +115,7 @@ class ModelWeights:
                 arr[i] = L.LayerWeights(lw["wqkv"].data_ptr(), lw["wo"].data_ptr(), lw["w1"].data_ptr(),
                                         lw["w2"].data_ptr(), lw["g_attn"].data_ptr(), lw["g_mlp"].data_ptr())
             dims = L.Dims(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.d_ff,
-                          cfg.vocab_size, cfg.max_seq)
+                          cfg.vocab_size, cfg.max_seq, L.MLP_KINDS[cfg.mlp_kind])
             self._layer_arr = arr
             self._desc = L.Model(dims, self.embed.data_ptr(), self.unembed_t.data_ptr(), self.g_final.data_ptr(),
                                  self.rope_cos.data_ptr(), self.rope_sin.data_ptr(),
@@ -128,20 +128,35 @@ def _bf16(x: np.ndarray, device) -> torch.Tensor:
 
 
 def from_host(config: ModelConfig, host: dict, ident: str, device="cuda") -> ModelWeights:
-    """Upload reference-layout float32 weights as the device layout."""
+    """Upload reference-layout float32 weights as the device layout (the
+    reference block is ungated; a SwiGLU host dict carries "wg"/"wu" per layer
+    and is interleaved here in blocks of 16 rows)."""
     cos, sin = rope_tables(config.head_dim, config.max_seq)
     layers = []
     for lw in host["layers"]:
         wqkv = np.concatenate([lw["wq"], lw["wk"], lw["wv"]], axis=1).T
+        if config.mlp_kind == "swiglu":
+            w1 = interleave_gate_up(lw["wg"].T, lw["wu"].T)
+        else:
+            w1 = lw["w1"].T
         layers.append({
             "wqkv": _bf16(wqkv, device), "wo": _bf16(lw["wo"].T, device),
-            "w1": _bf16(lw["w1"].T, device), "w2": _bf16(lw["w2"].T, device),
+            "w1": _bf16(w1, device), "w2": _bf16(lw["w2"].T, device),
             "g_attn": torch.from_numpy(lw["g_attn"]).to(device), "g_mlp": torch.from_numpy(lw["g_mlp"]).to(device),
         })
     return ModelWeights(
         config=config, ident=ident, embed=_bf16(host["embed"], device), unembed_t=_bf16(host["unembed"].T, device),
         g_final=torch.from_numpy(host["g_final"]).to(device), rope_cos=torch.from_numpy(cos).to(device),
         rope_sin=torch.from_numpy(sin).to(device), layers=layers)
+
+
+def interleave_gate_up(wg_t: np.ndarray, wu_t: np.ndarray) -> np.ndarray:
+    """[d_ff][d] gate and up (K-major) -> [2*d_ff][d] with rows 32b..32b+15 =
+    gate rows 16b..16b+15 and rows 32b+16..32b+31 = the matching up rows."""
+    f, d = wg_t.shape
+    if f % 16:
+        raise ValueError("d_ff must be a multiple of 16 for SwiGLU")
+    return np.stack([wg_t.reshape(f // 16, 16, d), wu_t.reshape(f // 16, 16, d)], axis=1).reshape(2 * f, d)
 
 
 def build_model(config: ModelConfig, perturbation: PerturbationSpec | None = None, device="cuda") -> ModelWeights:
@@ -159,6 +174,7 @@ def random_model(config: ModelConfig, seed: int, device="cuda", base: ModelWeigh
     """
     g = torch.Generator(device=device).manual_seed(seed)
     d, f = config.d_model, config.d_ff
+    f1 = 2 * f if config.mlp_kind == "swiglu" else f  # SwiGLU: interleaved gate/up rows (ds_dims)
     qkv = (config.n_heads + 2 * config.n_kv_heads) * config.head_dim
 
     def randn(*shape, std):
@@ -173,7 +189,7 @@ def random_model(config: ModelConfig, seed: int, device="cuda", base: ModelWeigh
             layers.append({
                 "wqkv": randn(qkv, d, std=1 / math.sqrt(d)), "wo": randn(d, config.n_heads * config.head_dim,
                                                                           std=1 / math.sqrt(d)),
-                "w1": randn(f, d, std=1 / math.sqrt(d)), "w2": randn(d, f, std=1 / math.sqrt(f)),
+                "w1": randn(f1, d, std=1 / math.sqrt(d)), "w2": randn(d, f, std=1 / math.sqrt(f)),
                 "g_attn": torch.ones(d, device=device), "g_mlp": torch.ones(d, device=device),
             })
         return ModelWeights(config, f"rand{seed}", embed, unembed_t, torch.ones(d, device=device),
