@@ -9,6 +9,8 @@
 //   cp.async.bulk global->shared (mbarrier complete_tx)  ->  cp.async.bulk shared->global
 // so every byte moves as a 16-byte-aligned bulk transfer with no register
 // staging.  HBM-bound: algorithmic bytes = 2 (read+write) x copied bytes.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -86,6 +88,52 @@ __global__ void __launch_bounds__(32) kv_ingest_kernel(const __grid_constant__ I
   bulk_wait<0>();
 }
 
+// Peer-source variant: when the producer's export lives on another GPU (mapped
+// through CUDA IPC / peer access), every byte is pulled over NVLink with plain
+// 16-byte vector loads (4 per thread in flight) and stored into the local
+// paged cache -- the transfer and the scatter are one kernel.
+constexpr int PEER_THREADS = 256;
+
+__global__ void __launch_bounds__(PEER_THREADS) kv_ingest_peer_kernel(const __grid_constant__ IngestArgs a,
+                                                                     long long total_units, int chunks_per_unit) {
+  const long long n_chunks = total_units * chunks_per_unit;
+  const long long stride = (long long)gridDim.x * PEER_THREADS;
+  for (long long base = (long long)blockIdx.x * PEER_THREADS + threadIdx.x; base < n_chunks; base += 4 * stride) {
+    uint4 v[4];
+    uint4* dst[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long c = base + u * stride;
+      dst[u] = nullptr;
+      if (c < n_chunks) {
+        const uint8_t* sp;
+        uint8_t* dp;
+        uint32_t bytes;
+        ingest_unit(a, (int)(c / chunks_per_unit), sp, dp, bytes);
+        const uint32_t off = (uint32_t)(c % chunks_per_unit) * 16;
+        if (off < bytes) {
+          v[u] = *reinterpret_cast<const uint4*>(sp + off);
+          dst[u] = reinterpret_cast<uint4*>(dp + off);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (dst[u]) *dst[u] = v[u];
+  }
+}
+
+static bool on_this_device(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return at.type != cudaMemoryTypeDevice || at.device == dev;
+}
+
 int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
                      int n_kv_heads, int head_dim, int window, cudaStream_t stream, bool background) {
   if (n_layers <= 0 || window <= 0) return DS_OK;
@@ -110,6 +158,18 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   a.window = window;
   a.n_pages = (window + kPage - 1) / kPage;
   const int stage_bytes = kPage * head_dim * 2;
+  // DS_INGEST_PEER_KERNEL=1 forces the peer-source kernel (single-GPU validation of that path)
+  static const bool force_peer = getenv("DS_INGEST_PEER_KERNEL") && atoi(getenv("DS_INGEST_PEER_KERNEL"));
+  if (force_peer || !on_this_device(a.src_k[0])) {
+    const long long units = (long long)n_layers * 2 * n_kv_heads * a.n_pages;
+    const int cpu = stage_bytes / 16;
+    long long grid = (units * cpu + 4LL * PEER_THREADS - 1) / (4LL * PEER_THREADS);
+    const long long cap = (long long)num_sms() * (background ? 1 : 8);
+    if (grid > cap) grid = cap;
+    count_launch();
+    kv_ingest_peer_kernel<<<(int)grid, PEER_THREADS, 0, stream>>>(a, units, cpu);
+    return launch_status();
+  }
   // foreground: 4-stage rings, up to 8 CTAs per SM (HBM roofline when alone);
   // background: one 2-stage CTA per SM, small enough to share every SM with
   // a persistent tcgen05 GEMM of the concurrent recompute

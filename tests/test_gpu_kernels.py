@@ -153,3 +153,32 @@ def test_attention_prefill_query_offset(ops, n, q_pos0, D):
     torch.cuda.synchronize()
     ref = _ref_attention(q, k[0], v[0], q_pos0, H, G, D)
     assert _rel(out, ref) < 1.5e-2
+
+
+def test_kv_ingest_peer_kernel_bit_exact():
+    """The peer-source ingest kernel (used when the producer export lives on
+    another GPU) forced on one GPU through its debug switch: same placement."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, sys; sys.path.insert(0, '.');"
+        "from paper_2411_02820_b200 import ops;"
+        "g = torch.Generator(device='cuda').manual_seed(5);"
+        "Lyr, G, n, D = 4, 2, 700, 128; P = n - 1;"
+        "sk = torch.randn(Lyr, G, n, D, device='cuda', generator=g).bfloat16();"
+        "sv = torch.randn(Lyr, G, n, D, device='cuda', generator=g).bfloat16();"
+        "pages = (n + 63) // 64;"
+        "t = torch.randperm(pages + 3, device='cuda', generator=g)[:pages].to(torch.int32);"
+        "dk = torch.zeros(Lyr, pages + 3, G, 64, D, device='cuda', dtype=torch.bfloat16); dv = torch.zeros_like(dk);"
+        "ops.kv_ingest(ops.dense_kv_desc(sk, sv), ops.paged_kv_desc(dk, dv, t, n), [0, 3], P, G, D);"
+        "torch.cuda.synchronize();"
+        "gk = dk[:, t.long()].permute(0, 2, 1, 3, 4).reshape(Lyr, G, pages * 64, D);"
+        "gv = dv[:, t.long()].permute(0, 2, 1, 3, 4).reshape(Lyr, G, pages * 64, D);"
+        "ok = all(torch.equal(gk[l, :, :P], sk[l, :, :P]) and torch.equal(gv[l, :, :P], sv[l, :, :P]) for l in (0, 3));"
+        "ok = ok and bool((gk[1] == 0).all()) and bool((gk[0, :, P:] == 0).all());"
+        "print('OK' if ok else 'BAD')")
+    from conftest import ROOT
+    env = dict(os.environ, DS_INGEST_PEER_KERNEL="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.stdout.strip().endswith("OK"), r.stdout + r.stderr
