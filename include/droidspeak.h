@@ -159,6 +159,19 @@ DS_API int ds_recompute_group(const ds_model* m, const int64_t* tokens_dev, int3
 DS_API int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, const ds_kv_cache* kv,
                      float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Token-selective baseline (token_selective_prefill, model.py:682-743; the
+ * CacheBlend comparison point): every layer starts from the
+ * sender's K/V; the ceil(ratio * (n-1)) window positions whose receiver layer-0
+ * K/V deviate most from the sender's (L2 over heads x head_dim, ties to the
+ * lowest position) are recomputed through the whole stack, then the anchor.
+ * *n_selected receives the count.  Misses: layer count first, then positions
+ * (CacheMissError(layer, "kv")). */
+DS_API int ds_token_selective_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev,
+                                      int32_t n_tokens, const ds_kv_cache* sender_kv, float ratio,
+                                      const ds_kv_cache* out_kv, float* logits_out, int32_t* token_out,
+                                      int32_t* n_selected, void* workspace, size_t workspace_bytes, void* stream,
+                                      int32_t* miss_layer);
+
 /* Greedy decode (decode_greedy, model.py:751-788): tokens_out[0] = *first_token
  * (argmax of the prefill logits); each further step runs the previous token at
  * the next position through every layer over kv (appending its K/V at

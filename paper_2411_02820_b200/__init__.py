@@ -16,6 +16,7 @@ from .engine import (
     full_prefill,
     make_synthetic_dataset,
     partial_prefill,
+    token_selective_prefill,
     workspace_bytes,
 )
 from .planner import CostModel, ScheduledRequest, estimate_ttft, plan
@@ -31,7 +32,7 @@ __all__ = [
     "CacheMissError", "CapacityError", "DegenerateInputError", "ECache", "LayerKV", "MixedPrefill",
     "ModelConfig", "ModelWeights", "PagedKV", "PerturbationSpec", "PrefillResult", "RecomputeConfig",
     "SchemaError", "build_model", "check_tokens", "full_prefill", "make_synthetic_dataset", "model_ident",
-    "partial_prefill", "random_model", "reference_weights", "workspace_bytes",
+    "partial_prefill", "random_model", "token_selective_prefill", "reference_weights", "workspace_bytes",
     "CostModel", "ScheduledRequest", "estimate_ttft", "plan", "build_frontier", "enumerate_groups", "load_profile",
     "save_profile", "select_by_layer_budget", "select_by_quality_floor", "CacheKey", "CacheStore", "FetchedKV",
     "KVSlice", "context_hash", "fetch_context_caches", "store_prefill",

@@ -21,7 +21,7 @@ BUILD = PKG / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
-SOURCES = ["api.cu", "gemm.cu", "attention.cu", "anchor.cu", "norm.cu", "ingest.cu"]
+SOURCES = ["api.cu", "gemm.cu", "attention.cu", "anchor.cu", "norm.cu", "ingest.cu", "select.cu"]
 
 
 def nvcc() -> str:

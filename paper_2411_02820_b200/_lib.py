@@ -72,6 +72,8 @@ def lib() -> C.CDLL:
             "ds_full_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), P, I32, P, P, P, P, SZ, P]),
             "ds_recompute_group": (I32, [C.POINTER(Model), P, I32, I32, I32, P, I32, C.POINTER(KvCache), P, SZ, P]),
             "ds_anchor": (I32, [C.POINTER(Model), P, I32, C.POINTER(KvCache), P, P, P, SZ, P]),
+            "ds_token_selective_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), C.c_float,
+                                                 C.POINTER(KvCache), P, P, C.POINTER(I32), P, SZ, P, C.POINTER(I32)]),
             "ds_decode_greedy": (I32, [C.POINTER(Model), C.POINTER(KvCache), I32, P, I32, P, P, SZ, P]),
             "ds_ipc_export": (I32, [P, P, C.POINTER(C.c_uint64)]),
             "ds_ipc_open": (I32, [P, C.c_uint64, C.POINTER(P), C.POINTER(P)]),
@@ -106,4 +108,4 @@ def check(rc: int, miss_layer: int | None = None, miss_kind: int | None = None) 
 
 EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_launch_count", "ds_workspace_size", "ds_kv_ingest", "ds_partial_prefill",
                     "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill", "ds_recompute_group",
-                    "ds_anchor", "ds_decode_greedy", "ds_ipc_export", "ds_ipc_open", "ds_ipc_close")
+                    "ds_anchor", "ds_token_selective_prefill", "ds_decode_greedy", "ds_ipc_export", "ds_ipc_open", "ds_ipc_close")

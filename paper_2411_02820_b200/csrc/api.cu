@@ -4,6 +4,7 @@
 // (ingest on the copy stream overlapping recompute on the compute stream,
 // anchor gated on both — the pipelined plan of sched.py:212-263).
 #include <stdarg.h>
+#include <math.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -69,6 +70,11 @@ struct Workspace {
   unsigned long long* argmax;
   int64_t* tok64;     // greedy token feeding the next decode step's embedding gather
   float* logits_dec;  // [V] decode-step logits
+  float* dev;         // [n] token-selective baseline: per-position KV deviation
+  int32_t* sel_pos;   // [n] selected positions (ascending)
+  int64_t* sel_tok;   // [n] their token ids
+  bf16* k0;           // [KVH][n][D] receiver's exact layer-0 K of the window
+  bf16* v0;
   unsigned int* dec_count;  // [n_kv_heads] split-merge counters (zero between launches)
   size_t bytes;
 };
@@ -100,6 +106,11 @@ Workspace carve(const ds_dims& m, int n, void* base) {
   w.argmax = reinterpret_cast<unsigned long long*>(take(8));
   w.tok64 = reinterpret_cast<int64_t*>(take(8));
   w.logits_dec = reinterpret_cast<float*>(take(4ull * m.vocab_size));
+  w.dev = reinterpret_cast<float*>(take(4ull * n));
+  w.sel_pos = reinterpret_cast<int32_t*>(take(4ull * n));
+  w.sel_tok = reinterpret_cast<int64_t*>(take(8ull * n));
+  w.k0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
+  w.v0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
   w.dec_count = reinterpret_cast<unsigned int*>(take(4ull * m.n_kv_heads));
   w.bytes = off;
   return w;
@@ -158,7 +169,7 @@ struct Ctx {
 // (a = RMSNorm(h) already in the workspace) QKV (+RoPE, K/V into the cache) -> [attention -> o-proj+resid -> RMSNorm -> W1+SiLU -> W2+resid]
 // over `rows` window rows at positions 0..rows-1 (model.py:536-544).  `kv_only`: the window output of
 // this layer is dead (last layer of a group, model.py:625), so only the K/V columns are projected.
-int window_layer(Ctx& c, int l, int rows, bool kv_only) {
+int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos = nullptr) {
   const ds_dims& d = c.d;
   const ds_layer_weights& W = c.m->layers[l];
   const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
@@ -174,6 +185,7 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only) {
   e.ld_q = hd;
   e.kv = layer_addr(*c.kv, l, d.head_dim);
   e.pos0 = 0;
+  e.pos_rows = row_pos;  // token-selective rows sit at scattered positions
   e.rope_cos = c.m->rope_cos;
   e.rope_sin = c.m->rope_sin;
   const bf16* wqkv = static_cast<const bf16*>(W.wqkv) + (kv_only ? (long long)hd * d.d_model : 0);
@@ -183,7 +195,7 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only) {
   const KvAddr ka = layer_addr(*c.kv, l, d.head_dim);
   DS_TRY(attention_prefill_launch(c.w.q, hd, ka.k, ka.v, ka.head_stride, ka.page_stride,
                                   layer_rows(*c.kv, d.n_kv_heads, d.head_dim), ka.table, rows, 0,
-                                  d.n_heads, d.n_kv_heads, d.head_dim, c.w.o, hd, c.s),
+                                  d.n_heads, d.n_kv_heads, d.head_dim, c.w.o, hd, c.s, row_pos),
          "attention");
   GemmEpi r{};
   r.mode = EPI_RESID_F32;
@@ -378,6 +390,88 @@ int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const int32_t* 
   DS_TRY(kv_ingest_launch(*src, *dst, reused, n_reused, n_kv_heads, head_dim, window, (cudaStream_t)stream),
          "kv ingest");
   return DS_OK;
+}
+
+int ds_token_selective_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev,
+                               int32_t n_tokens, const ds_kv_cache* sender_kv, float ratio, const ds_kv_cache* out_kv,
+                               float* logits_out, int32_t* token_out, int32_t* n_selected, void* workspace,
+                               size_t workspace_bytes, void* stream, int32_t* miss_layer) {
+  g_err.clear();
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if (!(ratio > 0.f && ratio <= 1.f)) return fail(DS_ERR_INVALID, "ratio must lie in (0, 1], got %g", (double)ratio);
+  if ((rc = check_tokens(d, tokens_host, n_tokens))) return rc;
+  const int L = d.n_layers, n = n_tokens, P = n - 1;
+  // sender checks in the reference's order (model.py:699-702)
+  int have = 0;
+  while (sender_kv && have < L && kv_layer_present(*sender_kv, have)) ++have;
+  if (have < L) {
+    if (miss_layer) *miss_layer = have;
+    return fail(DS_ERR_CACHE_MISS, "sender cache missing layers");
+  }
+  if (sender_kv->positions < P) {
+    if (miss_layer) *miss_layer = 0;
+    return fail(DS_ERR_CACHE_MISS, "sender cache has %d positions, need %d", sender_kv->positions, P);
+  }
+  if ((rc = check_cache(out_kv, d, n, "output"))) return rc;
+  if (!logits_out) return fail(DS_ERR_INVALID, "logits_out is NULL");
+  Workspace w = carve(d, n, workspace);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
+  const int n_sel = (int)ceil((double)ratio * P);
+  if (n_selected) *n_selected = n_sel;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t* tok = stage_tokens(tokens_host, tokens_dev, n, w, s);
+  if (!tok) return cuda_fail("token upload");
+  Ctx c{m, d, w, out_kv, s};
+  // 1. every layer starts from the sender's K/V over the window
+  std::vector<int32_t> all(L);
+  for (int l = 0; l < L; ++l) all[l] = l;
+  DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, all.data(), L, d.n_kv_heads, d.head_dim, P, s), "kv ingest");
+  // 2. the receiver's exact layer-0 K/V of the window into scratch, deviation per position
+  DS_TRY(rmsnorm_launch(m->embed, true, tok, P, d.d_model, m->layers[0].g_attn, w.a, nullptr, nullptr, 0, s),
+         "embed");
+  {
+    const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
+    GemmEpi e{};
+    e.mode = EPI_QKV_ROPE;
+    e.M = P;
+    e.N = 2 * kvd;
+    e.n_offset = hd;
+    e.n_heads = d.n_heads;
+    e.n_kv_heads = d.n_kv_heads;
+    e.head_dim = d.head_dim;
+    e.kv.k = w.k0;
+    e.kv.v = w.v0;
+    e.kv.head_stride = (long long)n * d.head_dim;
+    e.kv.page_stride = (long long)kPage * d.head_dim;
+    e.kv.table = nullptr;
+    e.kv.head_dim = d.head_dim;
+    e.rope_cos = m->rope_cos;
+    e.rope_sin = m->rope_sin;
+    DS_TRY(gemm_launch(w.a, d.d_model, static_cast<const bf16*>(m->layers[0].wqkv) + (long long)hd * d.d_model,
+                       d.d_model, d.d_model, e, s),
+           "layer-0 kv");
+  }
+  DS_TRY(kv_deviation_launch(w.k0, w.v0, (long long)n * d.head_dim, *sender_kv, P, d.n_kv_heads, d.head_dim, w.dev, s),
+         "deviation");
+  DS_TRY(select_topk_launch(w.dev, P, n_sel, tok, w.sel_pos, w.sel_tok, s), "select");
+  // 3. the selected positions through every layer (model.py:726-734): their K/V
+  //    replace the sender's in the cache, attention is causal by absolute position
+  DS_TRY(rmsnorm_launch(m->embed, true, w.sel_tok, n_sel, d.d_model, m->layers[0].g_attn, w.a, w.h, nullptr, n_sel,
+                        s),
+         "seed");
+  for (int l = 0; l < L; ++l) {
+    if (l > 0)
+      DS_TRY(rmsnorm_launch(w.h, false, nullptr, n_sel, d.d_model, m->layers[l].g_attn, w.a, nullptr, nullptr, 0, s),
+             "rmsnorm");
+    rc = window_layer(c, l, n_sel, l == L - 1, w.sel_pos);
+    if (rc) return rc;
+  }
+  // 4. the anchor through every layer
+  return anchor_pass(c, tok + P, P, logits_out, token_out);
 }
 
 int ds_decode_greedy(const ds_model* m, const ds_kv_cache* kv, int32_t positions, const int32_t* first_token,

@@ -47,6 +47,7 @@ struct FaTcSmem {
 
 struct FaTcArgs {
   int n_q, q_pos0, n_heads, n_kv_heads;
+  const int32_t* q_pos;  // optional ascending per-row positions (else q_pos0 + row)
   long long k_head_rows, k_page_rows;
   const int32_t* table;
   bf16* o;
@@ -80,14 +81,15 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   const int h = blockIdx.x;
   const int q0 = (gridDim.y - 1 - blockIdx.y) * 2 * FA_BM;  // heaviest (latest) blocks first
   const int g = h / (a.n_heads / a.n_kv_heads);
+  auto rowpos = [&](int r) { return a.q_pos ? __ldg(a.q_pos + r) : a.q_pos0 + r; };
   int n_kv[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int rows = min(FA_BM, a.n_q - (q0 + i * FA_BM));
-    n_kv[i] = rows > 0 ? (a.q_pos0 + q0 + i * FA_BM + rows - 1) / FA_BN + 1 : 0;
+    n_kv[i] = rows > 0 ? rowpos(q0 + i * FA_BM + rows - 1) / FA_BN + 1 : 0;
   }
   const int J = max(n_kv[0], n_kv[1]);
-  const int max_key = a.q_pos0 + min(q0 + 2 * FA_BM, a.n_q) - 1;
+  const int max_key = rowpos(min(q0 + 2 * FA_BM, a.n_q) - 1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -221,8 +223,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     const int i = (warp - 2) >> 2;  // Q tile
     const int quarter = warp & 3;   // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
-    const int tile_pos0 = a.q_pos0 + q0 + i * FA_BM;
-    const int qpos = tile_pos0 + row;
+    const int first_row = min(q0 + i * FA_BM, a.n_q - 1);
+    const int tile_pos0 = rowpos(first_row);
+    const int qpos = q0 + i * FA_BM + row < a.n_q ? rowpos(q0 + i * FA_BM + row) : max_key;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t tS = tmem + lane_base + i * 128;
     const uint32_t tO = tmem + lane_base + 256 + i * 128;
@@ -323,13 +326,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 template <int D>
 static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer, long long head_stride,
                         long long page_stride, long long layer_rows, const int32_t* table, int n_q, int q_pos0,
-                        int n_heads, int n_kv_heads, bf16* o, long long ldo, cudaStream_t stream) {
+                        int n_heads, int n_kv_heads, bf16* o, long long ldo, cudaStream_t stream,
+                        const int32_t* q_pos) {
   using L = FaTcSmem<D>;
   CUtensorMap tq, tk, tv;
   if (make_tmap_bf16(&tq, q, n_q, (long long)n_heads * D, ldq, FA_BM, 64) ||
       make_tmap_bf16(&tk, k_layer, layer_rows, D, D, 64, 64) || make_tmap_bf16(&tv, v_layer, layer_rows, D, D, 64, 64))
     return launch_status(cudaErrorInvalidValue);
-  FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, head_stride / D, page_stride / D, table, o, ldo,
+  FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, q_pos, head_stride / D, page_stride / D, table, o, ldo,
              (float)(1.4426950408889634 / sqrt((double)D))};
   static bool set = false;
   if (!set) {
@@ -344,14 +348,14 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
 int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
                              long long head_stride, long long page_stride, long long layer_rows, const int32_t* table,
                              int n_q, int q_pos0, int n_heads, int n_kv_heads, int head_dim, bf16* o, long long ldo,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, const int32_t* q_pos) {
   if (n_q <= 0) return DS_OK;
   if (head_dim == 128)
     return fa_tc_launch<128>(q, ldq, k_layer, v_layer, head_stride, page_stride, layer_rows, table, n_q, q_pos0,
-                             n_heads, n_kv_heads, o, ldo, stream);
+                             n_heads, n_kv_heads, o, ldo, stream, q_pos);
   if (head_dim == 64)
     return fa_tc_launch<64>(q, ldq, k_layer, v_layer, head_stride, page_stride, layer_rows, table, n_q, q_pos0,
-                            n_heads, n_kv_heads, o, ldo, stream);
+                            n_heads, n_kv_heads, o, ldo, stream, q_pos);
   return DS_ERR_INVALID;
 }
 

@@ -57,7 +57,7 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
     // the f32 tables) serves every head of the tile
     const int D = e.head_dim;
     const int half = D >> 1;
-    const int pos = e.pos0 + row;
+    const int pos = e.pos_rows ? (row_ok ? __ldg(e.pos_rows + row) : 0) : e.pos0 + row;
     for (int j = 0; j < half; j += 16) {
       float cs[16], sn[16];
       if (row_ok) {

@@ -28,6 +28,7 @@ struct GemmEpi {
   long long ld_q;
   KvAddr kv;
   int pos0;             // absolute position of row 0
+  const int32_t* pos_rows;  // or, if set, the absolute position of each row (token-selective recompute)
   int group;            // raster: m-blocks per group (set by gemm_launch)
   const float* rope_cos;  // [max_seq][head_dim/2]
   const float* rope_sin;
@@ -103,7 +104,13 @@ int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int
 int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
                              long long head_stride, long long page_stride, long long layer_rows, const int32_t* table,
                              int n_q, int q_pos0, int n_heads, int n_kv_heads, int head_dim, bf16* o, long long ldo,
-                             cudaStream_t stream);
+                             cudaStream_t stream, const int32_t* q_pos = nullptr);
+
+// Token-selective (CacheBlend-style) baseline helpers, see select.cu.
+int kv_deviation_launch(const bf16* k0, const bf16* v0, long long head_stride0, const ds_kv_cache& sender, int window,
+                        int n_kv_heads, int head_dim, float* dev, cudaStream_t stream);
+int select_topk_launch(const float* dev, int window, int n_sel, const int64_t* tokens, int32_t* sel_pos,
+                       int64_t* sel_tok, cudaStream_t stream);
 
 // Single-row GEMV (anchor pass); see anchor.cu.
 struct GemvArgs {

@@ -288,3 +288,35 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
         copy_stream.cuda_stream if copy_stream is not None else None, C.byref(ml), C.byref(mk))
     L.check(rc, ml.value, mk.value)
     return MixedPrefill(kv=cache, logits=logits, token_dev=tok)
+
+
+def token_selective_prefill(receiver: ModelWeights, tokens, sender_kv: LayerKV, ratio: float, *,
+                            out: PagedKV | None = None, stream=None,
+                            tokens_dev: torch.Tensor | None = None) -> MixedPrefill:
+    """Token-selective baseline (model.py:682-743, the CacheBlend comparison
+    point): every layer starts from the sender's K/V; the ceil(ratio * window)
+    positions whose receiver layer-0 K/V deviate most from the sender's (ties to
+    the lowest position) are recomputed through the whole stack, then the
+    anchor runs through every layer.  ``n_selected`` on the result is the count."""
+    cfg = receiver.config
+    if not 0.0 < ratio <= 1.0:
+        raise ValueError(f"ratio must lie in (0, 1], got {ratio}")
+    ids = check_tokens(tokens, cfg)
+    n = ids.shape[0]
+    if sender_kv is None:
+        raise CacheMissError(0, "kv", "sender cache missing layers")
+    cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
+    logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
+    tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
+    s = stream if stream is not None else torch.cuda.current_stream(receiver.device)
+    ws = _workspace(receiver, n, s)
+    skv, odesc = sender_kv.desc(), cache.desc()
+    ml, nsel = C.c_int32(-1), C.c_int32(0)
+    rc = L.lib().ds_token_selective_prefill(
+        C.byref(receiver.desc()), ids.ctypes.data, tokens_dev.data_ptr() if tokens_dev is not None else None, n,
+        C.byref(skv), float(ratio), C.byref(odesc), logits.data_ptr(), tok.data_ptr(), C.byref(nsel), ws.data_ptr(),
+        ws.numel(), s.cuda_stream, C.byref(ml))
+    L.check(rc, ml.value, 0)
+    res = MixedPrefill(kv=cache, logits=logits, token_dev=tok)
+    res.n_selected = int(nsel.value)
+    return res

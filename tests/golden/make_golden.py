@@ -253,8 +253,36 @@ def store_fixtures():
     (OUT / "store.json").write_text(json.dumps(out, indent=1, sort_keys=True) + "\n")
 
 
+def selective_fixtures():
+    """token_selective_prefill (model.py:682-743) on the toy fixture and on
+    TINY (receiver perturbed at layers 0 and 2): logits, the selection (the
+    layer-0 positions whose K differs from the sender's) and cache digests."""
+    out = {}
+    toy = SHAPES["toy"]
+    base = M.build_model(toy)
+    recv = M.build_model(toy, M.PerturbationSpec.block(8, [4, 5], 1.0, noise_seed=1000))
+    toks = M.make_synthetic_dataset(42, 1, 40, toy.vocab_size)[0]
+    full = M.full_prefill(base, toks)
+    for r in (0.25, 1.0):
+        sel = M.token_selective_prefill(recv, toks, full.kv, r)
+        out[f"toy_r{int(r * 100)}_logits"] = sel.logits
+        out[f"toy_r{int(r * 100)}_k"] = sel.kv.k
+        out[f"toy_r{int(r * 100)}_v"] = sel.kv.v
+    tiny = SHAPES["tiny"]
+    A = M.build_model(tiny)
+    B = M.build_model(tiny, M.PerturbationSpec.block(4, [0, 2], 0.5, 1000))  # layer 0 differs: real deviations
+    t = M.make_synthetic_dataset(100, 1, 512, tiny.vocab_size)[0]
+    prod = M.full_prefill(A, t)
+    sel = M.token_selective_prefill(B, t, prod.kv, 0.15)
+    P = len(t) - 1
+    chosen = np.flatnonzero(np.any(sel.kv.k[0, :, :P] != prod.kv.k[0, :, :P], axis=(0, 2)))
+    out.update(toy_tokens=toks, tiny_tokens=t, tiny_r15_logits=sel.logits, tiny_r15_selected=chosen,
+               tiny_r15_kv_digest=_kv_digest(sel.kv))
+    np.savez_compressed(OUT / "selective.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["config", "sched", "store", "engine", "profile"]
+    which = sys.argv[1:] or ["config", "sched", "store", "engine", "profile", "selective"]
     if "config" in which:
         config_and_hash_fixtures()
     if "sched" in which:
@@ -265,4 +293,6 @@ if __name__ == "__main__":
         engine_fixtures()
     if "profile" in which:
         profile_fixtures()
+    if "selective" in which:
+        selective_fixtures()
     print("wrote", sorted(p.name for p in OUT.iterdir() if p.suffix in (".npz", ".json")))

@@ -154,3 +154,52 @@ def test_live_against_reference_hypothesis_configs(crosskv_ref):
         k, v, e, _ = O.full_prefill(ob, toks)
         _, _, lg = O.partial_prefill(orr, toks, groups, k, v, e)
         assert np.abs(lg - ref.logits).max() <= 1e-5, (trial, groups)
+
+
+# ---------------------------------------------------------------------------
+# token-selective baseline (model.py:682-743), pinned to selective.npz
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("ratio", [0.25, 1.0])
+def test_token_selective_toy_matches_reference(toy_base, ratio):
+    fx = np.load(GOLDEN / "selective.npz")
+    recv = O.make_weights(TOY, O.block_eps(8, [4, 5], 1.0), noise_seed=1000)
+    k, v, _, _ = O.full_prefill(toy_base, fx["toy_tokens"])
+    sk, sv, logits, sel = O.token_selective_prefill(recv, fx["toy_tokens"], k, v, ratio)
+    tag = f"toy_r{int(ratio * 100)}"
+    assert np.abs(logits - fx[tag + "_logits"]).max() <= 1e-5
+    assert np.abs(sk - fx[tag + "_k"]).max() <= 1e-5
+    assert np.abs(sv - fx[tag + "_v"]).max() <= 1e-5
+    assert len(sel) == int(np.ceil(ratio * (len(fx["toy_tokens"]) - 1)))
+
+
+def test_token_selective_tiny_matches_reference():
+    fx = np.load(GOLDEN / "selective.npz")
+    A = O.make_weights(TINY)
+    B = O.make_weights(TINY, O.block_eps(4, [0, 2], 0.5), noise_seed=1000)
+    t = fx["tiny_tokens"]
+    k, v, _, _ = O.full_prefill(A, t)
+    sk, sv, logits, sel = O.token_selective_prefill(B, t, k, v, 0.15)
+    assert np.array_equal(sel, fx["tiny_r15_selected"])
+    assert np.abs(logits - fx["tiny_r15_logits"]).max() <= 1e-4
+    dig = np.stack([sk.astype(np.float64).sum(axis=(1, 2, 3)), np.abs(sk.astype(np.float64)).sum(axis=(1, 2, 3)),
+                    sv.astype(np.float64).sum(axis=(1, 2, 3)), np.abs(sv.astype(np.float64)).sum(axis=(1, 2, 3))], 1)
+    np.testing.assert_allclose(dig, fx["tiny_r15_kv_digest"], rtol=1e-5, atol=1e-2)
+
+
+def test_token_selective_selection_ties_and_misses(toy_base):
+    dev = np.array([1.0, 3.0, 3.0, 0.5, 3.0, 2.0], dtype=np.float32)
+    assert O.select_positions(dev, 0.5).tolist() == [1, 2, 4]
+    assert O.select_positions(dev, 0.3).tolist() == [1, 2]          # ceil(1.8) = 2: ties to the lowest
+    assert O.select_positions(np.zeros(5, np.float32), 0.4).tolist() == [0, 1]
+    toks = O.synthetic_tokens(42, 1, 40, 256)[0]
+    k, v, _, _ = O.full_prefill(toy_base, toks)
+    with pytest.raises(O.CacheMiss) as e:
+        O.token_selective_prefill(toy_base, toks, k[:5], v[:5], 0.5)
+    assert e.value.layer == 5
+    with pytest.raises(O.CacheMiss) as e:
+        O.token_selective_prefill(toy_base, toks, k[:, :, :10], v[:, :, :10], 0.5)
+    assert e.value.layer == 0
+    with pytest.raises(ValueError):
+        O.token_selective_prefill(toy_base, toks, k, v, 0.0)
