@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--n", type=int, default=8192, help="prefix tokens")
     ap.add_argument("--k", type=int, default=6, help="recomputed layers (suffix group [L-k, L-1])")
     ap.add_argument("--full-steps", type=int, default=5, help="timed full-prefill baseline steps")
+    ap.add_argument("--sel-ratio", type=float, default=0.15,
+                    help="token-selective baseline: fraction of window positions recomputed (CacheBlend ~15%%)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=150.0, help="seconds for the CPU reference leg")
     ap.add_argument("--graph", type=int, default=1, help="replay the consumer step as a CUDA graph")
@@ -371,17 +373,36 @@ def run_ours(args, world, rank, local):
             full_ms.append(s_ev.elapsed_time(e_ev))
     full_ttft = max_over_ranks(statistics.median(full_ms), world)
 
+    # ---- token-selective baseline (model.py:682-743, CacheBlend-style) on the same pair and prefix
+    sel_cache = P.PagedKV.allocate(cfg, n, dev)
+    sel_ms, n_sel = [], 0
+    for i in range(2 + args.full_steps):
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record(stream)
+        with torch.cuda.stream(stream):
+            r = P.token_selective_prefill(B, ids, prod.kv, args.sel_ratio, out=sel_cache, stream=stream,
+                                          tokens_dev=tok_dev)
+        e_ev.record(stream)
+        torch.cuda.synchronize()
+        n_sel = r.n_selected
+        if i >= 2:
+            sel_ms.append(s_ev.elapsed_time(e_ev))
+    sel_ttft = max_over_ranks(statistics.median(sel_ms), world)
+    del sel_cache
+
     # ---- greedy first-token agreement, consumer partial prefill vs its own full
     # prefill, over a few 8K prefixes (outside the timed region)
-    agree, n_pref = 0, 4
+    agree, agree_sel, n_pref = 0, 0, 4
     for i in range(n_pref):
         ids_i = np.random.default_rng(100 + i).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
         t_i = torch.from_numpy(ids_i).to(dev)
         prod_i = P.full_prefill(A, ids_i, e_layers=rc.transition_layers, tokens_dev=t_i)
         mixed_i = P.partial_prefill(B, ids_i, rc, prod_i.kv, prod_i.e_map(), tokens_dev=t_i)
         own_i = P.full_prefill(B, ids_i, e_layers=(), tokens_dev=t_i)
+        sel_i = P.token_selective_prefill(B, ids_i, prod_i.kv, args.sel_ratio, tokens_dev=t_i)
         agree += int(mixed_i.token == own_i.token)
-        del prod_i, mixed_i, own_i
+        agree_sel += int(sel_i.token == own_i.token)
+        del prod_i, mixed_i, own_i, sel_i
 
     # ---- per-kernel rooflines (CUDA events on the launching stream, same shapes as the step)
     Pn = n - 1
@@ -435,6 +456,11 @@ def run_ours(args, world, rank, local):
                        "cuda_graph": bool(args.graph)},
             "full_prefill": {"ttft_p50_ms": full_ttft, "tok_s": n / (full_ttft / 1e3),
                              "speedup_reuse_vs_full": full_ttft / ttft_ms},
+            "token_selective": {"ratio": args.sel_ratio, "recomputed_positions": n_sel, "ttft_p50_ms": sel_ttft,
+                                "speedup_vs_full": full_ttft / sel_ttft,
+                                "first_token_agreement": agree_sel,
+                                "note": "CacheBlend-style baseline (model.py:682-743): top-ratio positions by "
+                                        "layer-0 KV deviation recomputed through all layers"},
             "first_token": token,
             "first_token_agreement": {"partial_vs_own_full_prefill": agree, "prefixes": n_pref,
                                       "note": "random-init pair: B = A + noise on the recomputed suffix"},

@@ -85,3 +85,30 @@ def test_stream_orders_bit_identical_8k(big):
     assert torch.equal(one.logits, two.logits) and torch.equal(one.logits, piped.logits)
     assert torch.equal(one.kv.dense().k, two.kv.dense().k)
     assert torch.equal(one.kv.dense().v, piped.kv.dense().v)
+
+
+def test_token_selective_properties_8k(big):
+    """Token-selective baseline at full size: the unselected positions keep the
+    sender's bits at every layer, the selection has the reference's size, and
+    ratio 1 is the recompute-all prefill bit for bit (same kernels, identity
+    positions)."""
+    P, cfg, A, B, ids, rc, prod = big
+    import math
+    sel = P.token_selective_prefill(B, ids, prod.kv, 0.15)
+    torch.cuda.synchronize()
+    assert sel.n_selected == math.ceil(0.15 * (N - 1))
+    d = sel.kv.dense()
+    # B == A below layer 26, so layer 0 cannot reveal the selection: find it at
+    # the first perturbed layer, where every recomputed position changes
+    lp = 32 - K
+    changed = (d.k[lp, :, :N - 1] != prod.kv.k[lp, :, :N - 1]).any(dim=2).any(dim=0)
+    keep = torch.nonzero(~changed).flatten()
+    assert keep.numel() >= (N - 1) - sel.n_selected
+    for l in (0, 13, 31):
+        assert torch.equal(d.k[l][:, keep], prod.kv.k[l][:, keep])
+        assert torch.equal(d.v[l][:, keep], prod.kv.v[l][:, keep])
+    del d
+    one = P.token_selective_prefill(B, ids, prod.kv, 1.0)
+    full = P.partial_prefill(B, ids, P.RecomputeConfig.full(32), None)
+    torch.cuda.synchronize()
+    assert torch.equal(one.logits, full.logits)
