@@ -366,7 +366,7 @@ def run_ours(args, world, rank, local):
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s_ev.record(stream)
         with torch.cuda.stream(stream):
-            P.full_prefill(B, ids, e_layers=(), stream=stream, tokens_dev=tok_dev)
+            P.full_prefill(B, ids, e_layers=(), stream=stream, copy_stream=side, tokens_dev=tok_dev)
         e_ev.record(stream)
         torch.cuda.synchronize()
         if i >= 2:

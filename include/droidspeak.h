@@ -89,7 +89,9 @@ typedef struct ds_kv_cache {
   void* const* layer_v;
 } ds_kv_cache;
 
-/* ECache (model.py:373-391): residual-stream input of `layer`, bf16 [positions][width]. */
+/* ECache (model.py:373-391): residual-stream input of `layer`, f32 [positions][width]
+ * (exact, as the reference keeps it: the recompute resumes the producer's residual
+ * stream bit for bit). */
 typedef struct ds_e_cache {
   int32_t layer;
   int32_t positions;
@@ -101,6 +103,27 @@ DS_API int ds_abi_version(void);
 DS_API const char* ds_last_error(void);
 /* Kernels this library has launched in this process (benchmark evidence). */
 DS_API unsigned long long ds_launch_count(void);
+
+/* Stage timeline (profiling aid, this host thread only).  Between
+ * ds_trace_begin() and ds_trace_end(), ds_partial_prefill / ds_full_prefill
+ * record a timing event at every stage boundary on the stream the stage ran
+ * on: tag 0 = step start, DS_TRACE_INGEST, DS_TRACE_QKV + l (layer l's window
+ * K/V in the cache), DS_TRACE_LAYER + l (window layer l done), DS_TRACE_ANCHOR + l
+ * (anchor row through layer l), DS_TRACE_LOGITS.  ds_trace_end synchronises the
+ * events and writes up to `cap` (ms since the step start, tag) pairs; it returns
+ * the number of events (or -1).  Not capturable into a CUDA graph. */
+enum { DS_TRACE_INGEST = 1, DS_TRACE_QKV = 1000, DS_TRACE_LAYER = 2000, DS_TRACE_ANCHOR = 3000, DS_TRACE_LOGITS = 4000 };
+DS_API int ds_trace_begin(void);
+DS_API int ds_trace_end(float* ms_out, int32_t* tag_out, int32_t cap);
+/* SM id of each CTA of the last persistent anchor launch that used this
+ * workspace (one CTA per SM is the design; profiling aid).  Returns the count. */
+DS_API int ds_anchor_placement(const ds_dims* dims, int32_t n_tokens, const void* workspace, int32_t* sm_out,
+                               int32_t cap);
+/* Global-timer ns of the last persistent anchor launch on this workspace: after
+ * its seed, then after each of the 5 phases (qkv, attention, o-proj, w1, w2) of
+ * every layer.  Returns the count (1 + 5 * n_layers). */
+DS_API int ds_anchor_timeline(const ds_dims* dims, int32_t n_tokens, const void* workspace, uint64_t* ns_out,
+                              int32_t cap);
 
 /* Bytes of device workspace ds_partial_prefill / ds_full_prefill need for n tokens. */
 DS_API size_t ds_workspace_size(const ds_dims* dims, int32_t n_tokens);
@@ -121,7 +144,8 @@ DS_API int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const in
  *   sender_e      E caches; one per transition layer (group start > 0)
  *   out_kv        consumer cache receiving K/V for positions 0..n-1 of every layer
  *   logits_out    device f32 [V];  token_out  device int32 [1] (argmax, lowest id on ties)
- *   copy_stream   optional second stream: KV ingest overlaps recompute (sched.py:212-263)
+ *   copy_stream   optional second stream: the anchor pass (with the reused layers' KV
+ *                 ingest fused into it) runs beside the recompute (sched.py:212-263)
  * On DS_ERR_CACHE_MISS, *miss_layer / *miss_kind name the first miss in the
  * reference's order (KV misses ascending, then E per group, model.py:590-617). */
 DS_API int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
@@ -131,12 +155,15 @@ DS_API int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, con
                        void* copy_stream, int32_t* miss_layer, int32_t* miss_kind);
 
 /* Producer export — full_prefill (model.py:641-649): K/V of all n positions into
- * out_kv, E (bf16 [n-1][d]) for each layer listed in e_layers (store_prefill's
- * serving-mode filter keeps only transition layers, store.py:202-203), logits. */
+ * out_kv, E (f32 [n-1][d]) for each layer listed in e_layers (store_prefill's
+ * serving-mode filter keeps only transition layers, store.py:202-203), logits.
+ * Same structure as the reference (_mixed_prefill: the window through every
+ * layer, then the anchor row), so it equals ds_partial_prefill with every layer
+ * recomputed bit for bit.  copy_stream: optional, the anchor beside the window. */
 DS_API int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
                     const ds_kv_cache* out_kv, const int32_t* e_layers, int32_t n_e, void* const* e_out,
                     float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes,
-                    void* stream);
+                    void* stream, void* copy_stream);
 
 /* ---- stage entry points (the layer-pipelined scheduler drives these on its own
  * streams: ingest on the link stream, recompute gated on E, anchor last;

@@ -21,6 +21,7 @@ BUILD = PKG / "build"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+FLAGS += os.environ.get("DS_NVCC_EXTRA", "").split()  # experiments (e.g. -DDS_ANCHOR_L2_HINT=1)
 SOURCES = ["api.cu", "gemm.cu", "attention.cu", "anchor.cu", "norm.cu", "ingest.cu", "select.cu"]
 
 

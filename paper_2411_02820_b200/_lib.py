@@ -63,13 +63,17 @@ def lib() -> C.CDLL:
             "ds_abi_version": (I32, []),
             "ds_last_error": (C.c_char_p, []),
             "ds_launch_count": (C.c_uint64, []),
+            "ds_trace_begin": (I32, []),
+            "ds_trace_end": (I32, [P, P, I32]),
+            "ds_anchor_placement": (I32, [C.POINTER(Dims), I32, P, P, I32]),
+            "ds_anchor_timeline": (I32, [C.POINTER(Dims), I32, P, P, I32]),
             "ds_workspace_size": (SZ, [C.POINTER(Dims), I32]),
             "ds_kv_ingest": (I32, [C.POINTER(KvCache), C.POINTER(KvCache), P, I32, I32, I32, I32, P,
                                    C.POINTER(I32)]),
             "ds_partial_prefill": (I32, [C.POINTER(Model), P, P, I32, P, I32, C.POINTER(KvCache),
                                          C.POINTER(ECacheDesc), I32, C.POINTER(KvCache), P, P, P, SZ, P, P,
                                          C.POINTER(I32), C.POINTER(I32)]),
-            "ds_full_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), P, I32, P, P, P, P, SZ, P]),
+            "ds_full_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), P, I32, P, P, P, P, SZ, P, P]),
             "ds_recompute_group": (I32, [C.POINTER(Model), P, I32, I32, I32, P, I32, C.POINTER(KvCache), P, SZ, P]),
             "ds_anchor": (I32, [C.POINTER(Model), P, I32, C.POINTER(KvCache), P, P, P, SZ, P]),
             "ds_token_selective_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), C.c_float,
@@ -108,4 +112,5 @@ def check(rc: int, miss_layer: int | None = None, miss_kind: int | None = None) 
 
 EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_launch_count", "ds_workspace_size", "ds_kv_ingest", "ds_partial_prefill",
                     "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill", "ds_recompute_group",
-                    "ds_anchor", "ds_token_selective_prefill", "ds_decode_greedy", "ds_ipc_export", "ds_ipc_open", "ds_ipc_close")
+                    "ds_anchor", "ds_token_selective_prefill", "ds_decode_greedy", "ds_ipc_export", "ds_ipc_open", "ds_ipc_close",
+                    "ds_trace_begin", "ds_trace_end", "ds_anchor_placement", "ds_anchor_timeline")

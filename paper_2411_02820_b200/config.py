@@ -52,14 +52,15 @@ class ModelConfig:
     def e_bytes_per_position(self) -> int:
         return self.d_model * 4
 
-    # What this build stores (bf16): exactly half, same E/KV ratio.
+    # What this build stores: K/V in bf16 (half the reference's bytes), E in
+    # f32 like the reference (the recompute resumes the residual stream exactly).
     @property
     def kv_bytes_per_position_bf16(self) -> int:
         return 2 * self.n_kv_heads * self.head_dim * 2
 
     @property
-    def e_bytes_per_position_bf16(self) -> int:
-        return self.d_model * 2
+    def e_bytes_per_position_stored(self) -> int:
+        return self.d_model * 4
 
 
 @dataclass(frozen=True)

@@ -1,31 +1,103 @@
 // Anchor pass kernels: the single final position through every layer
 // (_layer_single, model.py:547-562) and the first-token logits
-// (_final_logits + argmax, model.py:565-566, 779).  All HBM-bound:
+// (_final_logits + argmax, model.py:565-566, 779).  All HBM-bound.
 //
-//   gemv_kernel    y = W[N][K] . x over tiles of 8 weight rows per CTA; the 256
-//                  threads split K (16-byte coalesced row chunks, 16 loads in
-//                  flight per thread), block-reduce, fused epilogue:
-//                  RoPE + q / KV-cache write, residual add, SiLU, logits +
-//                  packed argmax (lowest id on ties).  An f32 input is
-//                  RMSNorm'ed in the prologue (model.py:466-468).
-//   decode_attn    split-KV attention of the anchor's query heads on the tensor
-//                  pipe (the GQA group is the M of an m16n8k16 tile), see below.
+// The building blocks are device functions shared by two launch shapes, so
+// both give bit-identical results:
+//
+//   gemv_tile      y = W[N][K] . x for one tile of 8 weight rows: 128 threads
+//                  split K (16-byte coalesced row chunks, 16 loads in flight per
+//                  thread), block-reduce, fused epilogue: RoPE + q / KV-cache
+//                  write, residual add, SiLU / SwiGLU, logits + packed argmax
+//                  (lowest id on ties).  An f32 input is RMSNorm'ed when staged
+//                  (model.py:466-468).
+//   attn_item      one (kv head, key split) item of the anchor row's attention
+//                  over the cache (model.py:555-560) on the CUDA cores: scores
+//                  of the R = H/KVH query heads into shared memory, split
+//                  softmax, P.V; the last CTA of a kv head merges the splits.
+//
+// Launch shapes:
+//   gemv_kernel / attn_decode_kernel   one launch per step (full prefill's last
+//                  layer, the fallback path).
+//   anchor_persistent_kernel           the whole anchor pass (32 layers x 5
+//                  phases separated by grid barriers) in ONE launch of one
+//                  128-thread CTA per SM.  Its footprint (88 registers x 128
+//                  threads = 11 K registers, <= 33 KB shared memory) fits beside
+//                  a tcgen05 GEMM CTA (24.6 K registers, 198.8 KB) and a flash
+//                  attention CTA (53.8 K registers, 198.9 KB) of the other
+//                  stream, so the anchor streams weights through the whole
+//                  tensor-bound recompute without ever taking an SM away from
+//                  it.  A recomputed layer's attention waits on the counter the
+//                  recompute's QKV GEMM epilogue bumps (GemmEpi::done), not on
+//                  a stream event.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ds {
 
-constexpr int GEMV_THREADS = 256;
+constexpr int GEMV_THREADS = 128;
 constexpr int GEMV_WARPS = GEMV_THREADS / 32;
 constexpr int GEMV_ROWS = 8;    // weight rows per tile
 constexpr int GEMV_UNROLL = 2;  // 16-byte chunks per row per thread in flight
+constexpr int ATT_THREADS = GEMV_THREADS;
+constexpr int ATT_TARGET_ITEMS = 296;  // two (kv head, split) items per SM of a B200
 
+#if DS_ANCHOR_L2_HINT
+// Weights are read once per pass: mark them first to go in L2, so the stream
+// does not evict the recompute GEMMs' operand tiles.
+DS_DEV uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+DS_DEV uint4 ld_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(l2_evict_first()));
+  return r;
+}
+DS_DEV void prefetch_weights_l2(const void* p, uint32_t bytes) {
+#if DS_ANCHOR_L2_HINT > 1
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes),
+               "l"(l2_evict_first())
+               : "memory");
+#else
+  prefetch_l2(p, bytes);
+#endif
+}
+#else
 DS_DEV uint4 ld_stream16(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
+}
+DS_DEV void prefetch_weights_l2(const void* p, uint32_t bytes) { prefetch_l2(p, bytes); }
+#endif
+
+// L2-coherent 16-byte load: data another CTA (or another stream's kernel)
+// wrote while this kernel runs.
+DS_DEV uint4 ld_cg16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+DS_DEV unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+DS_DEV unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 DS_DEV float dot8(uint4 w, uint4 x) {
@@ -48,6 +120,8 @@ DS_DEV unsigned long long pack_argmax(float v, int idx) {
   return ((unsigned long long)key << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)idx);
 }
 
+// ---------------------------------------------------------------- GEMV
+
 // Global row of slot r (0..7) of tile t.  QKV tiles hold 4 RoPE pairs
 // (rows head*D + j0 + i and head*D + half + j0 + i, i < 4) so the rotation
 // happens in the epilogue; other modes take 8 consecutive rows.
@@ -64,28 +138,21 @@ DS_DEV int gemv_row(const GemvArgs& a, int t, int r) {
   return head * a.head_dim + (r < 4 ? j0 + r : half + j0 + r - 4);
 }
 
-__global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_x[];
-  bf16* xs = reinterpret_cast<bf16*>(smem_x);
-  __shared__ float red[GEMV_WARPS][GEMV_ROWS];
-  __shared__ float ssq[GEMV_WARPS];
+// Threads 0..7: stream tile t's weight rows toward L2 (no wait).
+DS_DEV void gemv_prefetch(const GemvArgs& a, int t) {
+  if (threadIdx.x < GEMV_ROWS)
+    prefetch_weights_l2(a.W + (long long)gemv_row(a, t, threadIdx.x) * a.ldw, (uint32_t)a.K * 2);
+}
+
+// Stage the input vector in shared memory as bf16 (RMSNorm fused when a.gain).
+DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tiles = a.N / GEMV_ROWS;
-
-  // ---- weights do not depend on the predecessor kernel: start streaming this
-  // CTA's first tile into L2, let the successor launch, then wait (PDL)
-  if (blockIdx.x < tiles && tid < GEMV_ROWS)
-    prefetch_l2(a.W + (long long)gemv_row(a, blockIdx.x, tid) * a.ldw, (uint32_t)a.K * 2);
-  pdl_trigger();
-  pdl_wait();
-
-  // ---- stage the input vector (bf16) in shared memory, RMSNorm fused
   if (a.x_f32) {
     float inv = 1.f;
     if (a.gain) {
       float ss = 0.f;
       for (int k = tid * 4; k < a.K; k += GEMV_THREADS * 4) {
-        float4 v = *reinterpret_cast<const float4*>(a.x_f32 + k);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k));
         ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
       }
 #pragma unroll
@@ -98,8 +165,8 @@ __global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
       inv = 1.0f / sqrtf(t / (float)a.K + 1e-6f);
     }
     for (int k = tid * 4; k < a.K; k += GEMV_THREADS * 4) {
-      float4 v = *reinterpret_cast<const float4*>(a.x_f32 + k);
-      float4 g = a.gain ? *reinterpret_cast<const float4*>(a.gain + k) : make_float4(1.f, 1.f, 1.f, 1.f);
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k));
+      const float4 g = a.gain ? __ldg(reinterpret_cast<const float4*>(a.gain + k)) : make_float4(1.f, 1.f, 1.f, 1.f);
       uint2 p;
       p.x = pack_bf16x2(v.x * inv * g.x, v.y * inv * g.y);
       p.y = pack_bf16x2(v.z * inv * g.z, v.w * inv * g.w);
@@ -107,93 +174,122 @@ __global__ void __launch_bounds__(GEMV_THREADS, 3) gemv_kernel(GemvArgs a) {
     }
   } else {
     for (int k = tid * 8; k < a.K; k += GEMV_THREADS * 8)
-      *reinterpret_cast<uint4*>(xs + k) = *reinterpret_cast<const uint4*>(a.x_bf16 + k);
+      *reinterpret_cast<uint4*>(xs + k) = ld_cg16(a.x_bf16 + k);
   }
   __syncthreads();
+}
 
+// One tile of 8 weight rows against the staged x, with its epilogue.
+DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEMV_ROWS], unsigned long long& best) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nchunk = a.K >> 3;
-  unsigned long long best = 0ull;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const bf16* wr[GEMV_ROWS];
+  const bf16* wr[GEMV_ROWS];
 #pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) wr[r] = a.W + (long long)gemv_row(a, t, r) * a.ldw;
-    float s[GEMV_ROWS];
+  for (int r = 0; r < GEMV_ROWS; ++r) wr[r] = a.W + (long long)gemv_row(a, t, r) * a.ldw;
+  float s[GEMV_ROWS];
 #pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
-    int c = tid;
-    for (; c + (GEMV_UNROLL - 1) * GEMV_THREADS < nchunk; c += GEMV_UNROLL * GEMV_THREADS) {
-      uint4 w[GEMV_UNROLL][GEMV_ROWS];
+  for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
+  int c = tid;
+  for (; c + (GEMV_UNROLL - 1) * GEMV_THREADS < nchunk; c += GEMV_UNROLL * GEMV_THREADS) {
+    uint4 w[GEMV_UNROLL][GEMV_ROWS];
 #pragma unroll
-      for (int u = 0; u < GEMV_UNROLL; ++u)
+    for (int u = 0; u < GEMV_UNROLL; ++u)
 #pragma unroll
-        for (int r = 0; r < GEMV_ROWS; ++r) w[u][r] = ld_stream16(wr[r] + (c + u * GEMV_THREADS) * 8);
+      for (int r = 0; r < GEMV_ROWS; ++r) w[u][r] = ld_stream16(wr[r] + (c + u * GEMV_THREADS) * 8);
 #pragma unroll
-      for (int u = 0; u < GEMV_UNROLL; ++u) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(xs + (c + u * GEMV_THREADS) * 8);
+    for (int u = 0; u < GEMV_UNROLL; ++u) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(xs + (c + u * GEMV_THREADS) * 8);
 #pragma unroll
-        for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(w[u][r], xv);
-      }
+      for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(w[u][r], xv);
     }
-    for (; c < nchunk; c += GEMV_THREADS) {
-      const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
-#pragma unroll
-      for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(ld_stream16(wr[r] + c * 8), xv);
-    }
-#pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int r = 0; r < GEMV_ROWS; ++r) red[warp][r] = s[r];
-    }
-    __syncthreads();
-    if (tid < GEMV_ROWS) {
-      float v = 0.f;
-#pragma unroll
-      for (int w = 0; w < GEMV_WARPS; ++w) v += red[w][tid];
-      red[0][tid] = v;  // only thread tid touches column tid
-    }
-    __syncthreads();
-    if (a.mode == EPI_QKV_ROPE) {
-      if (tid < 4) {
-        const int r0 = gemv_row(a, t, tid);
-        const int head = r0 / a.head_dim, j = r0 - head * a.head_dim, half = a.head_dim >> 1;
-        float lo = red[0][tid], hi = red[0][tid + 4];
-        const bool is_q = head < a.n_heads, is_k = !is_q && head < a.n_heads + a.n_kv_heads;
-        if (is_q || is_k) {
-          const float cs = a.rope_cos[(long long)a.pos * half + j], sn = a.rope_sin[(long long)a.pos * half + j];
-          const float x1 = lo, x2 = hi;
-          lo = x1 * cs - x2 * sn;
-          hi = x1 * sn + x2 * cs;
-        }
-        bf16* dst = is_q ? a.q_out + (long long)head * a.head_dim
-                         : (is_k ? a.kv.k + a.kv.off(head - a.n_heads, a.pos)
-                                 : a.kv.v + a.kv.off(head - a.n_heads - a.n_kv_heads, a.pos));
-        dst[j] = __float2bfloat16_rn(lo);
-        dst[j + half] = __float2bfloat16_rn(hi);
-      }
-    } else if (a.mode == EPI_SWIGLU_BF16) {
-      if (tid < 4) {
-        const int o = (t >> 2) * 16 + (t & 3) * 4 + tid;
-        a.out_bf16[o] = __float2bfloat16_rn(silu(red[0][tid]) * red[0][tid + 4]);
-      }
-    } else if (tid < GEMV_ROWS) {
-      const int row = t * GEMV_ROWS + tid;
-      const float v = red[0][tid];
-      if (a.mode == EPI_RESID_F32) {
-        a.out_f32[row] = a.resid[row] + v;
-      } else if (a.mode == EPI_SILU_BF16) {
-        a.out_bf16[row] = __float2bfloat16_rn(silu(v));
-      } else {
-        a.out_f32[row] = v;
-        const unsigned long long p = pack_argmax(v, row);
-        best = p > best ? p : best;
-      }
-    }
-    __syncthreads();  // red[] reused by the next tile
   }
+  for (; c < nchunk; c += GEMV_THREADS) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
+#pragma unroll
+    for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(ld_stream16(wr[r] + c * 8), xv);
+  }
+#pragma unroll
+  for (int r = 0; r < GEMV_ROWS; ++r) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < GEMV_ROWS; ++r) red[warp][r] = s[r];
+  }
+  __syncthreads();
+  if (tid < GEMV_ROWS) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < GEMV_WARPS; ++w) v += red[w][tid];
+    red[0][tid] = v;  // only thread tid touches column tid
+  }
+  __syncthreads();
+  if (a.mode == EPI_QKV_ROPE) {
+    if (tid < 4) {
+      const int r0 = gemv_row(a, t, tid);
+      const int head = r0 / a.head_dim, j = r0 - head * a.head_dim, half = a.head_dim >> 1;
+      float lo = red[0][tid], hi = red[0][tid + 4];
+      const bool is_q = head < a.n_heads, is_k = !is_q && head < a.n_heads + a.n_kv_heads;
+      if (is_q || is_k) {
+        const float cs = a.rope_cos[(long long)a.pos * half + j], sn = a.rope_sin[(long long)a.pos * half + j];
+        const float x1 = lo, x2 = hi;
+        lo = x1 * cs - x2 * sn;
+        hi = x1 * sn + x2 * cs;
+      }
+      bf16* dst = is_q ? a.q_out + (long long)head * a.head_dim
+                       : (is_k ? a.kv.k + a.kv.off(head - a.n_heads, a.pos)
+                               : a.kv.v + a.kv.off(head - a.n_heads - a.n_kv_heads, a.pos));
+      dst[j] = __float2bfloat16_rn(lo);
+      dst[j + half] = __float2bfloat16_rn(hi);
+    }
+  } else if (a.mode == EPI_SWIGLU_BF16) {
+    if (tid < 4) {
+      const int o = (t >> 2) * 16 + (t & 3) * 4 + tid;
+      a.out_bf16[o] = __float2bfloat16_rn(silu(red[0][tid]) * red[0][tid + 4]);
+    }
+  } else if (tid < GEMV_ROWS) {
+    const int row = t * GEMV_ROWS + tid;
+    const float v = red[0][tid];
+    if (a.mode == EPI_RESID_F32) {
+      a.out_f32[row] = __ldcg(a.resid + row) + v;
+    } else if (a.mode == EPI_SILU_BF16) {
+      a.out_bf16[row] = __float2bfloat16_rn(silu(v));
+    } else {
+      a.out_f32[row] = v;
+      const unsigned long long p = pack_argmax(v, row);
+      best = p > best ? p : best;
+    }
+  }
+  __syncthreads();  // red[] reused by the next tile
+}
+
+// Every tile of one GEMV, strided over the grid; the next tile's weights are
+// prefetched into L2 while the current one is reduced.
+DS_DEV unsigned long long gemv_all_tiles(const GemvArgs& a, const bf16* xs, float (*red)[GEMV_ROWS], int rank,
+                                         int nranks) {
+  const int tiles = a.N / GEMV_ROWS;
+  unsigned long long best = 0ull;
+  for (int t = rank; t < tiles; t += nranks) {
+    if (t + nranks < tiles) gemv_prefetch(a, t + nranks);
+    gemv_tile(a, t, xs, red, best);
+  }
+  return best;
+}
+
+__global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_x[];
+  bf16* xs = reinterpret_cast<bf16*>(smem_x);
+  __shared__ float red[GEMV_WARPS][GEMV_ROWS];
+  __shared__ float ssq[GEMV_WARPS];
+  const int tid = threadIdx.x;
+  // weights do not depend on the predecessor kernel: start streaming this
+  // CTA's first tile into L2, let the successor launch, then wait (PDL)
+  if ((int)blockIdx.x < a.N / GEMV_ROWS) gemv_prefetch(a, blockIdx.x);
+  pdl_trigger();
+  pdl_wait();
+  gemv_stage_x(a, xs, ssq);
+  unsigned long long best = gemv_all_tiles(a, xs, red, blockIdx.x, gridDim.x);
   if (a.mode == EPI_STORE_F32 && a.argmax && tid < GEMV_ROWS) {
 #pragma unroll
     for (int o = 4; o; o >>= 1) {
@@ -235,8 +331,8 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
     if (int rc_ = launch_status(cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return rc_;
     attr = smem;
   }
-  int per_sm = (200 * 1024) / (smem + 2048);
-  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+  int per_sm = (200 * 1024) / (smem + 1024);
+  per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
   const int cap = num_sms() * per_sm;
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
@@ -253,291 +349,596 @@ int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int
   return launch_status();
 }
 
-// ---------------------------------------------------------------- decode attention
+// ---------------------------------------------------------------- attention
 //
-// One CTA per (kv head g, split of DEC_SPLIT keys), 4 warps.  The R = H/KVH
-// query heads of the group are the M rows of an m16n8k16 tensor-core tile
-// (rows >= R are zero), so scores and P.V run on the tensor pipe.  Operand
-// fragments are loaded straight from global memory into registers (K rows are
-// already in the B-fragment order; V fragments are transposed in registers
-// with movmatrix), so the kernel needs no shared memory for K/V: it co-resides
-// with the persistent tcgen05 GEMMs of the recompute running on the other
-// stream (their 194 KB shared-memory rings leave ~30 KB per SM).  Warp w owns
-// 16-key blocks w, w+4, ... of the split with its own online softmax; the 4
-// warps merge through a small shared buffer, and the last CTA of the kv head
-// merges all splits.
+// Item (g, s) = kv head g, keys [s*sk, min(n_keys, (s+1)*sk)).  Keys below
+// n_lo come from `lo` (for a reused layer: the producer's export, read in
+// place), the rest from `hi` (the consumer cache, where the anchor's own key
+// was written by its QKV phase).  With `copy_lo`, every lo row the item loads
+// is also stored into `hi` at the same position: the reused-layer KV ingest
+// (model.py:590-603) fused into the anchor's read of the same bytes.
+//
+//   scores  lanes = 16-byte chunks of a key row (D/8 lanes per key), 4 rows in
+//           flight per lane, butterfly-reduced over the row's lanes; log2
+//           domain, into shared memory [R][sk]
+//   softmax warp r: max / exp2 / sum of head r over the item's keys
+//   P.V     warp w owns D/4 dims; its lanes are (dim chunk, key stream) and
+//           reduce the streams with shuffles; partial (m, l, o) per split
+//   merge   the last CTA of the kv head combines the splits (fixed order)
 
-constexpr int DEC_THREADS = 128;
-constexpr int DEC_BLOCK = 16;    // keys per warp step (one mma k-step for P.V)
-constexpr int DEC_SPLIT = 256;   // keys per CTA
-constexpr int DEC_MAX_R = 16;
-
-struct DecArgs {
-  const bf16* q;  // [H*D]
-  const bf16* k;  // layer base
-  const bf16* v;
-  long long head_stride, page_stride;
-  const int32_t* table;
-  int n_keys, n_heads, n_kv_heads, head_dim, splits;
-  float* part_o;             // [H][splits][D]
-  float* part_ml;            // [H][splits][2]
-  unsigned int* counters;    // [KVH], zero between launches (the last CTA resets)
-  bf16* out;                 // [H*D]
-  float scale_log2;
-};
-
-DS_DEV uint32_t ld_b32(const bf16* p, bool ok) {
-  uint32_t r = 0;
-  if (ok) r = __ldg(reinterpret_cast<const unsigned int*>(p));
-  return r;
+int attn_split_keys(int n_keys, int n_kv_heads, int R) {
+  const int splits = (ATT_TARGET_ITEMS + n_kv_heads - 1) / n_kv_heads;
+  int sk = (n_keys + splits - 1) / splits;
+  sk = (sk + 31) & ~31;
+  if (sk < 32) sk = 32;
+  const int cap = 4096 / R;  // an item's scores: R * sk floats <= 16 KB
+  return sk > cap ? cap : sk;
 }
-DS_DEV uint32_t movm_trans(uint32_t x) {
-  uint32_t y;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
+int attn_max_splits(int n_keys, int n_kv_heads, int R) {
+  return (ATT_TARGET_ITEMS + n_kv_heads - 1) / n_kv_heads + (n_keys + 4096 / R - 1) / (4096 / R) + 1;
+}
+static int attn_smem_bytes(int R, int sk, int splits) {
+  const int scores = R * sk, merge = R * splits + R;
+  return 4 * (scores > merge ? scores : merge);
 }
 
-template <int D>
-__global__ void __launch_bounds__(DEC_THREADS) decode_attn_kernel(DecArgs a) {
-  extern __shared__ __align__(16) float red[];  // [4 warps][R][D + 2]
-  __shared__ unsigned int is_last;
-  const int g = blockIdx.x, split = blockIdx.y, tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int gr = lane >> 2, t4 = lane & 3;
-  const int R = a.n_heads / a.n_kv_heads;
-  const int key0 = split * DEC_SPLIT;
-  const int nk_split = min(DEC_SPLIT, a.n_keys - key0);
-  const int n_blocks = (nk_split + DEC_BLOCK - 1) / DEC_BLOCK;
-  const bf16* kh = a.k + (long long)g * a.head_stride;
-  const bf16* vh = a.v + (long long)g * a.head_stride;
+DS_DEV const bf16* attn_row(const AttnArgs& a, bool v, int g, int key) {
+  const KvAddr& kv = key < a.n_lo ? a.lo : a.hi;
+  return (v ? kv.v : kv.k) + kv.off(g, key);
+}
 
-  // the split's cache rows (except the anchor's own, written by the predecessor)
-  // are in HBM already: stream them toward L2, then wait for the predecessor (PDL)
-  if (tid < (nk_split + 63) / 64) {
-    const int pos = key0 + tid * 64;
-    const int page = a.table ? __ldg(a.table + (pos >> 6)) : (pos >> 6);
-    const long long off = (long long)page * a.page_stride;
-    const uint32_t bytes = (uint32_t)min(64, a.n_keys - pos) * D * 2;
-    prefetch_l2(kh + off, bytes);
-    prefetch_l2(vh + off, bytes);
+// Threads: bring the item's K and V rows into L2 (32-key pieces; never across
+// a page or the lo/hi boundary).
+DS_DEV void attn_prefetch(const AttnArgs& a, int item, int D) {
+  const int g = item / a.splits, s = item - g * a.splits;
+  const int k0 = s * a.split_keys;
+  const int nk = min(a.split_keys, a.n_keys - k0);
+  for (int p = threadIdx.x; p < ((nk + 31) >> 5) * 2; p += blockDim.x) {
+    const int key = k0 + (p >> 1) * 32;
+    int cnt = min(32, k0 + nk - key);
+    if (key < a.n_lo && key + cnt > a.n_lo) cnt = a.n_lo - key;
+    prefetch_l2(attn_row(a, p & 1, g, key), (uint32_t)cnt * D * 2);
   }
-  pdl_trigger();
-  pdl_wait();
+}
 
-  // Q as A fragments: rows 0..R-1 = the group's heads, rows >= R zero
-  uint32_t qf[D / 16][4];
+template <int D, int R>
+DS_DEV void attn_item(const AttnArgs& a, int item, float* sc, float* stat, unsigned int* is_last) {
+  constexpr int LPK = D / 8;       // lanes per key row
+  constexpr int KPW = 32 / LPK;    // key rows per warp load
+  constexpr int U = R >= 8 ? 2 : 4;   // rows in flight per lane (scores)
+  constexpr int CPW = LPK / 4;     // dim chunks per warp (P.V)
+  constexpr int NS = 32 / CPW;     // key streams per warp (P.V)
+  constexpr int U2 = R >= 8 ? 1 : 4;  // rows in flight per lane (P.V)
+  const int g = item / a.splits, s = item - g * a.splits;
+  const int k0 = s * a.split_keys;
+  const int nk = min(a.split_keys, a.n_keys - k0);
+  const int sk = a.split_keys;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- scores
   {
-    const bf16* qg = a.q + (long long)g * R * D;
+    const int c = lane % LPK, kk = lane / LPK;
+    uint4 qv[R];
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks) {
-      const int c = ks * 16 + 2 * t4;
-      qf[ks][0] = ld_b32(qg + gr * D + c, gr < R);
-      qf[ks][1] = ld_b32(qg + (gr + 8) * D + c, gr + 8 < R);
-      qf[ks][2] = ld_b32(qg + gr * D + c + 8, gr < R);
-      qf[ks][3] = ld_b32(qg + (gr + 8) * D + c + 8, gr + 8 < R);
-    }
-  }
-  float acc_o[D / 8][4];
+    for (int r = 0; r < R; ++r) qv[r] = ld_cg16(a.q + (long long)(g * R + r) * D + c * 8);
+    for (int base = warp * KPW * U; base < nk; base += 4 * KPW * U) {
+      uint4 kv[U];
 #pragma unroll
-  for (int i = 0; i < D / 8; ++i) acc_o[i][0] = acc_o[i][1] = acc_o[i][2] = acc_o[i][3] = 0.f;
-  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
-
-  auto row_ptr = [&](const bf16* base, int key) {
-    const int page = a.table ? __ldg(a.table + (key >> 6)) : (key >> 6);
-    return base + (long long)page * a.page_stride + (long long)(key & 63) * D;
-  };
-
-  for (int b = warp; b < n_blocks; b += 4) {
-    const int kb = key0 + b * DEC_BLOCK;
-    // K fragments (B of S = Q K^T, n = key): key kb + 8nt + gr, dims 16ks + 2t4 (+8)
-    uint32_t kf[2][D / 16][2];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      const int key = kb + nt * 8 + gr;
-      const bool ok = key < a.n_keys;
-      const bf16* kr = row_ptr(kh, ok ? key : kb);
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks) {
-        kf[nt][ks][0] = ld_b32(kr + ks * 16 + 2 * t4, ok);
-        kf[nt][ks][1] = ld_b32(kr + ks * 16 + 8 + 2 * t4, ok);
+      for (int j = 0; j < U; ++j) {
+        const int key = base + j * KPW + kk;
+        kv[j] = make_uint4(0u, 0u, 0u, 0u);
+        if (key < nk) kv[j] = ld_cg16(attn_row(a, false, g, k0 + key) + c * 8);
       }
-    }
-    // V rows (key kb + gr and kb + 8 + gr, dims 8i + 2t4), transposed below
-    uint32_t vr[D / 8][2];
-    {
-      const int k0 = kb + gr, k1 = kb + 8 + gr;
-      const bool ok0 = k0 < a.n_keys, ok1 = k1 < a.n_keys;
-      const bf16* v0 = row_ptr(vh, ok0 ? k0 : kb);
-      const bf16* v1 = row_ptr(vh, ok1 ? k1 : kb);
+      if (a.copy_lo) {  // after every load of the step is in flight
 #pragma unroll
-      for (int i = 0; i < D / 8; ++i) {
-        vr[i][0] = ld_b32(v0 + i * 8 + 2 * t4, ok0);
-        vr[i][1] = ld_b32(v1 + i * 8 + 2 * t4, ok1);
+        for (int j = 0; j < U; ++j) {
+          const int pos = k0 + base + j * KPW + kk;
+          if (base + j * KPW + kk < nk && pos < a.n_lo)
+            *reinterpret_cast<uint4*>(a.hi.k + a.hi.off(g, pos) + c * 8) = kv[j];
+        }
       }
-    }
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      float p[U][R];
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks) {
-      mma_bf16_16816(s[0], qf[ks], kf[0][ks][0], kf[0][ks][1]);
-      mma_bf16_16816(s[1], qf[ks], kf[1][ks][0], kf[1][ks][1]);
-    }
+      for (int j = 0; j < U; ++j)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      const int kp = kb + nt * 8 + 2 * t4;
-      if (kp >= a.n_keys) s[nt][0] = s[nt][2] = -INFINITY;
-      if (kp + 1 >= a.n_keys) s[nt][1] = s[nt][3] = -INFINITY;
-    }
-    float mx[2] = {m_r[0], m_r[1]};
+        for (int r = 0; r < R; ++r) p[j][r] = dot8(kv[j], qv[r]);
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      mx[0] = fmaxf(mx[0], fmaxf(s[nt][0], s[nt][1]));
-      mx[1] = fmaxf(mx[1], fmaxf(s[nt][2], s[nt][3]));
-    }
+      for (int o = LPK / 2; o; o >>= 1)
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-    }
-    float corr[2], msc[2];
+        for (int j = 0; j < U; ++j)
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      corr[r] = mx[r] == -INFINITY ? 1.f : exp2f((m_r[r] - mx[r]) * a.scale_log2);
-      m_r[r] = mx[r];
-      msc[r] = mx[r] == -INFINITY ? 0.f : mx[r] * a.scale_log2;
-    }
-    uint32_t pa[4];
-    float rs[2] = {0.f, 0.f};
+          for (int r = 0; r < R; ++r) p[j][r] += __shfl_xor_sync(0xffffffffu, p[j][r], o);
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      const float p0 = exp2f(s[nt][0] * a.scale_log2 - msc[0]);
-      const float p1 = exp2f(s[nt][1] * a.scale_log2 - msc[0]);
-      const float p2 = exp2f(s[nt][2] * a.scale_log2 - msc[1]);
-      const float p3 = exp2f(s[nt][3] * a.scale_log2 - msc[1]);
-      rs[0] += p0 + p1;
-      rs[1] += p2 + p3;
-      pa[nt * 2 + 0] = pack_bf16x2(p0, p1);
-      pa[nt * 2 + 1] = pack_bf16x2(p2, p3);
-    }
-    l_r[0] = l_r[0] * corr[0] + rs[0];
-    l_r[1] = l_r[1] * corr[1] + rs[1];
+      for (int j = 0; j < U; ++j) {
+        const int key = base + j * KPW + kk;
+        float v = p[j][0];
 #pragma unroll
-    for (int i = 0; i < D / 8; ++i) {
-      acc_o[i][0] *= corr[0];
-      acc_o[i][1] *= corr[0];
-      acc_o[i][2] *= corr[1];
-      acc_o[i][3] *= corr[1];
-      // B of O += P V (k = key, n = dim): transpose the two 8x8 row tiles
-      mma_bf16_16816(acc_o[i], pa, movm_trans(vr[i][0]), movm_trans(vr[i][1]));
-    }
-  }
-
-  // ---- merge the 4 warps (rows < R only): m, l and the unnormalised O
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
-    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
-  }
-  constexpr int RS = D + 2;
-  float* mine = red + warp * R * RS;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const int row = gr + 8 * half;
-    if (row < R) {
-#pragma unroll
-      for (int i = 0; i < D / 8; ++i) {
-        mine[row * RS + 2 + i * 8 + 2 * t4] = acc_o[i][2 * half];
-        mine[row * RS + 2 + i * 8 + 2 * t4 + 1] = acc_o[i][2 * half + 1];
-      }
-      if (t4 == 0) {
-        mine[row * RS] = m_r[half];
-        mine[row * RS + 1] = l_r[half];
+        for (int r = 1; r < R; ++r)
+          if (c == r) v = p[j][r];
+        if (key < nk && c < R) sc[c * sk + key] = v * a.scale_log2;
       }
     }
   }
   __syncthreads();
-  for (int idx = tid; idx < R * D; idx += DEC_THREADS) {
-    const int r = idx / D, d = idx % D, h = g * R + r;
-    float M = -INFINITY;
+  // ---- softmax of each head over the item's keys
+  for (int r = warp; r < R; r += ATT_THREADS / 32) {
+    float m = -INFINITY;
+    for (int i = lane; i < nk; i += 32) m = fmaxf(m, sc[r * sk + i]);
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, red[(w * R + r) * RS]);
-    float o = 0.f, lsum = 0.f;
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.f;
+    for (int i = lane; i < nk; i += 32) {
+      const float e = exp2f(sc[r * sk + i] - m);
+      sc[r * sk + i] = e;
+      l += e;
+    }
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = red[(w * R + r) * RS];
-      const float wt = mw == -INFINITY ? 0.f : exp2f((mw - M) * a.scale_log2);
-      o += wt * red[(w * R + r) * RS + 2 + d];
-      lsum += wt * red[(w * R + r) * RS + 1];
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) {
+      stat[2 * r] = m;
+      stat[2 * r + 1] = l;
     }
-    a.part_o[((long long)h * a.splits + split) * D + d] = o;
-    if (d == 0) {
-      a.part_ml[((long long)h * a.splits + split) * 2] = M * a.scale_log2;  // log2 domain
-      a.part_ml[((long long)h * a.splits + split) * 2 + 1] = lsum;
+  }
+  __syncthreads();
+  // ---- P.V: warp w owns dim chunks [w*CPW, (w+1)*CPW)
+  {
+    const int cw = lane % CPW, st = lane / CPW;
+    const int chunk = warp * CPW + cw;
+    float acc[R][8];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[r][e] = 0.f;
+    for (int i = st; i < nk; i += NS * U2) {
+      uint4 vv[U2];
+#pragma unroll
+      for (int j = 0; j < U2; ++j) {
+        const int key = i + j * NS;
+        vv[j] = make_uint4(0u, 0u, 0u, 0u);
+        if (key < nk) vv[j] = ld_cg16(attn_row(a, true, g, k0 + key) + chunk * 8);
+      }
+      if (a.copy_lo) {
+#pragma unroll
+        for (int j = 0; j < U2; ++j) {
+          const int key = i + j * NS, pos = k0 + key;
+          if (key < nk && pos < a.n_lo) *reinterpret_cast<uint4*>(a.hi.v + a.hi.off(g, pos) + chunk * 8) = vv[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U2; ++j) {
+        const int key = i + j * NS;
+        if (key < nk) {
+          const float2 v0 = unpack_bf16x2(vv[j].x), v1 = unpack_bf16x2(vv[j].y);
+          const float2 v2 = unpack_bf16x2(vv[j].z), v3 = unpack_bf16x2(vv[j].w);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float pr = sc[r * sk + key];
+            acc[r][0] = fmaf(pr, v0.x, acc[r][0]);
+            acc[r][1] = fmaf(pr, v0.y, acc[r][1]);
+            acc[r][2] = fmaf(pr, v1.x, acc[r][2]);
+            acc[r][3] = fmaf(pr, v1.y, acc[r][3]);
+            acc[r][4] = fmaf(pr, v2.x, acc[r][4]);
+            acc[r][5] = fmaf(pr, v2.y, acc[r][5]);
+            acc[r][6] = fmaf(pr, v3.x, acc[r][6]);
+            acc[r][7] = fmaf(pr, v3.y, acc[r][7]);
+          }
+        }
+      }
     }
+#pragma unroll
+    for (int o = CPW; o < 32; o <<= 1)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[r][e] += __shfl_xor_sync(0xffffffffu, acc[r][e], o);
+    if (st == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float4* po = reinterpret_cast<float4*>(a.part_o + ((long long)(g * R + r) * a.splits + s) * D + chunk * 8);
+        __stcg(po, make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
+        __stcg(po + 1, make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]));
+      }
+    }
+  }
+  if (tid < R) {
+    float* ml = a.part_ml + ((long long)(g * R + tid) * a.splits + s) * 2;
+    __stcg(ml, stat[2 * tid]);
+    __stcg(ml + 1, stat[2 * tid + 1]);
   }
   // ---- the last CTA of this kv head merges every split (threadfence reduction)
   __threadfence();
   __syncthreads();
-  if (tid == 0) is_last = (atomicAdd(a.counters + g, 1u) == (unsigned)a.splits - 1);
+  if (tid == 0) *is_last = (atomicAdd(a.counters + g, 1u) == (unsigned)a.splits - 1);
   __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  float* wts = red;  // [R][splits] then den[R]
-  float* den = wts + R * a.splits;
-  for (int r = warp; r < R; r += DEC_THREADS / 32) {
-    const float* ml = a.part_ml + (long long)(g * R + r) * a.splits * 2;
-    float M = -INFINITY;
-    for (int s2 = lane; s2 < a.splits; s2 += 32) M = fmaxf(M, __ldcg(ml + 2 * s2));
+  if (*is_last) {
+    __threadfence();
+    float* wts = sc;  // [R][splits] then den[R]
+    float* den = wts + R * a.splits;
+    for (int r = warp; r < R; r += ATT_THREADS / 32) {
+      const float* ml = a.part_ml + (long long)(g * R + r) * a.splits * 2;
+      float M = -INFINITY;
+      for (int s2 = lane; s2 < a.splits; s2 += 32) M = fmaxf(M, __ldcg(ml + 2 * s2));
 #pragma unroll
-    for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    float dn = 0.f;
-    for (int s2 = lane; s2 < a.splits; s2 += 32) {
-      const float w = exp2f(__ldcg(ml + 2 * s2) - M);
-      wts[r * a.splits + s2] = w;
-      dn += w * __ldcg(ml + 2 * s2 + 1);
+      for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      float dn = 0.f;
+      for (int s2 = lane; s2 < a.splits; s2 += 32) {
+        const float w = exp2f(__ldcg(ml + 2 * s2) - M);
+        wts[r * a.splits + s2] = w;
+        dn += w * __ldcg(ml + 2 * s2 + 1);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
+      if (lane == 0) den[r] = dn;
+    }
+    __syncthreads();
+    // R*D outputs, R*D/128 per thread, each over every split: the loads of
+    // 8 splits x all of a thread's outputs are in flight together
+    constexpr int PER = (R * D + ATT_THREADS - 1) / ATT_THREADS;
+    float num[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) num[q] = 0.f;
+    for (int s0 = 0; s0 < a.splits; s0 += 8) {
+      float v[PER][8];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * ATT_THREADS;
+        const int r = idx / D, dd = idx % D;
+        const float* po = a.part_o + (long long)(g * R + r) * a.splits * D + dd;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[q][u] = (idx < R * D && s0 + u < a.splits) ? __ldcg(po + (long long)(s0 + u) * D) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * ATT_THREADS;
+        const int r = idx < R * D ? idx / D : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < a.splits) num[q] = fmaf(wts[r * a.splits + s0 + u], v[q][u], num[q]);
+      }
     }
 #pragma unroll
-    for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
-    if (lane == 0) den[r] = dn;
+    for (int q = 0; q < PER; ++q) {
+      const int idx = tid + q * ATT_THREADS;
+      if (idx < R * D) {
+        const int r = idx / D, dd = idx % D;
+        a.out[(long long)(g * R + r) * D + dd] = __float2bfloat16_rn(num[q] / den[r]);
+      }
+    }
+    if (tid == 0) a.counters[g] = 0u;
   }
-  __syncthreads();
-  for (int idx = tid; idx < R * D; idx += DEC_THREADS) {
-    const int r = idx / D, dd = idx % D, h = g * R + r;
-    const float* po = a.part_o + (long long)h * a.splits * D + dd;
-    float num = 0.f;
-#pragma unroll 8
-    for (int s2 = 0; s2 < a.splits; ++s2) num = fmaf(wts[r * a.splits + s2], __ldcg(po + (long long)s2 * D), num);
-    a.out[(long long)h * D + dd] = __float2bfloat16_rn(num / den[r]);
-  }
-  if (tid == 0) a.counters[g] = 0u;
+  __syncthreads();  // shared memory reused by the next item
 }
 
-int decode_splits(int n_keys) { return (n_keys + DEC_SPLIT - 1) / DEC_SPLIT; }
+template <int D, int R>
+__global__ void __launch_bounds__(ATT_THREADS) attn_decode_kernel(AttnArgs a) {
+  extern __shared__ __align__(16) float sc[];
+  __shared__ float stat[2 * R];
+  __shared__ unsigned int is_last;
+  // the cache rows (except the anchor's own key, written by the predecessor)
+  // are in HBM already: stream them toward L2, then wait for the predecessor
+  attn_prefetch(a, blockIdx.x, D);
+  pdl_trigger();
+  pdl_wait();
+  attn_item<D, R>(a, blockIdx.x, sc, stat, &is_last);
+}
 
-int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_layer, long long head_stride,
-                            long long page_stride, const int32_t* table, int n_keys, int n_heads, int n_kv_heads,
-                            int head_dim, float* part_o, float* part_ml, unsigned int* counters, bf16* out,
-                            cudaStream_t stream) {
-  const int R = n_heads / n_kv_heads;
-  if (R > DEC_MAX_R || (head_dim != 64 && head_dim != 128)) return DS_ERR_INVALID;
-  const int splits = decode_splits(n_keys);
-  // shared memory: the 4-warp merge [4][R][D+2], reused for the split merge [R][splits] + [R]
-  int smem = 4 * R * (head_dim + 2) * 4;
-  const int merge = (R * splits + R) * 4;
-  if (merge > smem) smem = merge;
-  if (smem > 200 * 1024) return DS_ERR_INVALID;
-  DecArgs a{q, k_layer, v_layer, head_stride, page_stride, table, n_keys, n_heads, n_kv_heads, head_dim, splits,
-            part_o, part_ml, counters, out, (float)(1.4426950408889634 / sqrt((double)head_dim))};
-  count_launch();
-  cudaError_t e;
-  static const bool c0 = prefer_max_smem(decode_attn_kernel<128>) && prefer_max_smem(decode_attn_kernel<64>);
+template <int D, int R>
+static cudaError_t attn_launch_t(const AttnArgs& a, int smem, cudaStream_t stream) {
+  auto kern = attn_decode_kernel<D, R>;
+  static const bool c0 = prefer_max_smem(kern);
   (void)c0;
-  if (head_dim == 128) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(decode_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    e = launch_pdl(decode_attn_kernel<128>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a);
-  } else {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(decode_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    e = launch_pdl(decode_attn_kernel<64>, dim3(n_kv_heads, splits), dim3(DEC_THREADS), smem, stream, a);
+  return launch_pdl(kern, dim3(a.n_kv_heads * a.splits), dim3(ATT_THREADS), smem, stream, a);
+}
+
+int decode_attention_launch(AttnArgs a, int head_dim, cudaStream_t stream) {
+  const int R = a.n_heads / a.n_kv_heads;
+  if ((R != 1 && R != 2 && R != 4 && R != 8) || (head_dim != 64 && head_dim != 128) || a.n_keys < 1)
+    return DS_ERR_INVALID;
+  a.split_keys = attn_split_keys(a.n_keys, a.n_kv_heads, R);
+  a.splits = (a.n_keys + a.split_keys - 1) / a.split_keys;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+  const int smem = attn_smem_bytes(R, a.split_keys, a.splits);
+  count_launch();
+  cudaError_t e = cudaErrorInvalidValue;
+#define DS_ATT_CASE(DD, RR) \
+  if (head_dim == DD && R == RR) e = attn_launch_t<DD, RR>(a, smem, stream);
+  DS_ATT_CASE(128, 1) DS_ATT_CASE(128, 2) DS_ATT_CASE(128, 4) DS_ATT_CASE(128, 8)
+  DS_ATT_CASE(64, 1) DS_ATT_CASE(64, 2) DS_ATT_CASE(64, 4) DS_ATT_CASE(64, 8)
+#undef DS_ATT_CASE
+  return launch_status(e);
+}
+
+// ---------------------------------------------------------------- persistent anchor
+
+// Sense-reversing grid barrier over one CTA per SM.  bar[0] counts arrivals,
+// bar[1] is the generation; `gen` is thread 0's copy of the generation.
+// Spins are bounded: a barrier (or a wait on the other stream) that has not
+// completed within 10 s traps instead of hanging the GPU.
+DS_DEV void spin_check(unsigned long long t0) {
+  if (global_ns() - t0 > 10000000000ull) __trap();
+}
+
+DS_DEV void grid_sync(unsigned int* bar, unsigned int& gen, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int g = gen;
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicExch(bar + 1, g + 1);
+    } else {
+      // back off: the generation word sits in one L2 slice that the other
+      // stream's GEMM / FA traffic also uses
+      const unsigned long long t0 = global_ns();
+      unsigned int it = 0, ns = 32;
+      while (ld_acquire_u32(bar + 1) == g) {
+        if (++it > 8) {
+          __nanosleep(ns);
+          ns = ns < 512 ? 2 * ns : 512;
+        }
+        if ((it & 255u) == 0) spin_check(t0);
+      }
+    }
+    gen = g + 1;
+    __threadfence();
   }
+  __syncthreads();
+}
+
+// CTA 0 records the global time at phase boundaries (ds_anchor_timeline).
+DS_DEV void stamp(const AnchorArgs& a, int rank, int i) {
+  if (rank == 0 && threadIdx.x == 0 && a.stamps) a.stamps[i] = global_ns();
+}
+
+// Thread 0 waits until *counter >= target (the other stream's GEMM epilogues).
+// One CTA polls (rank 0); the others wait for it at the next grid barrier.
+DS_DEV void wait_count(const unsigned int* counter, unsigned int target) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = global_ns();
+    unsigned int it = 0;
+    while (ld_acquire_u32(counter) < target) {
+      __nanosleep(500);
+      if ((++it & 255u) == 0) spin_check(t0);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int D, int R>
+__global__ void __maxnreg__(88) anchor_persistent_kernel(const __grid_constant__ AnchorArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  bf16* xs = reinterpret_cast<bf16*>(smem);
+  float* sc = reinterpret_cast<float*>(smem);
+  __shared__ float red[GEMV_WARPS][GEMV_ROWS];
+  __shared__ float ssq[GEMV_WARPS];
+  __shared__ float stat[2 * R];
+  __shared__ unsigned int is_last;
+  const int tid = threadIdx.x;
+  const int hd = a.n_heads * D, kvd = a.n_kv_heads * D;
+  const bool swiglu = a.mlp_kind == DS_MLP_SWIGLU;
+  const int n_items = a.n_kv_heads * a.splits;
+  // One working CTA per SM: a CTA that finds another of this grid on its SM
+  // (the scheduler packed them onto an idle SM) leaves after the first
+  // barrier, so the SM's resources go back to the other stream's GEMM / FA;
+  // the work is spread over the CTAs that stay (rank / nranks).
+  __shared__ int s_rank;
+  __shared__ unsigned int s_nranks;
+  unsigned int gen = 0;
+  unsigned int smid = 0;
+  if (tid == 0) {
+    gen = ld_acquire_u32(a.bar + 1);
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.bar[2 + blockIdx.x] = smid;  // placement record (ds_anchor_placement)
+    const bool first = atomicAdd(a.claim + (smid & (kAnchorClaimSlots - 1)), 1u) == 0u;
+    s_rank = first ? (int)atomicAdd(a.n_active, 1u) : -1;
+  }
+  grid_sync(a.bar, gen, gridDim.x);
+  const int rank = s_rank;
+  if (rank < 0) return;
+  if (tid == 0) {
+    s_nranks = ld_acquire_u32(a.n_active);
+    a.claim[smid & (kAnchorClaimSlots - 1)] = 0u;  // every claim on this SM happened before the barrier
+  }
+  __syncthreads();
+  const int nranks = (int)s_nranks;
+
+  // seed: h = embed[token] (f32 residual stream of the anchor row)
+  if (rank == 0) {
+    const bf16* e = a.embed + (long long)__ldcg(a.token) * a.d_model;
+    for (int k = tid; k < a.d_model; k += GEMV_THREADS) a.h[k] = __bfloat162float(e[k]);
+  }
+  grid_sync(a.bar, gen, nranks);
+  stamp(a, rank, 0);
+
+  for (int l = 0; l < a.n_layers; ++l) {
+    const AnchorLayer& W = a.layer[l];
+    // ---- q/k/v of the anchor row (+RoPE; its K/V into the consumer cache)
+    {
+      GemvArgs g{};
+      g.W = W.wqkv;
+      g.ldw = a.d_model;
+      g.N = hd + 2 * kvd;
+      g.K = a.d_model;
+      g.x_f32 = a.h;
+      g.gain = W.g_attn;
+      g.mode = EPI_QKV_ROPE;
+      g.n_heads = a.n_heads;
+      g.n_kv_heads = a.n_kv_heads;
+      g.head_dim = D;
+      g.pos = a.pos;
+      g.q_out = a.q;
+      g.kv = W.dst;
+      g.rope_cos = a.rope_cos;
+      g.rope_sin = a.rope_sin;
+      if (rank < g.N / GEMV_ROWS) gemv_prefetch(g, rank);
+      gemv_stage_x(g, xs, ssq);
+      gemv_all_tiles(g, xs, red, rank, nranks);
+    }
+    grid_sync(a.bar, gen, nranks);
+    stamp(a, rank, 1 + 5 * l + 0);
+    // ---- attention over keys 0..pos (a recomputed layer: once its window K/V are in)
+    if (W.wait) {
+      if (rank == 0) wait_count(a.done + l, W.wait);
+      grid_sync(a.bar, gen, nranks);
+    }
+    {
+      AttnArgs t{};
+      t.q = a.q;
+      t.lo = W.src;
+      t.hi = W.dst;
+      t.copy_lo = W.copy;
+      t.n_lo = a.pos;
+      t.n_keys = a.pos + 1;
+      t.n_heads = a.n_heads;
+      t.n_kv_heads = a.n_kv_heads;
+      t.splits = a.splits;
+      t.split_keys = a.split_keys;
+      t.part_o = a.part_o;
+      t.part_ml = a.part_ml;
+      t.counters = a.head_count;
+      t.out = a.o;
+      t.scale_log2 = a.scale_log2;
+      if (rank < n_items) attn_prefetch(t, rank, D);
+      for (int it = rank; it < n_items; it += nranks) {
+        if (it + nranks < n_items) attn_prefetch(t, it + nranks, D);
+        attn_item<D, R>(t, it, sc, stat, &is_last);
+      }
+    }
+    grid_sync(a.bar, gen, nranks);
+    stamp(a, rank, 1 + 5 * l + 1);
+    // ---- o-proj + residual
+    {
+      GemvArgs g{};
+      g.W = W.wo;
+      g.ldw = hd;
+      g.N = a.d_model;
+      g.K = hd;
+      g.x_bf16 = a.o;
+      g.mode = EPI_RESID_F32;
+      g.out_f32 = a.h;
+      g.resid = a.h;
+      if (rank < g.N / GEMV_ROWS) gemv_prefetch(g, rank);
+      gemv_stage_x(g, xs, ssq);
+      gemv_all_tiles(g, xs, red, rank, nranks);
+    }
+    grid_sync(a.bar, gen, nranks);
+    stamp(a, rank, 1 + 5 * l + 2);
+    // ---- MLP up (RMSNorm fused) + SiLU / SwiGLU
+    {
+      GemvArgs g{};
+      g.W = W.w1;
+      g.ldw = a.d_model;
+      g.N = swiglu ? 2 * a.d_ff : a.d_ff;
+      g.K = a.d_model;
+      g.x_f32 = a.h;
+      g.gain = W.g_mlp;
+      g.mode = swiglu ? EPI_SWIGLU_BF16 : EPI_SILU_BF16;
+      g.out_bf16 = a.u;
+      if (rank < g.N / GEMV_ROWS) gemv_prefetch(g, rank);
+      gemv_stage_x(g, xs, ssq);
+      gemv_all_tiles(g, xs, red, rank, nranks);
+    }
+    grid_sync(a.bar, gen, nranks);
+    stamp(a, rank, 1 + 5 * l + 3);
+    // ---- MLP down + residual
+    {
+      GemvArgs g{};
+      g.W = W.w2;
+      g.ldw = a.d_ff;
+      g.N = a.d_model;
+      g.K = a.d_ff;
+      g.x_bf16 = a.u;
+      g.mode = EPI_RESID_F32;
+      g.out_f32 = a.h;
+      g.resid = a.h;
+      if (rank < g.N / GEMV_ROWS) gemv_prefetch(g, rank);
+      gemv_stage_x(g, xs, ssq);
+      gemv_all_tiles(g, xs, red, rank, nranks);
+    }
+    grid_sync(a.bar, gen, nranks);
+    stamp(a, rank, 1 + 5 * l + 4);
+  }
+  // every wait is over: re-arm the counters for the next step
+  if (rank == 0) {
+    for (int i = tid; i < a.n_layers; i += GEMV_THREADS)
+      if (a.layer[i].wait) a.done[i] = 0u;
+    if (tid == 0) *a.n_active = 0u;
+  }
+}
+
+int anchor_persistent_smem(const ds_dims& d, int n_keys) {
+  const int R = d.n_heads / d.n_kv_heads;
+  const int sk = attn_split_keys(n_keys, d.n_kv_heads, R);
+  const int splits = (n_keys + sk - 1) / sk;
+  int kmax = d.d_model > d.d_ff ? d.d_model : d.d_ff;
+  if (d.n_heads * d.head_dim > kmax) kmax = d.n_heads * d.head_dim;
+  const int x = 2 * kmax, att = attn_smem_bytes(R, sk, splits);
+  return x > att ? x : att;
+}
+
+// Largest dynamic shared memory that still lets the kernel share an SM with
+// a tcgen05 GEMM or flash-attention CTA (each ~198.9 KB incl. its reservation).
+constexpr int kAnchorSmemMax = 32 * 1024;
+// Alone on the GPU: more than half an SM's shared memory, so the scheduler
+// cannot pack two CTAs onto one SM (the grid is one CTA per SM).
+constexpr int kAnchorSmemAlone = 120 * 1024;
+
+bool anchor_persistent_fits(const ds_dims& d, int n_keys) {
+  if (d.n_kv_heads < 1) return false;
+  const int R = d.n_heads / d.n_kv_heads;
+  return (R == 1 || R == 2 || R == 4 || R == 8) && (d.head_dim == 64 || d.head_dim == 128) &&
+         d.n_layers <= kMaxLayers && anchor_persistent_smem(d, n_keys) <= kAnchorSmemMax;
+}
+
+template <int D, int R>
+static cudaError_t anchor_launch_t(const AnchorArgs& a, int smem, cudaStream_t stream) {
+  auto kern = anchor_persistent_kernel<D, R>;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAnchorSmemAlone);
+    if (e != cudaSuccess) return e;
+    prefer_max_smem(kern);
+    init = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(num_sms());
+  cfg.blockDim = dim3(GEMV_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // one co-resident CTA per SM (grid barriers)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+int anchor_persistent_launch(AnchorArgs a, cudaStream_t stream, bool co_resident) {
+  const int R = a.n_heads / a.n_kv_heads;
+  const int D = a.head_dim;
+  if ((R != 1 && R != 2 && R != 4 && R != 8) || (D != 64 && D != 128) || a.n_layers > kMaxLayers) return DS_ERR_INVALID;
+  ds_dims d{};
+  d.n_heads = a.n_heads;
+  d.n_kv_heads = a.n_kv_heads;
+  d.head_dim = D;
+  d.d_model = a.d_model;
+  d.d_ff = a.d_ff;
+  int smem = anchor_persistent_smem(d, a.pos + 1);
+  if (smem > kAnchorSmemMax) return DS_ERR_INVALID;
+  if (!co_resident) smem = kAnchorSmemAlone;
+  a.split_keys = attn_split_keys(a.pos + 1, a.n_kv_heads, R);
+  a.splits = (a.pos + 1 + a.split_keys - 1) / a.split_keys;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));
+  count_launch();
+  cudaError_t e = cudaErrorInvalidValue;
+#define DS_ANC_CASE(DD, RR) \
+  if (D == DD && R == RR) e = anchor_launch_t<DD, RR>(a, smem, stream);
+  DS_ANC_CASE(128, 1) DS_ANC_CASE(128, 2) DS_ANC_CASE(128, 4) DS_ANC_CASE(128, 8)
+  DS_ANC_CASE(64, 1) DS_ANC_CASE(64, 2) DS_ANC_CASE(64, 4) DS_ANC_CASE(64, 8)
+#undef DS_ANC_CASE
   return launch_status(e);
 }
 

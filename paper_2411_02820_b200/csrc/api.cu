@@ -51,6 +51,34 @@ int cuda_fail(const char* what) {
     }                                           \
   } while (0)
 
+// Stage timeline (ds_trace_begin / ds_trace_end): a pool of timing events
+// recorded at stage boundaries while tracing is on.
+struct Trace {
+  bool on = false;
+  int n = 0;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int32_t> tag;
+};
+thread_local Trace g_trace;
+
+void trace(cudaStream_t s, int tag) {
+  Trace& t = g_trace;
+  if (!t.on) return;
+  if (t.n == (int)t.ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    t.ev.push_back(e);
+    t.tag.push_back(0);
+  }
+  t.tag[t.n] = tag;
+  cudaEventRecord(t.ev[t.n++], s);
+}
+
+constexpr int kMaxAnchorCtas = 1024;
+// persistent anchor control block (zeroed per step): done[kMaxLayers] | bar[2] |
+// smid[kMaxAnchorCtas] | claim[kAnchorClaimSlots] | n_active[1]
+constexpr int kAnchorCtlWords = kMaxLayers + 2 + kMaxAnchorCtas + kAnchorClaimSlots + 1;
+
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Workspace {
@@ -76,6 +104,8 @@ struct Workspace {
   bf16* k0;           // [KVH][n][D] receiver's exact layer-0 K of the window
   bf16* v0;
   unsigned int* dec_count;  // [n_kv_heads] split-merge counters (zero between launches)
+  unsigned int* an_ctl;     // persistent anchor control block: done[kMaxLayers], bar[2], smid[kMaxAnchorCtas]
+  unsigned long long* an_stamps;  // persistent anchor phase times (ds_anchor_timeline)
   size_t bytes;
 };
 
@@ -89,7 +119,7 @@ Workspace carve(const ds_dims& m, int n, void* base) {
     return r;
   };
   const size_t hd = (size_t)m.n_heads * m.head_dim;
-  const int splits = decode_splits(n);
+  const int splits = attn_max_splits(n, m.n_kv_heads, m.n_heads / (m.n_kv_heads > 0 ? m.n_kv_heads : 1));
   w.tokens = reinterpret_cast<int64_t*>(take(8ull * n));
   w.h = reinterpret_cast<float*>(take(4ull * n * m.d_model));
   w.a = reinterpret_cast<bf16*>(take(2ull * n * m.d_model));
@@ -112,6 +142,8 @@ Workspace carve(const ds_dims& m, int n, void* base) {
   w.k0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
   w.v0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
   w.dec_count = reinterpret_cast<unsigned int*>(take(4ull * m.n_kv_heads));
+  w.an_ctl = reinterpret_cast<unsigned int*>(take(4ull * kAnchorCtlWords));
+  w.an_stamps = reinterpret_cast<unsigned long long*>(take(8ull * (1 + 5 * kMaxLayers)));
   w.bytes = off;
   return w;
 }
@@ -164,6 +196,9 @@ struct Ctx {
   const ds_kv_cache* kv;
   cudaStream_t s;
   cudaEvent_t* layer_ready = nullptr;  // recorded once layer l's window K/V are in the cache
+  unsigned int* qkv_done = nullptr;    // per layer: QKV GEMM epilogue arrivals (persistent anchor waits)
+  float* const* e_export = nullptr;    // [L] producer export: E (the window's f32 residual input) per layer
+  cudaEvent_t after_seed = nullptr;    // recorded after the first group's seed kernel
 };
 
 // (a = RMSNorm(h) already in the workspace) QKV (+RoPE, K/V into the cache) -> [attention -> o-proj+resid -> RMSNorm -> W1+SiLU -> W2+resid]
@@ -188,8 +223,10 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos =
   e.pos_rows = row_pos;  // token-selective rows sit at scattered positions
   e.rope_cos = c.m->rope_cos;
   e.rope_sin = c.m->rope_sin;
+  if (c.qkv_done) e.done = c.qkv_done + l;
   const bf16* wqkv = static_cast<const bf16*>(W.wqkv) + (kv_only ? (long long)hd * d.d_model : 0);
   DS_TRY(gemm_launch(c.w.a, d.d_model, wqkv, d.d_model, d.d_model, e, c.s), "qkv gemm");
+  trace(c.s, DS_TRACE_QKV + l);
   if (c.layer_ready && cudaEventRecord(c.layer_ready[l], c.s) != cudaSuccess) return cuda_fail("event record");
   if (kv_only) return DS_OK;
   const KvAddr ka = layer_addr(*c.kv, l, d.head_dim);
@@ -217,6 +254,7 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos =
   f.ld_out = d.d_ff;
   DS_TRY(gemm_launch(c.w.a, d.d_model, W.w1, d.d_model, d.d_model, f, c.s), "w1 gemm");
   DS_TRY(gemm_launch(c.w.u, d.d_ff, W.w2, d.d_ff, d.d_ff, r, c.s), "w2 gemm");
+  trace(c.s, DS_TRACE_LAYER + l);
   return DS_OK;
 }
 
@@ -243,9 +281,19 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a) {
   g.rope_sin = c.m->rope_sin;
   DS_TRY(gemv_launch(g, c.s), "anchor qkv");
   const KvAddr ka = g.kv;
-  DS_TRY(decode_attention_launch(c.w.q_a, ka.k, ka.v, ka.head_stride, ka.page_stride, ka.table, pos + 1,
-                                 d.n_heads, d.n_kv_heads, d.head_dim, c.w.part_o, c.w.part_ml, c.w.dec_count, c.w.o_a,
-                                 c.s),
+  AttnArgs at{};
+  at.q = c.w.q_a;
+  at.lo = ka;
+  at.hi = ka;
+  at.n_lo = pos;
+  at.n_keys = pos + 1;
+  at.n_heads = d.n_heads;
+  at.n_kv_heads = d.n_kv_heads;
+  at.part_o = c.w.part_o;
+  at.part_ml = c.w.part_ml;
+  at.counters = c.w.dec_count;
+  at.out = c.w.o_a;
+  DS_TRY(decode_attention_launch(at, d.head_dim, c.s),
          "anchor attention");
   GemvArgs o{};
   o.W = static_cast<const bf16*>(W.wo);
@@ -304,15 +352,30 @@ int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token, int64_t* to
 int recompute_group(Ctx& c, const int64_t* tok, int P, int a, int b, const void* seed) {
   const ds_dims& d = c.d;
   const ds_layer_weights& Wa = c.m->layers[a];
+  // E at layer l = the window's f32 residual-stream input of layer l (model.py:620-621),
+  // exported exactly (a = 0: the token embeddings, model.py:609)
+  auto export_e = [&](int l) -> int {
+    if (!c.e_export || !c.e_export[l]) return DS_OK;
+    if (cudaMemcpyAsync(c.e_export[l], c.w.h, 4ull * P * d.d_model, cudaMemcpyDeviceToDevice, c.s) != cudaSuccess)
+      return cuda_fail("e export");
+    return DS_OK;
+  };
   if (a == 0)
     DS_TRY(rmsnorm_launch(c.m->embed, true, tok, P, d.d_model, Wa.g_attn, c.w.a, c.w.h, nullptr, P, c.s), "seed");
   else
-    DS_TRY(rmsnorm_launch(seed, true, nullptr, P, d.d_model, Wa.g_attn, c.w.a, c.w.h, nullptr, P, c.s), "seed");
+    DS_TRY(rmsnorm_launch(seed, false, nullptr, P, d.d_model, Wa.g_attn, c.w.a, c.w.h, nullptr, P, c.s), "seed");
+  if (int rc = export_e(a)) return rc;
+  if (c.after_seed) {
+    if (cudaEventRecord(c.after_seed, c.s) != cudaSuccess) return cuda_fail("event record");
+    c.after_seed = nullptr;
+  }
   for (int l = a; l <= b; ++l) {
-    if (l > a)
+    if (l > a) {
       DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, P, d.d_model, c.m->layers[l].g_attn, c.w.a, nullptr, nullptr, 0,
                             c.s),
              "rmsnorm");
+      if (int rc = export_e(l)) return rc;
+    }
     int rc = window_layer(c, l, P, l == b);
     if (rc) return rc;
   }
@@ -326,22 +389,100 @@ int reset_counters(Ctx& c) {
   return DS_OK;
 }
 
-// wait_for (optional): per layer, an event the anchor's layer l must wait for
-// (the recompute of l on another stream); NULL entries need no wait.
-// token_id: device pointer to the row's token id; P: its position.
-int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* token,
-                const cudaEvent_t* wait_for = nullptr, int64_t* token64 = nullptr) {
+// How the anchor pass reads each layer.  Default (no plan): every layer from
+// the consumer cache, no waits.
+struct AnchorPlan {
+  const ds_kv_cache* sender = nullptr;  // reused layers are read from here (and copied into the cache)
+  const char* reused = nullptr;         // [L] 1 = reused layer
+  unsigned int wait[kMaxLayers] = {};   // persistent path: QKV GEMM arrivals to wait for per layer
+  const cudaEvent_t* wait_for = nullptr;  // per-launch path: per-layer events to wait for
+  bool ctl_zeroed = false;              // the caller zeroed the control block in stream order
+  bool co_resident = false;             // runs beside the recompute (small footprint); else one CTA per SM forced
+};
+
+// The whole anchor pass as one persistent kernel (anchor.cu).
+int anchor_persistent(Ctx& c, const int64_t* token_id, int P, const AnchorPlan* plan) {
   const ds_dims& d = c.d;
-  if (int rc = reset_counters(c)) return rc;
-  DS_TRY(rmsnorm_launch(c.m->embed, true, token_id, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr,
-                        1, c.s),
-         "anchor seed");
+  static thread_local AnchorArgs A;  // ~20 KB of kernel parameters
+  memset(&A, 0, sizeof(A));
   for (int l = 0; l < d.n_layers; ++l) {
-    if (wait_for && wait_for[l] && cudaStreamWaitEvent(c.s, wait_for[l], 0) != cudaSuccess) return cuda_fail("wait");
-    int rc = anchor_layer(c, l, P, c.w.h_a);
-    if (rc) return rc;
+    const ds_layer_weights& W = c.m->layers[l];
+    AnchorLayer& al = A.layer[l];
+    al.wqkv = static_cast<const bf16*>(W.wqkv);
+    al.wo = static_cast<const bf16*>(W.wo);
+    al.w1 = static_cast<const bf16*>(W.w1);
+    al.w2 = static_cast<const bf16*>(W.w2);
+    al.g_attn = W.g_attn;
+    al.g_mlp = W.g_mlp;
+    al.dst = layer_addr(*c.kv, l, d.head_dim);
+    const bool from_sender = plan && plan->sender && plan->reused && plan->reused[l];
+    al.src = from_sender ? layer_addr(*plan->sender, l, d.head_dim) : al.dst;
+    al.copy = from_sender ? 1 : 0;
+    al.wait = plan ? plan->wait[l] : 0u;
   }
-  return lm_head(c, c.w.h_a, logits, token, token64);
+  A.n_layers = d.n_layers;
+  A.d_model = d.d_model;
+  A.n_heads = d.n_heads;
+  A.n_kv_heads = d.n_kv_heads;
+  A.head_dim = d.head_dim;
+  A.d_ff = d.d_ff;
+  A.mlp_kind = d.mlp_kind;
+  A.pos = P;
+  A.token = token_id;
+  A.embed = static_cast<const bf16*>(c.m->embed);
+  A.rope_cos = c.m->rope_cos;
+  A.rope_sin = c.m->rope_sin;
+  A.h = c.w.h_a;
+  A.q = c.w.q_a;
+  A.o = c.w.o_a;
+  A.u = c.w.u_a;
+  A.part_o = c.w.part_o;
+  A.part_ml = c.w.part_ml;
+  A.head_count = c.w.dec_count;
+  A.done = c.w.an_ctl;
+  A.bar = c.w.an_ctl + kMaxLayers;
+  A.stamps = c.w.an_stamps;
+  A.claim = c.w.an_ctl + kMaxLayers + 2 + kMaxAnchorCtas;
+  A.n_active = A.claim + kAnchorClaimSlots;
+  return anchor_persistent_launch(A, c.s, plan && plan->co_resident);
+}
+
+int zero_anchor_ctl(Ctx& c, cudaStream_t s) {
+  if (cudaMemsetAsync(c.w.an_ctl, 0, 4ull * kAnchorCtlWords, s) != cudaSuccess ||
+      cudaMemsetAsync(c.w.dec_count, 0, 4ull * c.d.n_kv_heads, s) != cudaSuccess)
+    return cuda_fail("memset");
+  return DS_OK;
+}
+
+// token_id: device pointer to the row's token id; P: its position.  The
+// persistent kernel runs the whole pass when the shape fits its co-resident
+// budget; otherwise one launch per kernel (same device functions, same
+// results), waiting on plan->wait_for events.
+int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* token,
+                const AnchorPlan* plan = nullptr, int64_t* token64 = nullptr) {
+  const ds_dims& d = c.d;
+  if (anchor_persistent_fits(d, P + 1)) {
+    if (!(plan && plan->ctl_zeroed))
+      if (int rc = zero_anchor_ctl(c, c.s)) return rc;
+    DS_TRY(anchor_persistent(c, token_id, P, plan), "anchor");
+    trace(c.s, DS_TRACE_ANCHOR + d.n_layers - 1);
+  } else {
+    if (plan && plan->sender) return fail(DS_ERR_INVALID, "anchor: sender reads need the persistent kernel");
+    if (int rc = reset_counters(c)) return rc;
+    DS_TRY(rmsnorm_launch(c.m->embed, true, token_id, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr,
+                          1, c.s),
+           "anchor seed");
+    for (int l = 0; l < d.n_layers; ++l) {
+      if (plan && plan->wait_for && plan->wait_for[l] && cudaStreamWaitEvent(c.s, plan->wait_for[l], 0) != cudaSuccess)
+        return cuda_fail("wait");
+      int rc = anchor_layer(c, l, P, c.w.h_a);
+      if (rc) return rc;
+      trace(c.s, DS_TRACE_ANCHOR + l);
+    }
+  }
+  int rc = lm_head(c, c.w.h_a, logits, token, token64);
+  trace(c.s, DS_TRACE_LOGITS);
+  return rc;
 }
 
 const int64_t* stage_tokens(const int64_t* host, const int64_t* dev, int n, Workspace& w, cudaStream_t s) {
@@ -358,11 +499,157 @@ int check_cache(const ds_kv_cache* c, const ds_dims& d, int n, const char* what)
   return DS_OK;
 }
 
+// The prefill after validation, shared by ds_partial_prefill and
+// ds_full_prefill (= every layer recomputed, no sender: the reference's
+// full_prefill is _mixed_prefill over the same window + anchor structure,
+// model.py:641-649, so recompute-all is the full prefill bit for bit).
+int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n_groups,
+                 const std::vector<const ds_e_cache*>& seed, const ds_kv_cache* sender_kv,
+                 const std::vector<int32_t>& reused, const std::vector<char>& covered, float* logits_out,
+                 int32_t* token_out, cudaStream_t xs) {
+  const ds_model* m = c.m;
+  const ds_dims& d = c.d;
+  Workspace& w = c.w;
+  const ds_kv_cache* out_kv = c.kv;
+  const cudaStream_t cs = c.s;
+  const int L = d.n_layers, P = n - 1;
+  int rc;
+
+  // Persistent anchor (the usual case): it reads the reused layers straight
+  // from the sender's export and stores them into the consumer cache as it
+  // goes (the KV ingest fused into the anchor's read of the same bytes).
+  const bool fused = anchor_persistent_fits(d, n);
+  std::vector<char> reused_flag(L, 0);
+  for (int l : reused) reused_flag[l] = 1;
+  AnchorPlan plan;
+  if (fused && !reused.empty()) {
+    plan.sender = sender_kv;
+    plan.reused = reused_flag.data();
+  }
+
+  if (xs == cs) {
+    // single stream: (ingest,) recompute, then the anchor after all KV has landed (sched.py:256)
+    if (!fused && !reused.empty()) {
+      DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P,
+                              cs),
+             "kv ingest");
+      trace(cs, DS_TRACE_INGEST);
+    }
+    for (int i = 0; i < n_groups; ++i) {
+      rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
+      if (rc) return rc;
+    }
+    return anchor_pass(c, tok + P, P, logits_out, token_out, &plan);
+  }
+
+  // Two streams.  Compute stream: the recompute groups.  Copy stream: the
+  // anchor pass.  The anchor's layer l needs only layer l's window K/V
+  // (model.py:559) and its own layer l-1 output, so for a recomputed layer it
+  // waits for that layer's QKV GEMM and nothing else: the HBM-bound anchor
+  // streams weights while the tensor-bound recompute runs.  Persistent path:
+  // the wait is on the GEMM epilogue's arrival counter (one kernel, no events);
+  // per-launch path: on an event after the QKV GEMM, with the ingest first.
+  // Same kernels, same results as the single-stream order.  Events are created
+  // once per host thread (capturable into CUDA graphs).
+  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_seed = nullptr;
+  thread_local cudaEvent_t ev_layer[kMaxLayers] = {};
+  if (!ev_fork) {
+    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_seed, cudaEventDisableTiming) != cudaSuccess)
+      return cuda_fail("event");
+    for (int l = 0; l < kMaxLayers; ++l)
+      if (cudaEventCreateWithFlags(&ev_layer[l], cudaEventDisableTiming) != cudaSuccess) return cuda_fail("event");
+  }
+  cudaEvent_t wait_for[kMaxLayers] = {};
+  if (fused) {
+    // counters zeroed in stream order before either stream can touch them
+    if (int rc2 = zero_anchor_ctl(c, cs)) return rc2;
+    plan.ctl_zeroed = true;
+    const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
+    for (int i = 0; i < n_groups; ++i)
+      for (int l = groups[2 * i]; l <= groups[2 * i + 1]; ++l)
+        plan.wait[l] = gemm_done_target(P, l == groups[2 * i + 1] ? 2 * kvd : hd + 2 * kvd);
+    c.qkv_done = w.an_ctl;
+    // The anchor launches once the first QKV GEMM's CTAs (PDL-launched while
+    // the seed kernel drains) hold every SM: its CTAs then land one per SM,
+    // beside them, instead of packing onto idle SMs.
+    if (n_groups > 0) c.after_seed = ev_seed;
+  } else {
+    for (int l = 0; l < L; ++l) wait_for[l] = covered[l] ? ev_layer[l] : nullptr;
+    plan.wait_for = wait_for;
+    c.layer_ready = ev_layer;
+  }
+  cudaEventRecord(ev_fork, cs);
+  cudaStreamWaitEvent(xs, ev_fork, 0);
+  if (!fused && !reused.empty()) {
+    DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P, xs,
+                            /*background=*/true),
+           "kv ingest");
+    trace(xs, DS_TRACE_INGEST);
+  }
+  Ctx cx{m, d, w, out_kv, xs};
+  // enqueue the recompute (which records ev_layer[l]) before the anchor's waits:
+  // a cudaStreamWaitEvent binds to the latest record at enqueue time
+  for (int i = 0; i < n_groups; ++i) {
+    rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
+    if (rc) return rc;
+  }
+  if (fused && n_groups > 0) cudaStreamWaitEvent(xs, ev_seed, 0);
+  plan.co_resident = fused && n_groups > 0;
+  rc = anchor_pass(cx, tok + P, P, logits_out, token_out, &plan);
+  if (rc) return rc;
+  cudaEventRecord(ev_join, xs);
+  cudaStreamWaitEvent(cs, ev_join, 0);
+  return DS_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int ds_abi_version(void) { return DS_ABI_VERSION; }
+int ds_anchor_placement(const ds_dims* dims, int32_t n_tokens, const void* workspace, int32_t* sm_out, int32_t cap) {
+  g_err.clear();
+  if (!dims || !workspace || !sm_out || n_tokens < 1) return fail(DS_ERR_INVALID, "bad placement arguments");
+  Workspace w = carve(*dims, n_tokens, const_cast<void*>(workspace));
+  const int n = num_sms() < cap ? num_sms() : cap;
+  if (cudaMemcpy(sm_out, w.an_ctl + kMaxLayers + 2, 4ull * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return cuda_fail("placement copy");
+  return n;
+}
+
+int ds_anchor_timeline(const ds_dims* dims, int32_t n_tokens, const void* workspace, uint64_t* ns_out, int32_t cap) {
+  g_err.clear();
+  if (!dims || !workspace || !ns_out || n_tokens < 1) return fail(DS_ERR_INVALID, "bad timeline arguments");
+  Workspace w = carve(*dims, n_tokens, const_cast<void*>(workspace));
+  int n = 1 + 5 * dims->n_layers;
+  if (n > cap) n = cap;
+  if (cudaMemcpy(ns_out, w.an_stamps, 8ull * n, cudaMemcpyDeviceToHost) != cudaSuccess) return cuda_fail("timeline copy");
+  return n;
+}
+
+int ds_trace_begin(void) {
+  g_trace.on = true;
+  g_trace.n = 0;
+  return DS_OK;
+}
+
+int ds_trace_end(float* ms_out, int32_t* tag_out, int32_t cap) {
+  Trace& t = g_trace;
+  t.on = false;
+  if (t.n == 0) return 0;
+  for (int i = 0; i < t.n; ++i)
+    if (cudaEventSynchronize(t.ev[i]) != cudaSuccess) return cuda_fail("trace sync"), -1;
+  for (int i = 0; i < t.n && i < cap; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, t.ev[0], t.ev[i]) != cudaSuccess) return cuda_fail("trace elapsed"), -1;
+    if (ms_out) ms_out[i] = ms;
+    if (tag_out) tag_out[i] = t.tag[i];
+  }
+  return t.n;
+}
+
 unsigned long long ds_launch_count(void) { return __atomic_load_n(&ds::g_launches, __ATOMIC_RELAXED); }
 const char* ds_last_error(void) { return g_err.c_str(); }
 
@@ -653,57 +940,8 @@ int ds_partial_prefill(const ds_model* m, const int64_t* tokens_host, const int6
   const int64_t* tok = stage_tokens(tokens_host, tokens_dev, n, w, cs);
   if (!tok) return cuda_fail("token upload");
   Ctx c{m, d, w, out_kv, cs};
-
-  if (xs == cs) {
-    // single stream: ingest, recompute, then the anchor after all KV has landed (sched.py:256)
-    if (!reused.empty())
-      DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P,
-                              cs),
-             "kv ingest");
-    for (int i = 0; i < n_groups; ++i) {
-      rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
-      if (rc) return rc;
-    }
-    return anchor_pass(c, tok + P, P, logits_out, token_out);
-  }
-
-  // Two streams.  Copy stream: KV ingest, then the anchor pass layer by layer;
-  // compute stream: the recompute groups.  The anchor's layer l needs only
-  // layer l's window K/V (model.py:559) and its own layer l-1 output, so it
-  // waits for the recompute of l (an event after l's QKV GEMM) and nothing
-  // else: the HBM-bound anchor streams weights while the tensor-bound
-  // recompute runs.  Same kernels, same results as the single-stream order.
-  // Events are created once per host thread (capturable into CUDA graphs).
-  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  thread_local cudaEvent_t ev_layer[kMaxLayers] = {};
-  if (!ev_fork) {
-    if (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
-      return cuda_fail("event");
-    for (int l = 0; l < kMaxLayers; ++l)
-      if (cudaEventCreateWithFlags(&ev_layer[l], cudaEventDisableTiming) != cudaSuccess) return cuda_fail("event");
-  }
-  cudaEvent_t wait_for[kMaxLayers] = {};
-  for (int l = 0; l < L; ++l) wait_for[l] = covered[l] ? ev_layer[l] : nullptr;
-  cudaEventRecord(ev_fork, cs);
-  cudaStreamWaitEvent(xs, ev_fork, 0);
-  if (!reused.empty())
-    DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P, xs,
-                            /*background=*/true),
-           "kv ingest");
-  c.layer_ready = ev_layer;
-  Ctx cx{m, d, w, out_kv, xs};
-  // enqueue the recompute (which records ev_layer[l]) before the anchor's waits:
-  // a cudaStreamWaitEvent binds to the latest record at enqueue time
-  for (int i = 0; i < n_groups; ++i) {
-    rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
-    if (rc) return rc;
-  }
-  rc = anchor_pass(cx, tok + P, P, logits_out, token_out, wait_for);
-  if (rc) return rc;
-  cudaEventRecord(ev_join, xs);
-  cudaStreamWaitEvent(cs, ev_join, 0);
-  return DS_OK;
+  trace(cs, 0);
+  return prefill_core(c, tok, n, groups, n_groups, seed, sender_kv, reused, covered, logits_out, token_out, xs);
 }
 
 int ds_recompute_group(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, int32_t a, int32_t b,
@@ -748,7 +986,8 @@ int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tokens, co
 
 int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev, int32_t n_tokens,
                     const ds_kv_cache* out_kv, const int32_t* e_layers, int32_t n_e, void* const* e_out,
-                    float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream) {
+                    float* logits_out, int32_t* token_out, void* workspace, size_t workspace_bytes, void* stream,
+                    void* copy_stream) {
   g_err.clear();
   if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
   const ds_dims& d = m->dims;
@@ -757,12 +996,12 @@ int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t
   if ((rc = check_tokens(d, tokens_host, n_tokens))) return rc;
   if ((rc = check_cache(out_kv, d, n_tokens, "output"))) return rc;
   if (!logits_out) return fail(DS_ERR_INVALID, "logits_out is NULL");
-  const int L = d.n_layers, n = n_tokens, P = n - 1;
-  std::vector<bf16*> e_at(L, nullptr);
+  const int L = d.n_layers, n = n_tokens;
+  std::vector<float*> e_at(L, nullptr);
   for (int i = 0; i < n_e; ++i) {
     const int l = e_layers[i];
     if (l < 0 || l >= L || !e_out || !e_out[i]) return fail(DS_ERR_INVALID, "bad e export layer %d", l);
-    e_at[l] = static_cast<bf16*>(e_out[i]);
+    e_at[l] = static_cast<float*>(e_out[i]);
   }
   Workspace w = carve(d, n, workspace);
   if (!workspace || workspace_bytes < w.bytes)
@@ -771,26 +1010,14 @@ int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t
   const int64_t* tok = stage_tokens(tokens_host, tokens_dev, n, w, s);
   if (!tok) return cuda_fail("token upload");
   Ctx c{m, d, w, out_kv, s};
-  // All n rows run batched through layers 0..L-2 (the anchor row is just row P
-  // of the causal prefill); at the last layer only the window's K/V are live,
-  // so rows 0..P-1 project K/V and row P finishes through the anchor path.
-  // E at layer 0 = the token embeddings over the window (model.py:609, 620-621)
-  DS_TRY(rmsnorm_launch(m->embed, true, tok, n, d.d_model, m->layers[0].g_attn, w.a, w.h, e_at[0], P, s), "seed");
-  for (int l = 0; l < L; ++l) {
-    const bool last = l == L - 1;
-    if (l > 0)
-      DS_TRY(rmsnorm_launch(w.h, false, nullptr, n, d.d_model, m->layers[l].g_attn, w.a, nullptr, e_at[l], P, s),
-             "rmsnorm");
-    if (!last) {
-      rc = window_layer(c, l, n, false);
-    } else {
-      rc = window_layer(c, l, P, true);
-      if (!rc) rc = reset_counters(c);
-      if (!rc) rc = anchor_layer(c, l, P, w.h + (long long)P * d.d_model);
-    }
-    if (rc) return rc;
-  }
-  return lm_head(c, w.h + (long long)P * d.d_model, logits_out, token_out);
+  c.e_export = e_at.data();
+  trace(s, 0);
+  const int32_t all[2] = {0, L - 1};
+  std::vector<const ds_e_cache*> seed(1, nullptr);
+  std::vector<int32_t> reused;
+  std::vector<char> covered(L, 1);
+  return prefill_core(c, tok, n, all, 1, seed, nullptr, reused, covered, logits_out, token_out,
+                      copy_stream ? (cudaStream_t)copy_stream : s);
 }
 
 }  // extern "C"

@@ -55,8 +55,10 @@ struct FaTcArgs {
   float scale_log2;
 };
 
+// At most 136 registers per thread: 3 FA warps of an SM sub-partition then
+// leave room for one 88-register warp of the persistent anchor (anchor.cu).
 template <int D>
-__global__ void __launch_bounds__(FA_THREADS, 1)
+__global__ void __maxnreg__(136)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
   using L = FaTcSmem<D>;
@@ -235,15 +237,20 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     for (int j = 0; j < n_kv[i]; ++j) {
       mbar_wait(&s_full[i], j & 1);
       tc_fence_after();
-      uint32_t sr[FA_BN];
-#pragma unroll
-      for (int c = 0; c < FA_BN / 32; ++c) tmem_ld32_nowait(tS + c * 32, sr + c * 32);
-      tmem_wait_ld();
+      // The row in two 64-column halves (at most 136 registers per thread, so
+      // an anchor warp of the other stream fits beside the 3 FA warps of an SM
+      // sub-partition): pass 1 takes the masked row max, upper half first so
+      // the lower half stays in registers for pass 2.
       const int kbase = j * FA_BN;
-      if (kbase + FA_BN - 1 > tile_pos0) {
+      const bool maskit = kbase + FA_BN - 1 > tile_pos0;
+      uint32_t sr[FA_BN / 2];
+      tmem_ld32_nowait(tS + 64, sr);
+      tmem_ld32_nowait(tS + 96, sr + 32);
+      tmem_wait_ld();
+      if (maskit) {
 #pragma unroll
-        for (int c = 0; c < FA_BN; ++c)
-          if (kbase + c > qpos) sr[c] = __float_as_uint(-INFINITY);
+        for (int c = 0; c < FA_BN / 2; ++c)
+          if (kbase + FA_BN / 2 + c > qpos) sr[c] = __float_as_uint(-INFINITY);
       }
       // row max as 8 independent chains (a single 128-long fmax chain is
       // ~4 cycles per link on the softmax critical path)
@@ -251,7 +258,17 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
       for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(sr[q]);
 #pragma unroll
-      for (int c = 8; c < FA_BN; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+      for (int c = 8; c < FA_BN / 2; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+      tmem_ld32_nowait(tS, sr);
+      tmem_ld32_nowait(tS + 32, sr + 32);
+      tmem_wait_ld();
+      if (maskit) {
+#pragma unroll
+        for (int c = 0; c < FA_BN / 2; ++c)
+          if (kbase + c > qpos) sr[c] = __float_as_uint(-INFINITY);
+      }
+#pragma unroll
+      for (int c = 0; c < FA_BN / 2; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
       const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const bool need = mt > m_used + thr;
@@ -277,17 +294,34 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       }
       const float msc = m_used * sc;
       float sum4[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
-      uint32_t pk[FA_BN / 2];
+      uint32_t pk[FA_BN / 4];
+      // pass 2: lower half from registers -> P columns [0, 32) (over consumed S)
 #pragma unroll
-      for (int c = 0; c < FA_BN / 2; ++c) {
+      for (int c = 0; c < FA_BN / 4; ++c) {
+        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * c]), sc, -msc));
+        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc));
+        sum4[c & 3] += p0 + p1;
+        pk[c] = pack_bf16x2(p0, p1);
+      }
+      tmem_st32_nowait(tS, pk);
+      // upper half re-read -> P columns [32, 64) (S columns 32..63 are consumed)
+      tmem_ld32_nowait(tS + 64, sr);
+      tmem_ld32_nowait(tS + 96, sr + 32);
+      tmem_wait_ld();
+      if (maskit) {
+#pragma unroll
+        for (int c = 0; c < FA_BN / 2; ++c)
+          if (kbase + FA_BN / 2 + c > qpos) sr[c] = __float_as_uint(-INFINITY);
+      }
+#pragma unroll
+      for (int c = 0; c < FA_BN / 4; ++c) {
         const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * c]), sc, -msc));
         const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc));
         sum4[c & 3] += p0 + p1;
         pk[c] = pack_bf16x2(p0, p1);
       }
       l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
-      tmem_st32_nowait(tS, pk);
-      tmem_st32_nowait(tS + 32, pk + 32);
+      tmem_st32_nowait(tS + 32, pk);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();

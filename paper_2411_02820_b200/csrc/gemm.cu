@@ -301,8 +301,14 @@ __global__ void __maxnreg__(128)
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       epilogue_tile<BN>(epi, tbase, mb * GEMM_BM + quarter * 32 + lane, nb);
       tc_fence_before();
+      if (epi.done) __threadfence();  // this warp's stores, before its completion count (release)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        mbar_arrive(&tempty[acc]);
+        // a consumer on another stream (the persistent anchor) waits for
+        // 4 * tiles arrivals before it reads this layer's K/V
+        if (epi.done) atomicAdd(epi.done, 1u);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -378,10 +384,18 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
   return launch_pdl(kern, dim3(grid), dim3(GEMM_THREADS), L::TOTAL, stream, ta, tb, K, epi);
 }
 
+int gemm_bn(int N) { return N >= 1024 ? 256 : 128; }
+
+// Arrivals on GemmEpi::done once the GEMM has finished: 4 epilogue warps per tile.
+unsigned int gemm_done_target(int M, int N) {
+  const int bn = gemm_bn(N);
+  return 4u * (unsigned)(((M + GEMM_BM - 1) / GEMM_BM) * ((N + bn - 1) / bn));
+}
+
 // A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks BN from N.
 int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
                 cudaStream_t stream, int force_bn, int max_ctas) {
-  int bn = force_bn ? force_bn : (epi.N >= 1024 ? 256 : 128);
+  int bn = force_bn ? force_bn : gemm_bn(epi.N);
   GemmEpi e2 = epi;
   e2.group = 16;  // measured best of 8 / 16 / 64 for the recompute shapes
   CUtensorMap ta, tb;

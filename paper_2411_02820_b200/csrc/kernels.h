@@ -32,6 +32,7 @@ struct GemmEpi {
   int group;            // raster: m-blocks per group (set by gemm_launch)
   const float* rope_cos;  // [max_seq][head_dim/2]
   const float* rope_sin;
+  unsigned int* done;   // optional: +1 per (tile, epilogue warp) once its stores are visible
 };
 
 // Base of layer `layer`'s K (v = false) or V block in a cache descriptor:
@@ -91,6 +92,7 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, long long rows, long long 
 int num_sms();
 int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
                 cudaStream_t stream, int force_bn = 0, int max_ctas = 0);
+unsigned int gemm_done_target(int M, int N);
 
 int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
                      int n_kv_heads, int head_dim, int window, cudaStream_t stream, bool background = false);
@@ -135,10 +137,68 @@ struct GemvArgs {
 int gemv_launch(const GemvArgs& a, cudaStream_t stream);
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream);
 int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaStream_t stream);
-int decode_splits(int n_keys);
-int decode_attention_launch(const bf16* q, const bf16* k_layer, const bf16* v_layer, long long head_stride,
-                            long long page_stride, const int32_t* table, int n_keys, int n_heads, int n_kv_heads,
-                            int head_dim, float* part_o, float* part_ml, unsigned int* counters, bf16* out,
-                            cudaStream_t stream);
+
+// Split-KV attention of one query row (the anchor / a decode step) over a
+// cache layer; see anchor.cu.  Keys < n_lo are read from `lo`, the rest from
+// `hi`; copy_lo also stores every lo row into hi (fused KV ingest).
+struct AttnArgs {
+  const bf16* q;  // [H*D], RoPE applied
+  KvAddr lo, hi;
+  int copy_lo;
+  int n_lo, n_keys, n_heads, n_kv_heads;
+  int splits, split_keys;    // set by the launcher
+  float* part_o;             // [H][splits][D]
+  float* part_ml;            // [H][splits][2]
+  unsigned int* counters;    // [KVH], zero between launches (the merging CTA resets)
+  bf16* out;                 // [H*D]
+  float scale_log2;
+};
+int attn_split_keys(int n_keys, int n_kv_heads, int R);
+int attn_max_splits(int n_keys, int n_kv_heads, int R);  // workspace bound for any n <= n_keys
+int decode_attention_launch(AttnArgs a, int head_dim, cudaStream_t stream);
+
+// The whole anchor pass as one persistent kernel (one CTA per SM), see anchor.cu.
+constexpr int kAnchorClaimSlots = 256;  // > any SM id
+struct AnchorLayer {
+  const bf16* wqkv;
+  const bf16* wo;
+  const bf16* w1;
+  const bf16* w2;
+  const float* g_attn;
+  const float* g_mlp;
+  KvAddr src;         // keys 0..pos-1 (a reused layer: the producer's export, read in place)
+  KvAddr dst;         // the consumer cache layer (the anchor's own key goes here)
+  unsigned int wait;  // > 0: GemmEpi::done arrivals to wait for before the attention
+  int copy;           // store the src rows into dst while reading them (fused ingest)
+};
+struct AnchorArgs {
+  AnchorLayer layer[kMaxLayers];
+  int n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, mlp_kind, pos;
+  const int64_t* token;  // device: the anchor row's token id
+  const bf16* embed;
+  const float* rope_cos;
+  const float* rope_sin;
+  float* h;              // [d] residual stream of the anchor row
+  bf16* q;               // [H*D]
+  bf16* o;               // [H*D]
+  bf16* u;               // [d_ff]
+  float* part_o;
+  float* part_ml;
+  unsigned int* head_count;  // [KVH] zero
+  unsigned int* done;        // [n_layers] zero at launch; re-armed by the kernel
+  unsigned int* bar;         // [2] grid barrier (count zero), then [gridDim] SM id of each CTA
+  unsigned long long* stamps;  // [1 + 5 * n_layers] global ns after the seed and each phase (rank 0)
+  unsigned int* claim;       // [kAnchorClaimSlots] CTAs seen per SM id, zero
+  unsigned int* n_active;    // [1] working CTAs (one per SM), zero
+  int splits, split_keys;    // set by the launcher
+  float scale_log2;
+};
+int anchor_persistent_smem(const ds_dims& d, int n_keys);
+bool anchor_persistent_fits(const ds_dims& d, int n_keys);
+// DS_ERR_INVALID when the shape does not fit the co-resident budget (callers fall back).
+// co_resident: sized to share each SM with a GEMM / FA CTA of another stream
+// (launch it once those hold the SMs); else it claims enough shared memory that
+// no two of its CTAs share an SM.
+int anchor_persistent_launch(AnchorArgs a, cudaStream_t stream, bool co_resident);
 
 }  // namespace ds

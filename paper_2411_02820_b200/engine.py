@@ -139,7 +139,7 @@ class PagedKV:
 
 @dataclass(eq=False)
 class ECache:
-    """Residual-stream input of one layer over the window, bf16 [positions, d_model]
+    """Residual-stream input of one layer over the window, f32 [positions, d_model]
     (model.py:373-391)."""
 
     layer: int
@@ -226,17 +226,19 @@ def _normalize_e(sender_e) -> dict:
 
 
 def full_prefill(model: ModelWeights, tokens, e_layers: Iterable[int] | None = None, *, out: LayerKV | None = None,
-                 stream=None, tokens_dev: torch.Tensor | None = None) -> PrefillResult:
+                 stream=None, copy_stream=None, tokens_dev: torch.Tensor | None = None) -> PrefillResult:
     """Producer export: K/V at every layer over all n positions, E over the
     window (n-1 rows) at ``e_layers`` (default: every layer, profiling mode;
     pass the transition layers for the serving-mode filter, store.py:202-203),
-    and first-token logits."""
+    and first-token logits.  Same kernels and structure as a partial prefill
+    with every layer recomputed (model.py:641-649), so the two agree bit for
+    bit; ``copy_stream`` runs the anchor row beside the window."""
     cfg = model.config
     ids = check_tokens(tokens, cfg)
     n = ids.shape[0]
     layers = list(range(cfg.n_layers)) if e_layers is None else sorted(set(int(l) for l in e_layers))
     kv = out if out is not None else LayerKV.empty(cfg, n, model.device)
-    e_bufs = [torch.empty(n - 1, cfg.d_model, dtype=torch.bfloat16, device=model.device) for _ in layers]
+    e_bufs = [torch.empty(n - 1, cfg.d_model, dtype=torch.float32, device=model.device) for _ in layers]
     logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=model.device)
     tok = torch.empty(1, dtype=torch.int32, device=model.device)
     s = stream if stream is not None else torch.cuda.current_stream(model.device)
@@ -247,7 +249,7 @@ def full_prefill(model: ModelWeights, tokens, e_layers: Iterable[int] | None = N
     rc = L.lib().ds_full_prefill(C.byref(model.desc()), ids.ctypes.data,
                                  tokens_dev.data_ptr() if tokens_dev is not None else None, n, C.byref(desc), la,
                                  len(layers), ptrs, logits.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel(),
-                                 s.cuda_stream)
+                                 s.cuda_stream, copy_stream.cuda_stream if copy_stream is not None else None)
     L.check(rc)
     return PrefillResult(kv=kv, e_caches=tuple(ECache(l, b) for l, b in zip(layers, e_bufs)), logits=logits,
                          token_dev=tok)
@@ -274,8 +276,8 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
     groups = [x for g in config.groups for x in g]
     ga = (C.c_int32 * max(1, len(groups)))(*groups)
     for l, e in e_map.items():
-        if e.hidden.dtype != torch.bfloat16 or not e.hidden.is_cuda or not e.hidden.is_contiguous():
-            raise ValueError(f"E cache of layer {l} must be a contiguous bf16 device tensor")
+        if e.hidden.dtype != torch.float32 or not e.hidden.is_cuda or not e.hidden.is_contiguous():
+            raise ValueError(f"E cache of layer {l} must be a contiguous f32 device tensor")
     e_list = [L.ECacheDesc(l, e.positions, e.hidden.shape[1], e.hidden.data_ptr()) for l, e in sorted(e_map.items())]
     ea = (L.ECacheDesc * max(1, len(e_list)))(*e_list)
     skv = sender_kv.desc() if sender_kv is not None else None

@@ -66,11 +66,11 @@ class CostModel:
     @classmethod
     def from_measured(cls, config: ModelConfig, positions: int, link_gbs: float, layer_ms: float,
                       anchor_ms: float, dtype_bytes: int = 2) -> "CostModel":
-        """Cost model in milliseconds of the B200 path: bf16 byte sizes, a link of
-        ``link_gbs`` GB/s (NVLink P2P, or HBM for a same-GPU ingest), and the
-        measured recompute time per layer and anchor pass time."""
+        """Cost model in milliseconds of the B200 path: bf16 KV and f32 E byte
+        sizes, a link of ``link_gbs`` GB/s (NVLink P2P, or HBM for a same-GPU
+        ingest), and the measured recompute time per layer and anchor pass time."""
         kv = 2 * config.n_kv_heads * config.head_dim * dtype_bytes * positions
-        e = config.d_model * dtype_bytes * positions
+        e = config.d_model * 4 * positions
         return cls(link_bandwidth=link_gbs * 1e6, kv_layer_bytes=float(kv), e_layer_bytes=float(e),
                    layer_compute_time=layer_ms, anchor_time=anchor_ms)
 

@@ -78,11 +78,11 @@ def export_prefill(prefill: PrefillResult, model_id: str, tokens) -> ExportHandl
 
 
 class PeerBuffer:
-    """A bf16 [rows, cols] region of a peer GPU's HBM mapped into this process.
+    """An f32 [rows, cols] region (an E export) of a peer GPU's HBM mapped into this process.
     Duck-types the few tensor properties the engine reads (data_ptr, shape,
     dtype, is_cuda, is_contiguous, dim, nbytes)."""
 
-    dtype = torch.bfloat16
+    dtype = torch.float32
     is_cuda = True
 
     def __init__(self, ptr: int, rows: int, cols: int):
@@ -99,7 +99,7 @@ class PeerBuffer:
 
     @property
     def nbytes(self) -> int:
-        return self.shape[0] * self.shape[1] * 2
+        return self.shape[0] * self.shape[1] * 4
 
 
 class RemoteKV:
@@ -198,7 +198,7 @@ class NcclTransport:
     def e_job(self, layer: int, e, link):
         buf = self.e_stage.get(layer)
         if buf is None:
-            buf = torch.empty(self.window, self.d_model, dtype=torch.bfloat16, device=self.device)
+            buf = torch.empty(self.window, self.d_model, dtype=torch.float32, device=self.device)
             self.e_stage[layer] = buf
         with torch.cuda.stream(link) if link is not None else _null():
             self._recv(buf)

@@ -66,6 +66,7 @@ def test_config1_partial_prefill_parity(pkg, tiny):
     k, v, e, lp = O.full_prefill(oA, toks)
     assert rel(_host(prod.kv.k), k) < 2e-2 and rel(_host(prod.kv.v), v) < 2e-2
     assert rel(_host(prod.e_map()[2].hidden), e[2]) < 1e-2
+    assert prod.e_map()[2].hidden.dtype == torch.float32
     assert np.array_equal(_host(prod.e_map()[0].hidden), O.bf16_round(oA["embed"][toks[:P]]))
     assert np.abs(_host(prod.logits) - lp).max() < 0.1
     # --- consumer
@@ -86,7 +87,7 @@ def test_config1_partial_prefill_parity(pkg, tiny):
     assert cons.token == int(np.argmax(logits))
     # bf16-faithful mirror: same rounding points as the kernels
     bA, bB = O.round_weights_bf16(oA), O.round_weights_bf16(oB)
-    fk, fv, fe, _ = O.full_prefill(bA, toks, act=O.bf16_round, e_act=O.bf16_round)
+    fk, fv, fe, _ = O.full_prefill(bA, toks, act=O.bf16_round)  # E exported exactly (f32)
     _, _, lf = O.partial_prefill(bB, toks, [(2, 3)], O.bf16_round(fk), O.bf16_round(fv), fe, act=O.bf16_round)
     assert rel(logits, lf) < 1e-2
 

@@ -56,7 +56,7 @@ def test_store_fetch_then_pipeline(pair):
     prod = P.full_prefill(A, toks)
     st = P.CacheStore(mode="serving", transition_layers=rc.transition_layers, config=cfg)
     total = P.store_prefill(st, A.ident, toks, prod)
-    assert total == 4 * cfg.kv_bytes_per_position_bf16 * len(toks) + cfg.e_bytes_per_position_bf16 * (len(toks) - 1)
+    assert total == 4 * cfg.kv_bytes_per_position_bf16 * len(toks) + cfg.e_bytes_per_position_stored * (len(toks) - 1)
     kv, e_map = P.fetch_context_caches(st, A.ident, toks, rc, cfg.n_layers)
     assert sorted(e_map) == [2] and kv.layers[2] is None and kv.layers[3] is None
     ref = P.partial_prefill(B, toks, rc, prod.kv, prod.e_map())

@@ -173,7 +173,7 @@ def test_cost_from_model_golden(sched_fx):
     assert [c.link_bandwidth, c.kv_layer_bytes, c.e_layer_bytes, c.layer_compute_time, c.anchor_time,
             c.unit_mode] == sched_fx["cost_from_model_8b"]
     m = S.CostModel.from_measured(cfg, 8191, 770.0, 2.3, 1.9)
-    assert m.kv_layer_bytes == 2 * 8 * 128 * 2 * 8191 and m.e_layer_bytes == 2 * m.kv_layer_bytes
+    assert m.kv_layer_bytes == 2 * 8 * 128 * 2 * 8191 and m.e_layer_bytes == 4096 * 4 * 8191
 
 
 def test_plan_rejects_bad_requests():

@@ -29,7 +29,7 @@ def _prefill(n_layers, G, n, D, d):
     g = torch.Generator().manual_seed(123)
     k = torch.randn(n_layers, G, n, D, generator=g).to(torch.bfloat16)
     v = torch.randn(n_layers, G, n, D, generator=g).to(torch.bfloat16)
-    es = tuple(P.ECache(l, torch.randn(n - 1, d, generator=g).to(torch.bfloat16)) for l in range(n_layers))
+    es = tuple(P.ECache(l, torch.randn(n - 1, d, generator=g)) for l in range(n_layers))
     return P.PrefillResult(P.LayerKV(k, v), es, torch.zeros(4), torch.zeros(1, dtype=torch.int32))
 
 
