@@ -18,6 +18,8 @@
 //   EPI_SILU_BF16 out = bf16(silu(acc))            (silu(rms(x)*g @ w1))
 //   EPI_SWIGLU_BF16 out = bf16(silu(gate) * up)    (Llama-3 MLP, interleaved gate/up columns)
 //   EPI_STORE_*   plain stores (tests / lm head)
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -321,6 +323,218 @@ __global__ void __maxnreg__(128)
   }
 }
 
+
+// ---------------------------------------------------------------- CTA-pair (cta_group::2) variant
+//
+// A cluster of 2 CTAs on one TPC computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 16), issued by the leader
+// (rank 0).  CTA r holds A rows [256m + 128r, +128) and B rows (output
+// columns) [256n + 128r, +128) in its own shared memory; the MMA reads both
+// halves, and CTA r's TMEM receives its 128 output rows x all 256 columns.
+// Per CTA and k-block the operands are 32 KB instead of 48 KB (B is shared),
+// so L2->SM traffic per FLOP drops by a third and 6 stages fit where 4 did.
+//
+//   full[s]   leader only: one arrive.expect_tx (both CTAs' bytes) + the
+//             complete_tx of both CTAs' TMA loads (cta_group::2 TMA signals
+//             the leader's barrier)
+//   empty[s]  both CTAs: MMA commit multicast -> the producers refill
+//   tfull[a]  both CTAs: MMA commit multicast after a tile's last k-block
+//   tempty[a] leader only, 8 arrivals: the 4 epilogue warps of each CTA
+constexpr int PAIR_BN = 256;             // output columns per pair tile
+constexpr int PAIR_HALF = 128;           // B rows per CTA
+constexpr int PAIR_STAGES = 6;
+
+struct Gemm2Smem {
+  static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;    // 16 KB
+  static constexpr uint32_t B_BYTES = PAIR_HALF * GEMM_BK * 2;  // 16 KB
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t BAR_BYTES = (2 * PAIR_STAGES + 4) * 8 + 16;
+  static constexpr uint32_t TOTAL = 1024 + PAIR_STAGES * STAGE_BYTES + BAR_BYTES;
+};
+
+DS_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DS_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Shared-memory address of the same variable in CTA `rank` of the cluster.
+DS_DEV uint32_t map_to_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+DS_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+DS_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on the barrier at this offset in both CTAs once the pair's MMAs complete.
+DS_DEV void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .b16 m;\n mov.b16 m, 3;\n"
+      " tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+DS_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
+                    GemmEpi epi) {
+  using L = Gemm2Smem;
+  constexpr uint32_t TMEM_COLS = 2 * PAIR_BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + PAIR_STAGES * L::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + PAIR_STAGES * L::B_BYTES);
+  uint64_t* empty = full + PAIR_STAGES;
+  uint64_t* tfull = empty + PAIR_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int num_m = (epi.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM);
+  const int num_n = (epi.N + PAIR_BN - 1) / PAIR_BN;
+  const int num_tiles = num_m * num_n;
+  const int k_blocks = (K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < PAIR_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t leader_full0 = map_to_rank(&full[0], 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < num_tiles; t += n_pairs) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, epi.group, mb, nb);
+        const int arow = mb * 2 * GEMM_BM + (int)rank * GEMM_BM;
+        const int brow = nb * PAIR_BN + (int)rank * PAIR_HALF;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
+          const uint32_t fb = leader_full0 + stage * 8;
+          tma_load_2d_pair(sA + stage * L::A_BYTES, &tmA, fb, kb * GEMM_BK, arow);
+          tma_load_2d_pair(sB + stage * L::B_BYTES, &tmB, fb, kb * GEMM_BK, brow);
+          if (++stage == PAIR_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t IDESC = umma_idesc_bf16(2 * GEMM_BM, PAIR_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < num_tiles; t += n_pairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * PAIR_BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + stage * L::A_BYTES);
+            const uint32_t b_addr = smem_u32(sB + stage * L::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              const uint64_t ad = sdesc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bd = sdesc_sw128(b_addr + k * 32, 16, 1024);
+              umma_bf16_pair(d_tmem, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+            }
+            umma_commit_pair(&empty[stage]);
+            if (kb == k_blocks - 1) umma_commit_pair(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == PAIR_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const uint32_t leader_tempty0 = map_to_rank(&tempty[0], 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < num_tiles; t += n_pairs) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, epi.group, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * PAIR_BN;
+      epilogue_tile<PAIR_BN>(epi, tbase, mb * 2 * GEMM_BM + (int)rank * GEMM_BM + quarter * 32 + lane, nb);
+      tc_fence_before();
+      if (epi.done) __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_remote(leader_tempty0 + acc * 8);
+        if (epi.done) atomicAdd(epi.done, 1u);
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs / arrivals touch this CTA's smem and TMEM until here
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -386,19 +600,66 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
 
 int gemm_bn(int N) { return N >= 1024 ? 256 : 128; }
 
-// Arrivals on GemmEpi::done once the GEMM has finished: 4 epilogue warps per tile.
+// The CTA-pair kernel serves the large recompute shapes (DS_GEMM_PAIR=0 turns it off).
+static bool use_pair(int M, int N) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("DS_GEMM_PAIR");
+    env = (v && v[0] == '0') ? 0 : 1;
+  }
+  return env && N >= 1024 && M > GEMM_BM && num_sms() >= 2;
+}
+
+// Arrivals on GemmEpi::done once the GEMM has finished: 4 epilogue warps per
+// 128-row CTA tile (the pair kernel: 2 CTA tiles per 256 x 256 pair tile).
 unsigned int gemm_done_target(int M, int N) {
+  if (use_pair(M, N))
+    return 8u * (unsigned)(((M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((N + PAIR_BN - 1) / PAIR_BN));
   const int bn = gemm_bn(N);
   return 4u * (unsigned)(((M + GEMM_BM - 1) / GEMM_BM) * ((N + bn - 1) / bn));
 }
 
-// A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks BN from N.
+static cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, int K, const GemmEpi& epi,
+                                   cudaStream_t stream, int max_ctas) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Smem::TOTAL);
+    if (e != cudaSuccess) return e;
+    prefer_max_smem(gemm_tc2_kernel);
+    attr_set = true;
+  }
+  const int tiles = ((epi.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((epi.N + PAIR_BN - 1) / PAIR_BN);
+  int pairs = num_sms() / 2;
+  if (max_ctas > 0 && pairs > max_ctas / 2) pairs = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
+  if (pairs > tiles) pairs = tiles;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Gemm2Smem::TOTAL;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  return cudaLaunchKernelEx(&cfg, gemm_tc2_kernel, ta, tb, K, epi);
+}
+
+// A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks the kernel from the shape.
 int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
                 cudaStream_t stream, int force_bn, int max_ctas) {
-  int bn = force_bn ? force_bn : gemm_bn(epi.N);
   GemmEpi e2 = epi;
-  e2.group = 16;  // measured best of 8 / 16 / 64 for the recompute shapes
   CUtensorMap ta, tb;
+  if (!force_bn && use_pair(epi.M, epi.N)) {
+    e2.group = 8;  // 8 pair m-blocks = the 16 128-row m-blocks of the single-CTA raster
+    if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK) ||
+        make_tmap_bf16(&tb, B, epi.N, K, ldb, PAIR_HALF, GEMM_BK))
+      return launch_status(cudaErrorInvalidValue);
+    return launch_status(launch_gemm_pair(ta, tb, K, e2, stream, max_ctas));
+  }
+  int bn = force_bn ? force_bn : gemm_bn(epi.N);
+  e2.group = 16;  // measured best of 8 / 16 / 64 for the recompute shapes
   if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK) || make_tmap_bf16(&tb, B, epi.N, K, ldb, bn, GEMM_BK))
     return launch_status(cudaErrorInvalidValue);
   cudaError_t e = bn == 256 ? launch_gemm_t<256, 4>(ta, tb, K, e2, stream, max_ctas)
