@@ -4,6 +4,7 @@
 // (ingest on the copy stream overlapping recompute on the compute stream,
 // anchor gated on both — the pipelined plan of sched.py:212-263).
 #include <stdarg.h>
+#include <stdlib.h>
 #include <math.h>
 #include <stdio.h>
 #include <string.h>
@@ -104,6 +105,8 @@ struct Workspace {
   bf16* k0;           // [KVH][n][D] receiver's exact layer-0 K of the window
   bf16* v0;
   unsigned int* dec_count;  // [n_kv_heads] split-merge counters (zero between launches)
+  float* ssq;               // [ceil(d/128)][n] per-column-tile sums of squares (RMSNorm folded into the GEMMs)
+  long long rows;           // positions the workspace was carved for
   unsigned int* an_ctl;     // persistent anchor control block: done[kMaxLayers], bar[2], smid[kMaxAnchorCtas]
   unsigned long long* an_stamps;  // persistent anchor phase times (ds_anchor_timeline)
   size_t bytes;
@@ -142,9 +145,11 @@ Workspace carve(const ds_dims& m, int n, void* base) {
   w.k0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
   w.v0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
   w.dec_count = reinterpret_cast<unsigned int*>(take(4ull * m.n_kv_heads));
+  w.ssq = reinterpret_cast<float*>(take(4ull * ((m.d_model + 127) / 128) * n));
   w.an_ctl = reinterpret_cast<unsigned int*>(take(4ull * kAnchorCtlWords));
   w.an_stamps = reinterpret_cast<unsigned long long*>(take(8ull * (1 + 5 * kMaxLayers)));
   w.bytes = off;
+  w.rows = n;
   return w;
 }
 
@@ -201,13 +206,41 @@ struct Ctx {
   cudaEvent_t after_seed = nullptr;    // recorded after the first group's seed kernel
 };
 
-// (a = RMSNorm(h) already in the workspace) QKV (+RoPE, K/V into the cache) -> [attention -> o-proj+resid -> RMSNorm -> W1+SiLU -> W2+resid]
+// QKV (+RoPE, K/V into the cache) -> [attention -> o-proj+resid -> W1+SiLU -> W2+resid]
 // over `rows` window rows at positions 0..rows-1 (model.py:536-544).  `kv_only`: the window output of
 // this layer is dead (last layer of a group, model.py:625), so only the K/V columns are projected.
-int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos = nullptr) {
+// RMSNorm is folded into the GEMMs: the residual epilogues (o-proj, W2) store bf16(h * g) and
+// per-column-tile sums of squares, and the consuming GEMM (W1, next QKV) scales its rows by 1/rms.
+// fuse_in: the QKV operand comes from the previous layer's W2 epilogue (else from an RMSNorm
+// kernel, already normalised); g_next: the next layer's attention gain (W2 prepares its operand).
+// DS_FUSE_NORM=0: the stand-alone RMSNorm kernels instead (A/B measurements).
+bool fuse_norm() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_FUSE_NORM");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos = nullptr, bool fuse_in = false,
+                 const float* g_next = nullptr) {
   const ds_dims& d = c.d;
   const ds_layer_weights& W = c.m->layers[l];
   const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
+  const int parts = (d.d_model + gemm_col_tile(rows, d.d_model) - 1) / gemm_col_tile(rows, d.d_model);
+  auto norm_in = [&](GemmEpi& g) {
+    g.ssq_in = c.w.ssq;
+    g.ssq_parts = parts;
+    g.norm_dim = d.d_model;
+    g.ld_ssq = c.w.rows;
+  };
+  auto norm_out = [&](GemmEpi& g, const float* gain) {
+    g.norm_out = c.w.a;
+    g.norm_gain = gain;
+    g.ssq_out = c.w.ssq;
+    g.ld_ssq = c.w.rows;
+  };
   GemmEpi e{};
   e.mode = EPI_QKV_ROPE;
   e.M = rows;
@@ -223,6 +256,7 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos =
   e.pos_rows = row_pos;  // token-selective rows sit at scattered positions
   e.rope_cos = c.m->rope_cos;
   e.rope_sin = c.m->rope_sin;
+  if (fuse_in) norm_in(e);
   if (c.qkv_done) e.done = c.qkv_done + l;
   const bf16* wqkv = static_cast<const bf16*>(W.wqkv) + (kv_only ? (long long)hd * d.d_model : 0);
   DS_TRY(gemm_launch(c.w.a, d.d_model, wqkv, d.d_model, d.d_model, e, c.s), "qkv gemm");
@@ -242,9 +276,11 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos =
   r.ld_out = d.d_model;
   r.resid = c.w.h;
   r.ld_resid = d.d_model;
+  if (fuse_norm()) norm_out(r, W.g_mlp);
   DS_TRY(gemm_launch(c.w.o, hd, W.wo, hd, hd, r, c.s), "o-proj gemm");
-  DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, rows, d.d_model, W.g_mlp, c.w.a, nullptr, nullptr, 0, c.s),
-         "rmsnorm");
+  if (!fuse_norm())
+    DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, rows, d.d_model, W.g_mlp, c.w.a, nullptr, nullptr, 0, c.s),
+           "rmsnorm");
   GemmEpi f{};
   const bool swiglu = d.mlp_kind == DS_MLP_SWIGLU;
   f.mode = swiglu ? EPI_SWIGLU_BF16 : EPI_SILU_BF16;
@@ -252,8 +288,18 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos =
   f.N = swiglu ? 2 * d.d_ff : d.d_ff;
   f.out = c.w.u;
   f.ld_out = d.d_ff;
+  if (fuse_norm()) norm_in(f);
   DS_TRY(gemm_launch(c.w.a, d.d_model, W.w1, d.d_model, d.d_model, f, c.s), "w1 gemm");
-  DS_TRY(gemm_launch(c.w.u, d.d_ff, W.w2, d.d_ff, d.d_ff, r, c.s), "w2 gemm");
+  GemmEpi r2{};
+  r2.mode = EPI_RESID_F32;
+  r2.M = rows;
+  r2.N = d.d_model;
+  r2.out = c.w.h;
+  r2.ld_out = d.d_model;
+  r2.resid = c.w.h;
+  r2.ld_resid = d.d_model;
+  if (g_next && fuse_norm()) norm_out(r2, g_next);
+  DS_TRY(gemm_launch(c.w.u, d.d_ff, W.w2, d.d_ff, d.d_ff, r2, c.s), "w2 gemm");
   trace(c.s, DS_TRACE_LAYER + l);
   return DS_OK;
 }
@@ -360,7 +406,12 @@ int recompute_group(Ctx& c, const int64_t* tok, int P, int a, int b, const void*
       return cuda_fail("e export");
     return DS_OK;
   };
-  if (a == 0)
+  const bool fuse = fuse_norm();
+  if (fuse)
+    DS_TRY(norm_seed_launch(a == 0 ? c.m->embed : seed, a == 0, a == 0 ? tok : nullptr, P, d.d_model,
+                            gemm_col_tile(P, d.d_model), Wa.g_attn, c.w.a, c.w.h, c.w.ssq, c.w.rows, c.s),
+           "seed");
+  else if (a == 0)
     DS_TRY(rmsnorm_launch(c.m->embed, true, tok, P, d.d_model, Wa.g_attn, c.w.a, c.w.h, nullptr, P, c.s), "seed");
   else
     DS_TRY(rmsnorm_launch(seed, false, nullptr, P, d.d_model, Wa.g_attn, c.w.a, c.w.h, nullptr, P, c.s), "seed");
@@ -371,12 +422,13 @@ int recompute_group(Ctx& c, const int64_t* tok, int P, int a, int b, const void*
   }
   for (int l = a; l <= b; ++l) {
     if (l > a) {
-      DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, P, d.d_model, c.m->layers[l].g_attn, c.w.a, nullptr, nullptr, 0,
-                            c.s),
-             "rmsnorm");
+      if (!fuse)
+        DS_TRY(rmsnorm_launch(c.w.h, false, nullptr, P, d.d_model, c.m->layers[l].g_attn, c.w.a, nullptr, nullptr, 0,
+                              c.s),
+               "rmsnorm");
       if (int rc = export_e(l)) return rc;
     }
-    int rc = window_layer(c, l, P, l == b);
+    int rc = window_layer(c, l, P, l == b, nullptr, /*fuse_in=*/fuse, l < b ? c.m->layers[l + 1].g_attn : nullptr);
     if (rc) return rc;
   }
   return DS_OK;
@@ -747,14 +799,21 @@ int ds_token_selective_prefill(const ds_model* m, const int64_t* tokens_host, co
   DS_TRY(select_topk_launch(w.dev, P, n_sel, tok, w.sel_pos, w.sel_tok, s), "select");
   // 3. the selected positions through every layer (model.py:726-734): their K/V
   //    replace the sender's in the cache, attention is causal by absolute position
-  DS_TRY(rmsnorm_launch(m->embed, true, w.sel_tok, n_sel, d.d_model, m->layers[0].g_attn, w.a, w.h, nullptr, n_sel,
-                        s),
-         "seed");
+  //    (the same per-layer sequence as a recompute group, so ratio 1 is recompute-all bit for bit)
+  const bool fuse = fuse_norm();
+  if (fuse)
+    DS_TRY(norm_seed_launch(m->embed, true, w.sel_tok, n_sel, d.d_model, gemm_col_tile(n_sel, d.d_model),
+                            m->layers[0].g_attn, w.a, w.h, w.ssq, w.rows, s),
+           "seed");
+  else
+    DS_TRY(rmsnorm_launch(m->embed, true, w.sel_tok, n_sel, d.d_model, m->layers[0].g_attn, w.a, w.h, nullptr, n_sel,
+                          s),
+           "seed");
   for (int l = 0; l < L; ++l) {
-    if (l > 0)
+    if (l > 0 && !fuse)
       DS_TRY(rmsnorm_launch(w.h, false, nullptr, n_sel, d.d_model, m->layers[l].g_attn, w.a, nullptr, nullptr, 0, s),
              "rmsnorm");
-    rc = window_layer(c, l, n_sel, l == L - 1, w.sel_pos);
+    rc = window_layer(c, l, n_sel, l == L - 1, w.sel_pos, fuse, l < L - 1 ? m->layers[l + 1].g_attn : nullptr);
     if (rc) return rc;
   }
   // 4. the anchor through every layer

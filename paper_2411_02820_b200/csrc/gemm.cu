@@ -50,10 +50,19 @@ DS_DEV void tile_coords(int t, int num_m, int num_n, int group, int& mb, int& nb
   nb = r / gsize;
 }
 
+// 1 / rms of the row from the producer GEMM's per-tile partial sums (fixed order).
+DS_DEV float row_inv_rms(const GemmEpi& e, int row, bool row_ok) {
+  if (!e.ssq_in || !row_ok) return 1.f;
+  float t = 0.f;
+  for (int p = 0; p < e.ssq_parts; ++p) t += __ldcg(e.ssq_in + p * e.ld_ssq + row);
+  return 1.0f / sqrtf(t / (float)e.norm_dim + 1e-6f);
+}
+
 template <int BN>
 DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
   const bool row_ok = row < e.M;
   const int col0 = nb * BN;
+  const float inv = row_inv_rms(e, row, row_ok);
   if (e.mode == EPI_QKV_ROPE) {
     // j outer, heads inner: one row's cos/sin chunk (16-byte vector loads of
     // the f32 tables) serves every head of the tile
@@ -81,6 +90,13 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
         float lo[16], hi[16];
         tmem_ld16x2(tbase + cb + j, tbase + cb + half + j, lo, hi);
         if (!row_ok) continue;
+        if (e.ssq_in) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            lo[i] *= inv;
+            hi[i] *= inv;
+          }
+        }
         if (is_q || is_k) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -125,6 +141,7 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
         if (ncols > 16) r1[i] = r[4 + i];
       }
     }
+    float ss = 0.f;
     for (int c = 0; c < ncols; c += 16) {
       if (row_ok && c + 32 < ncols) {
 #pragma unroll
@@ -134,9 +151,27 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
       tmem_ld16(tbase + c, v);
       if (row_ok) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          o[c / 4 + i] = make_float4(r0[i].x + v[4 * i], r0[i].y + v[4 * i + 1], r0[i].z + v[4 * i + 2],
-                                     r0[i].w + v[4 * i + 3]);
+        for (int i = 0; i < 16; ++i) v[i] += (&r0[i / 4].x)[i % 4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[c / 4 + i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        if (e.norm_out) {
+          // the next GEMM's operand: bf16(h * g); its epilogue applies 1/rms
+          const float4* g4 = reinterpret_cast<const float4*>(e.norm_gain + col0 + c);
+          uint32_t p[8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 g = __ldg(g4 + i);
+            ss = fmaf(v[4 * i], v[4 * i], ss);
+            ss = fmaf(v[4 * i + 1], v[4 * i + 1], ss);
+            ss = fmaf(v[4 * i + 2], v[4 * i + 2], ss);
+            ss = fmaf(v[4 * i + 3], v[4 * i + 3], ss);
+            p[2 * i] = pack_bf16x2(v[4 * i] * g.x, v[4 * i + 1] * g.y);
+            p[2 * i + 1] = pack_bf16x2(v[4 * i + 2] * g.z, v[4 * i + 3] * g.w);
+          }
+          bf16* a = e.norm_out + (long long)row * e.ld_out + col0 + c;
+          st_global_v4(a, p[0], p[1], p[2], p[3]);
+          st_global_v4(a + 8, p[4], p[5], p[6], p[7]);
+        }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -144,6 +179,7 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
         r1[i] = r2[i];
       }
     }
+    if (e.ssq_out && row_ok) e.ssq_out[nb * e.ld_ssq + row] = ss;
     return;
   }
   if (e.mode == EPI_SWIGLU_BF16) {
@@ -155,6 +191,13 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
       float gt[16], up[16];
       tmem_ld16x2(tbase + c, tbase + c + 16, gt, up);
       if (!row_ok) continue;
+      if (e.ssq_in) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          gt[i] *= inv;
+          up[i] *= inv;
+        }
+      }
       uint32_t p[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) p[i] = pack_bf16x2(silu(gt[2 * i]) * up[2 * i], silu(gt[2 * i + 1]) * up[2 * i + 1]);
@@ -175,6 +218,10 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     } else {
+      if (e.ssq_in) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= inv;
+      }
       if (e.mode == EPI_SILU_BF16) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = silu(v[i]);
@@ -609,6 +656,8 @@ static bool use_pair(int M, int N) {
   }
   return env && N >= 1024 && M > GEMM_BM && num_sms() >= 2;
 }
+
+int gemm_col_tile(int M, int N) { return use_pair(M, N) ? PAIR_BN : gemm_bn(N); }
 
 // Arrivals on GemmEpi::done once the GEMM has finished: 4 epilogue warps per
 // 128-row CTA tile (the pair kernel: 2 CTA tiles per 256 x 256 pair tile).

@@ -33,6 +33,18 @@ struct GemmEpi {
   const float* rope_cos;  // [max_seq][head_dim/2]
   const float* rope_sin;
   unsigned int* done;   // optional: +1 per (tile, epilogue warp) once its stores are visible
+  // RMSNorm folded into the GEMMs (model.py:466-468): RMSNorm(h)*g @ W = ((h*g) @ W) * inv_rms(h).
+  // Producer side (EPI_RESID_F32): also store norm_out = bf16(h_new * norm_gain) and, per output
+  // column tile nb, ssq_out[nb * ld_ssq + row] = sum of h_new^2 over the tile's columns.
+  bf16* norm_out;
+  const float* norm_gain;
+  float* ssq_out;
+  // Consumer side (QKV / SiLU / SwiGLU): scale each row's accumulator by
+  // 1 / sqrt(sum_p ssq_in[p * ld_ssq + row] / norm_dim + 1e-6), partials summed in order.
+  const float* ssq_in;
+  int ssq_parts;
+  int norm_dim;
+  long long ld_ssq;
 };
 
 // Base of layer `layer`'s K (v = false) or V block in a cache descriptor:
@@ -93,12 +105,15 @@ int num_sms();
 int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int K, const GemmEpi& epi,
                 cudaStream_t stream, int force_bn = 0, int max_ctas = 0);
 unsigned int gemm_done_target(int M, int N);
+int gemm_col_tile(int M, int N);  // output columns per epilogue tile (the ssq partial granularity)
 
 int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
                      int n_kv_heads, int head_dim, int window, cudaStream_t stream, bool background = false);
 
 int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,
                    float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream);
+int norm_seed_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, int T, const float* gain,
+                     bf16* out, float* copy_f32, float* ssq, long long ld, cudaStream_t stream);
 
 // Causal GQA prefill attention over one cache layer.  layer_rows = rows of the
 // layer region viewed as a [rows][head_dim] matrix (TMA bound).  Cache memory

@@ -106,6 +106,60 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, co
   }
 }
 
+// Group seed in the folded-RMSNorm format (see GemmEpi::norm_out / ssq_in): for
+// row r and column tile p (T columns), a[r][c] = bf16(x[r][c] * g[c]), the
+// f32 row copy, and ssq[p * ld + r] = fmaf-sum of x^2 over the tile's columns
+// in ascending order -- exactly what a residual GEMM epilogue writes, so a
+// group's first layer sees the same operand as a layer inside a group.
+template <bool IN_BF16>
+__global__ void __launch_bounds__(NORM_THREADS) norm_seed_kernel(const void* x, const int64_t* gather, int M, int d,
+                                                                 int T, const float* gain, bf16* out, float* copy_f32,
+                                                                 float* ssq, long long ld) {
+  pdl_trigger();
+  pdl_wait();
+  const int parts = d / T;
+  const long long t = (long long)blockIdx.x * NORM_THREADS + threadIdx.x;
+  if (t >= (long long)M * parts) return;
+  const int r = (int)(t / parts), p = (int)(t - (long long)r * parts);
+  const long long src = gather ? (long long)__ldg(gather + r) : (long long)r;
+  float ss = 0.f;
+  for (int c = p * T; c < (p + 1) * T; c += 8) {
+    float v[8];
+    load8<IN_BF16>(x, src * d + c, v);
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + c));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + c + 4));
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    uint32_t q[4];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss = fmaf(v[e], v[e], ss);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) q[e] = pack_bf16x2(v[2 * e] * g[2 * e], v[2 * e + 1] * g[2 * e + 1]);
+    *reinterpret_cast<uint4*>(out + (long long)r * d + c) = make_uint4(q[0], q[1], q[2], q[3]);
+    if (copy_f32) {
+      float4* o = reinterpret_cast<float4*>(copy_f32 + (long long)r * d + c);
+      o[0] = make_float4(v[0], v[1], v[2], v[3]);
+      o[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  }
+  ssq[p * ld + r] = ss;
+}
+
+int norm_seed_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, int T, const float* gain,
+                     bf16* out, float* copy_f32, float* ssq, long long ld, cudaStream_t stream) {
+  if (M <= 0) return DS_OK;
+  if (T <= 0 || d % T || T % 8) return DS_ERR_INVALID;
+  count_launch();
+  static const bool c0 = prefer_max_smem(norm_seed_kernel<true>) && prefer_max_smem(norm_seed_kernel<false>);
+  (void)c0;
+  const long long threads = (long long)M * (d / T);
+  const dim3 grid((unsigned)((threads + NORM_THREADS - 1) / NORM_THREADS));
+  if (x_bf16)
+    return launch_status(launch_pdl(norm_seed_kernel<true>, grid, dim3(NORM_THREADS), 0, stream, x, gather, M, d, T,
+                                    gain, out, copy_f32, ssq, ld));
+  return launch_status(launch_pdl(norm_seed_kernel<false>, grid, dim3(NORM_THREADS), 0, stream, x, gather, M, d, T,
+                                  gain, out, copy_f32, ssq, ld));
+}
+
 int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,
                    float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream) {
   if (M <= 0) return DS_OK;
