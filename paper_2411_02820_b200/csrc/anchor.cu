@@ -30,6 +30,8 @@
 //                  it.  A recomputed layer's attention waits on the counter the
 //                  recompute's QKV GEMM epilogue bumps (GemmEpi::done), not on
 //                  a stream event.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -179,7 +181,12 @@ DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
   __syncthreads();
 }
 
-// One tile of 8 weight rows against the staged x, with its epilogue.
+// One tile of 8 weight rows against the staged x, with its epilogue.  UNROLL
+// (16-byte chunks per row per thread in flight) only batches the loads: every
+// thread still accumulates its chunks in ascending order, so the persistent
+// kernel (register-capped, UNROLL 2) and the stand-alone GEMV (UNROLL 4) give
+// bit-identical results.
+template <int UNROLL = GEMV_UNROLL>
 DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEMV_ROWS], unsigned long long& best) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nchunk = a.K >> 3;
@@ -190,14 +197,14 @@ DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEM
 #pragma unroll
   for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
   int c = tid;
-  for (; c + (GEMV_UNROLL - 1) * GEMV_THREADS < nchunk; c += GEMV_UNROLL * GEMV_THREADS) {
-    uint4 w[GEMV_UNROLL][GEMV_ROWS];
+  for (; c + (UNROLL - 1) * GEMV_THREADS < nchunk; c += UNROLL * GEMV_THREADS) {
+    uint4 w[UNROLL][GEMV_ROWS];
 #pragma unroll
-    for (int u = 0; u < GEMV_UNROLL; ++u)
+    for (int u = 0; u < UNROLL; ++u)
 #pragma unroll
       for (int r = 0; r < GEMV_ROWS; ++r) w[u][r] = ld_stream16(wr[r] + (c + u * GEMV_THREADS) * 8);
 #pragma unroll
-    for (int u = 0; u < GEMV_UNROLL; ++u) {
+    for (int u = 0; u < UNROLL; ++u) {
       const uint4 xv = *reinterpret_cast<const uint4*>(xs + (c + u * GEMV_THREADS) * 8);
 #pragma unroll
       for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(w[u][r], xv);
@@ -266,13 +273,14 @@ DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEM
 
 // Every tile of one GEMV, strided over the grid; the next tile's weights are
 // prefetched into L2 while the current one is reduced.
+template <int UNROLL = GEMV_UNROLL>
 DS_DEV unsigned long long gemv_all_tiles(const GemvArgs& a, const bf16* xs, float (*red)[GEMV_ROWS], int rank,
                                          int nranks) {
   const int tiles = a.N / GEMV_ROWS;
   unsigned long long best = 0ull;
   for (int t = rank; t < tiles; t += nranks) {
     if (t + nranks < tiles) gemv_prefetch(a, t + nranks);
-    gemv_tile(a, t, xs, red, best);
+    gemv_tile<UNROLL>(a, t, xs, red, best);
   }
   return best;
 }
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
   pdl_trigger();
   pdl_wait();
   gemv_stage_x(a, xs, ssq);
-  unsigned long long best = gemv_all_tiles(a, xs, red, blockIdx.x, gridDim.x);
+  unsigned long long best = gemv_all_tiles<2 * GEMV_UNROLL>(a, xs, red, blockIdx.x, gridDim.x);
   if (a.mode == EPI_STORE_F32 && a.argmax && tid < GEMV_ROWS) {
 #pragma unroll
     for (int o = 4; o; o >>= 1) {
@@ -331,8 +339,14 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
     if (int rc_ = launch_status(cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return rc_;
     attr = smem;
   }
+  static int per_sm_cap = -1;
+  if (per_sm_cap < 0) {
+    const char* v = getenv("DS_GEMV_PER_SM");  // experiments
+    per_sm_cap = v ? atoi(v) : 16;
+    if (per_sm_cap < 1) per_sm_cap = 16;
+  }
   int per_sm = (200 * 1024) / (smem + 1024);
-  per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
+  per_sm = per_sm < 1 ? 1 : (per_sm > per_sm_cap ? per_sm_cap : per_sm);
   const int cap = num_sms() * per_sm;
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
@@ -401,14 +415,16 @@ DS_DEV void attn_prefetch(const AttnArgs& a, int item, int D) {
   }
 }
 
-template <int D, int R>
+// DEEP: rows in flight per lane doubled (the stand-alone kernel, no register
+// cap); batching only -- every score and every P.V accumulation keeps its order.
+template <int D, int R, bool DEEP = false>
 DS_DEV void attn_item(const AttnArgs& a, int item, float* sc, float* stat, unsigned int* is_last) {
   constexpr int LPK = D / 8;       // lanes per key row
   constexpr int KPW = 32 / LPK;    // key rows per warp load
-  constexpr int U = R >= 8 ? 2 : 4;   // rows in flight per lane (scores)
+  constexpr int U = (R >= 8 ? 2 : 4) * (DEEP ? 2 : 1);   // rows in flight per lane (scores)
   constexpr int CPW = LPK / 4;     // dim chunks per warp (P.V)
   constexpr int NS = 32 / CPW;     // key streams per warp (P.V)
-  constexpr int U2 = R >= 8 ? 1 : 4;  // rows in flight per lane (P.V)
+  constexpr int U2 = (R >= 8 ? 1 : 4) * (DEEP ? 2 : 1);  // rows in flight per lane (P.V)
   const int g = item / a.splits, s = item - g * a.splits;
   const int k0 = s * a.split_keys;
   const int nk = min(a.split_keys, a.n_keys - k0);
@@ -620,7 +636,7 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_decode_kernel(AttnArgs a) {
   attn_prefetch(a, blockIdx.x, D);
   pdl_trigger();
   pdl_wait();
-  attn_item<D, R>(a, blockIdx.x, sc, stat, &is_last);
+  attn_item<D, R, true>(a, blockIdx.x, sc, stat, &is_last);
 }
 
 template <int D, int R>

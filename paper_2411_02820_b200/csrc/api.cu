@@ -305,7 +305,9 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos =
 }
 
 // The single anchor row at position `pos` through layer l (_layer_single, model.py:547-562).
-int anchor_layer(Ctx& c, int l, int pos, float* h_a) {
+// sender (optional): keys 0..pos-1 are read from the producer's export and
+// copied into the consumer cache as they are read (the fused KV ingest).
+int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender = nullptr) {
   const ds_dims& d = c.d;
   const ds_layer_weights& W = c.m->layers[l];
   const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
@@ -329,8 +331,9 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a) {
   const KvAddr ka = g.kv;
   AttnArgs at{};
   at.q = c.w.q_a;
-  at.lo = ka;
+  at.lo = sender ? layer_addr(*sender, l, d.head_dim) : ka;
   at.hi = ka;
+  at.copy_lo = sender ? 1 : 0;
   at.n_lo = pos;
   at.n_keys = pos + 1;
   at.n_heads = d.n_heads;
@@ -513,13 +516,15 @@ int zero_anchor_ctl(Ctx& c, cudaStream_t s) {
 int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* token,
                 const AnchorPlan* plan = nullptr, int64_t* token64 = nullptr) {
   const ds_dims& d = c.d;
-  if (anchor_persistent_fits(d, P + 1)) {
-    if (!(plan && plan->ctl_zeroed))
+  // The persistent kernel is the shape for running beside the recompute; alone,
+  // one 4-warp CTA per SM is latency-bound, so the per-launch kernels (up to 16
+  // GEMV CTAs per SM) run the pass -- same device functions, same results.
+  if (plan && plan->co_resident && anchor_persistent_fits(d, P + 1)) {
+    if (!plan->ctl_zeroed)
       if (int rc = zero_anchor_ctl(c, c.s)) return rc;
     DS_TRY(anchor_persistent(c, token_id, P, plan), "anchor");
     trace(c.s, DS_TRACE_ANCHOR + d.n_layers - 1);
   } else {
-    if (plan && plan->sender) return fail(DS_ERR_INVALID, "anchor: sender reads need the persistent kernel");
     if (int rc = reset_counters(c)) return rc;
     DS_TRY(rmsnorm_launch(c.m->embed, true, token_id, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr,
                           1, c.s),
@@ -527,7 +532,8 @@ int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* 
     for (int l = 0; l < d.n_layers; ++l) {
       if (plan && plan->wait_for && plan->wait_for[l] && cudaStreamWaitEvent(c.s, plan->wait_for[l], 0) != cudaSuccess)
         return cuda_fail("wait");
-      int rc = anchor_layer(c, l, P, c.w.h_a);
+      const bool from_sender = plan && plan->sender && plan->reused && plan->reused[l];
+      int rc = anchor_layer(c, l, P, c.w.h_a, from_sender ? plan->sender : nullptr);
       if (rc) return rc;
       trace(c.s, DS_TRACE_ANCHOR + l);
     }
@@ -567,26 +573,27 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
   const int L = d.n_layers, P = n - 1;
   int rc;
 
-  // Persistent anchor (the usual case): it reads the reused layers straight
-  // from the sender's export and stores them into the consumer cache as it
-  // goes (the KV ingest fused into the anchor's read of the same bytes).
-  const bool fused = anchor_persistent_fits(d, n);
+  // The anchor reads the reused layers straight from the sender's export and
+  // stores them into the consumer cache as it goes (the KV ingest fused into
+  // the anchor's read of the same bytes), in both orders.  `fused`: the
+  // persistent co-resident anchor runs beside the recompute (two streams).
+  // It is the right shape when the recompute is long enough to hide it (its
+  // 4 warps per SM stream the weights slower than the per-launch kernels,
+  // which take whole SMs): measured crossover (config-5 sweep, 8B shapes) at
+  // k * P ~ 800 * L recomputed row-layers.
+  long long recomputed = 0;
+  for (int l = 0; l < L; ++l) recomputed += covered[l];
+  const bool fused = anchor_persistent_fits(d, n) && recomputed * P >= 800LL * L;
   std::vector<char> reused_flag(L, 0);
   for (int l : reused) reused_flag[l] = 1;
   AnchorPlan plan;
-  if (fused && !reused.empty()) {
+  if (!reused.empty()) {
     plan.sender = sender_kv;
     plan.reused = reused_flag.data();
   }
 
   if (xs == cs) {
-    // single stream: (ingest,) recompute, then the anchor after all KV has landed (sched.py:256)
-    if (!fused && !reused.empty()) {
-      DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P,
-                              cs),
-             "kv ingest");
-      trace(cs, DS_TRACE_INGEST);
-    }
+    // single stream: recompute, then the anchor (sched.py:256), per-launch kernels
     for (int i = 0; i < n_groups; ++i) {
       rc = recompute_group(c, tok, P, groups[2 * i], groups[2 * i + 1], seed[i] ? seed[i]->hidden : nullptr);
       if (rc) return rc;
@@ -600,7 +607,7 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
   // waits for that layer's QKV GEMM and nothing else: the HBM-bound anchor
   // streams weights while the tensor-bound recompute runs.  Persistent path:
   // the wait is on the GEMM epilogue's arrival counter (one kernel, no events);
-  // per-launch path: on an event after the QKV GEMM, with the ingest first.
+  // per-launch path (shapes beyond its budget): on an event after the QKV GEMM.
   // Same kernels, same results as the single-stream order.  Events are created
   // once per host thread (capturable into CUDA graphs).
   thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_seed = nullptr;
@@ -634,12 +641,6 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
   }
   cudaEventRecord(ev_fork, cs);
   cudaStreamWaitEvent(xs, ev_fork, 0);
-  if (!fused && !reused.empty()) {
-    DS_TRY(kv_ingest_launch(*sender_kv, *out_kv, reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim, P, xs,
-                            /*background=*/true),
-           "kv ingest");
-    trace(xs, DS_TRACE_INGEST);
-  }
   Ctx cx{m, d, w, out_kv, xs};
   // enqueue the recompute (which records ev_layer[l]) before the anchor's waits:
   // a cudaStreamWaitEvent binds to the latest record at enqueue time

@@ -701,7 +701,13 @@ int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int 
   GemmEpi e2 = epi;
   CUtensorMap ta, tb;
   if (!force_bn && use_pair(epi.M, epi.N)) {
-    e2.group = 8;  // 8 pair m-blocks = the 16 128-row m-blocks of the single-CTA raster
+    static int group = -1;
+    if (group < 0) {
+      const char* v = getenv("DS_GEMM_GROUP");  // raster experiments
+      group = v ? atoi(v) : 8;
+      if (group < 1) group = 8;
+    }
+    e2.group = group;  // 8 pair m-blocks = the 16 128-row m-blocks of the single-CTA raster
     if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK) ||
         make_tmap_bf16(&tb, B, epi.N, K, ldb, PAIR_HALF, GEMM_BK))
       return launch_status(cudaErrorInvalidValue);

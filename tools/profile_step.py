@@ -24,6 +24,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=8192)
 ap.add_argument("--k", type=int, default=6)
 ap.add_argument("--what", default="partial", choices=["partial", "full"])
+ap.add_argument("--single", action="store_true", help="one stream (per-launch anchor kernels)")
 args = ap.parse_args()
 
 cfg = P.ModelConfig(32, 4096, 32, 8, 128, 14336, 128256, max(args.n, 8192), 0)
@@ -35,7 +36,7 @@ ids = np.random.default_rng(7).integers(0, cfg.vocab_size, size=args.n, dtype=np
 tok = torch.from_numpy(ids).cuda()
 prod = P.full_prefill(A, ids, e_layers=rc.transition_layers, tokens_dev=tok)
 cache = P.PagedKV.allocate(cfg, args.n)
-side = torch.cuda.Stream()
+side = None if args.single else torch.cuda.Stream()
 for _ in range(2):
     P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), out=cache, copy_stream=side, tokens_dev=tok)
 torch.cuda.synchronize()
