@@ -111,53 +111,62 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const void* x, co
 // f32 row copy, and ssq[p * ld + r] = fmaf-sum of x^2 over the tile's columns
 // in ascending order -- exactly what a residual GEMM epilogue writes, so a
 // group's first layer sees the same operand as a layer inside a group.
+// One CTA per row, 16 columns per thread (coalesced); a tile's T/16 threads
+// are adjacent lanes of one warp and pass the running sum along in order.
 template <bool IN_BF16>
-__global__ void __launch_bounds__(NORM_THREADS) norm_seed_kernel(const void* x, const int64_t* gather, int M, int d,
-                                                                 int T, const float* gain, bf16* out, float* copy_f32,
-                                                                 float* ssq, long long ld) {
+__global__ void __launch_bounds__(1024) norm_seed_kernel(const void* x, const int64_t* gather, int d, int T,
+                                                         const float* gain, bf16* out, float* copy_f32, float* ssq,
+                                                         long long ld) {
   pdl_trigger();
   pdl_wait();
-  const int parts = d / T;
-  const long long t = (long long)blockIdx.x * NORM_THREADS + threadIdx.x;
-  if (t >= (long long)M * parts) return;
-  const int r = (int)(t / parts), p = (int)(t - (long long)r * parts);
+  const int r = blockIdx.x, i = threadIdx.x;
+  const int tpp = T / 16, p = i / tpp, j = i - p * tpp;
   const long long src = gather ? (long long)__ldg(gather + r) : (long long)r;
-  float ss = 0.f;
-  for (int c = p * T; c < (p + 1) * T; c += 8) {
-    float v[8];
-    load8<IN_BF16>(x, src * d + c, v);
-    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gain + c));
-    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gain + c + 4));
-    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-    uint32_t q[4];
+  const int c = i * 16;
+  float v[16];
+  load8<IN_BF16>(x, src * d + c, v);
+  load8<IN_BF16>(x, src * d + c + 8, v + 8);
+  uint32_t q[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ss = fmaf(v[e], v[e], ss);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) q[e] = pack_bf16x2(v[2 * e] * g[2 * e], v[2 * e + 1] * g[2 * e + 1]);
-    *reinterpret_cast<uint4*>(out + (long long)r * d + c) = make_uint4(q[0], q[1], q[2], q[3]);
-    if (copy_f32) {
-      float4* o = reinterpret_cast<float4*>(copy_f32 + (long long)r * d + c);
-      o[0] = make_float4(v[0], v[1], v[2], v[3]);
-      o[1] = make_float4(v[4], v[5], v[6], v[7]);
-    }
+  for (int e = 0; e < 4; ++e) {
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c) + e);
+    q[2 * e] = pack_bf16x2(v[4 * e] * g.x, v[4 * e + 1] * g.y);
+    q[2 * e + 1] = pack_bf16x2(v[4 * e + 2] * g.z, v[4 * e + 3] * g.w);
   }
-  ssq[p * ld + r] = ss;
+  uint4* o = reinterpret_cast<uint4*>(out + (long long)r * d + c);
+  o[0] = make_uint4(q[0], q[1], q[2], q[3]);
+  o[1] = make_uint4(q[4], q[5], q[6], q[7]);
+  if (copy_f32) {
+    float4* h = reinterpret_cast<float4*>(copy_f32 + (long long)r * d + c);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+  }
+  // the tile's sum of squares in ascending column order: lane j continues lane j-1's sum
+  const int lane = threadIdx.x & 31, first = lane - j;
+  float ss = 0.f;
+  for (int st = 0; st < tpp; ++st) {
+    if (j == st) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) ss = fmaf(v[e], v[e], ss);
+    }
+    ss = __shfl_sync(0xffffffffu, ss, first + st);
+  }
+  if (j == 0) ssq[p * ld + r] = ss;
 }
 
 int norm_seed_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, int T, const float* gain,
                      bf16* out, float* copy_f32, float* ssq, long long ld, cudaStream_t stream) {
   if (M <= 0) return DS_OK;
-  if (T <= 0 || d % T || T % 8) return DS_ERR_INVALID;
+  if (T < 16 || T > 512 || T % 16 || d % T || d / 16 > 1024 || (32 % (T / 16) && (T / 16) % 32)) return DS_ERR_INVALID;
   count_launch();
   static const bool c0 = prefer_max_smem(norm_seed_kernel<true>) && prefer_max_smem(norm_seed_kernel<false>);
   (void)c0;
-  const long long threads = (long long)M * (d / T);
-  const dim3 grid((unsigned)((threads + NORM_THREADS - 1) / NORM_THREADS));
+  const dim3 block(d / 16);
   if (x_bf16)
-    return launch_status(launch_pdl(norm_seed_kernel<true>, grid, dim3(NORM_THREADS), 0, stream, x, gather, M, d, T,
-                                    gain, out, copy_f32, ssq, ld));
-  return launch_status(launch_pdl(norm_seed_kernel<false>, grid, dim3(NORM_THREADS), 0, stream, x, gather, M, d, T,
-                                  gain, out, copy_f32, ssq, ld));
+    return launch_status(launch_pdl(norm_seed_kernel<true>, dim3(M), block, 0, stream, x, gather, d, T, gain, out,
+                                    copy_f32, ssq, ld));
+  return launch_status(launch_pdl(norm_seed_kernel<false>, dim3(M), block, 0, stream, x, gather, d, T, gain, out,
+                                  copy_f32, ssq, ld));
 }
 
 int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int d, const float* gain, bf16* out,

@@ -115,3 +115,45 @@ def test_token_selective_properties_8k(big):
     full = P.partial_prefill(B, ids, P.RecomputeConfig.full(32), None)
     torch.cuda.synchronize()
     assert torch.equal(one.logits, full.logits)
+
+
+def test_short_recompute_orders_bit_identical_8k(big):
+    """Below the persistent anchor's threshold (k * P < 800 * L) the two-stream
+    call runs the per-launch anchor kernels beside the recompute: same results
+    as the single-stream call, reused K/V placed bit-exactly."""
+    P, cfg, A, B, ids, rc, prod = big
+    rc1 = P.RecomputeConfig([(31, 31)])
+    prod1 = P.full_prefill(A, ids, e_layers=rc1.transition_layers)
+    one = P.partial_prefill(B, ids, rc1, prod1.kv, prod1.e_map())
+    two = P.partial_prefill(B, ids, rc1, prod1.kv, prod1.e_map(), copy_stream=torch.cuda.Stream())
+    torch.cuda.synchronize()
+    assert torch.equal(one.logits, two.logits)
+    d = two.kv.dense()
+    assert torch.equal(d.k[:31, :, :N - 1], prod1.kv.k[:31, :, :N - 1])
+    assert torch.equal(d.v[:31, :, :N - 1], prod1.kv.v[:31, :, :N - 1])
+
+
+def test_persistent_anchor_placement_and_trace_8k(big):
+    """The co-resident anchor keeps one working CTA per SM (ds_anchor_placement),
+    and the stage trace orders the recompute's QKV events and ends with the logits."""
+    import ctypes as C
+    P, cfg, A, B, ids, rc, prod = big
+    from paper_2411_02820_b200 import _lib as L
+    from paper_2411_02820_b200.engine import _workspace
+    lib = L.lib()
+    s, side = torch.cuda.Stream(), torch.cuda.Stream()
+    ws = _workspace(B, N, s)
+    with torch.cuda.stream(s):
+        lib.ds_trace_begin()
+        P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), stream=s, copy_stream=side)
+        ms = (C.c_float * 256)()
+        tags = (C.c_int32 * 256)()
+        cnt = lib.ds_trace_end(ms, tags, 256)
+    torch.cuda.synchronize()
+    ev = {int(tags[i]): float(ms[i]) for i in range(cnt)}
+    qkv = [ev[1000 + l] for l in range(32 - K, 32)]
+    assert qkv == sorted(qkv) and ev[4000] >= qkv[-1] and ev[0] == 0.0
+    sm = (C.c_int32 * 1024)()
+    n = lib.ds_anchor_placement(C.byref(B.desc().dims), N, C.c_void_p(ws.data_ptr()), sm, 1024)
+    assert n == torch.cuda.get_device_properties(0).multi_processor_count
+    assert len(set(sm[i] for i in range(n))) >= n - 8  # packed CTAs (if any) leave; the rest hold distinct SMs
