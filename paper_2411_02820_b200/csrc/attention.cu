@@ -30,6 +30,55 @@ namespace ds {
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D).
 // ======================================================================
 
+
+// ---------------------------------------------------------------- packed softmax math
+// sm_100 issues two fp32 lanes per instruction (FFMA2 / FADD2) and a 3-input
+// max (FMNMX3): the softmax's non-MUFU work roughly halves.
+DS_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+DS_DEV float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+DS_DEV float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// 2^x for a pair on the FMA pipe (x <= ~2^8 here): round-to-nearest split
+// x = k + f, f in [-0.5, 0.5], 2^f by a degree-3 polynomial (rel. error < 7e-4,
+// below the bf16 rounding P gets anyway), k added into the exponent bits.
+// Takes a share of the exponentials off the MUFU pipe.
+DS_DEV float2 exp2_fma2(float2 x) {
+  const float2 shift = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float x0 = x.x, x1 = x.y;
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 j = fadd2(x, shift);
+  const float2 k = fadd2(j, make_float2(-12582912.f, -12582912.f));  // round(x)
+  const float2 f = ffma2(k, make_float2(-1.f, -1.f), x);               // x - round(x)
+  float2 p = make_float2(0.0555041087f, 0.0555041087f);
+  p = ffma2(p, f, make_float2(0.2402265070f, 0.2402265070f));
+  p = ffma2(p, f, make_float2(0.6931471806f, 0.6931471806f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  const int kx = __float_as_int(j.x) - 0x4B400000, ky = __float_as_int(j.y) - 0x4B400000;  // round(x) as int
+  // below 2^-126 (masked scores are -inf): exactly 0, as ex2.approx.ftz gives
+  return make_float2(x0 > -126.f ? __int_as_float(__float_as_int(p.x) + (kx << 23)) : 0.f,
+                     x1 > -126.f ? __int_as_float(__float_as_int(p.y) + (ky << 23)) : 0.f);
+}
+#ifndef DS_FA_EMU_MOD
+#define DS_FA_EMU_MOD 4  // one pair in DS_FA_EMU_MOD on the FMA pipe (0: all on MUFU)
+#endif
+
 constexpr int FA_BM = 128;
 constexpr int FA_BN = 128;
 constexpr int FA_THREADS = 320;
@@ -258,7 +307,8 @@ __global__ void __maxnreg__(136)
 #pragma unroll
       for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(sr[q]);
 #pragma unroll
-      for (int c = 8; c < FA_BN / 2; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+      for (int c = 8; c < FA_BN / 2; c += 2)
+        mx8[(c >> 1) & 7] = fmax3(mx8[(c >> 1) & 7], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
       tmem_ld32_nowait(tS, sr);
       tmem_ld32_nowait(tS + 32, sr + 32);
       tmem_wait_ld();
@@ -268,7 +318,8 @@ __global__ void __maxnreg__(136)
           if (kbase + c > qpos) sr[c] = __float_as_uint(-INFINITY);
       }
 #pragma unroll
-      for (int c = 0; c < FA_BN / 2; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(sr[c]));
+      for (int c = 0; c < FA_BN / 2; c += 2)
+        mx8[(c >> 1) & 7] = fmax3(mx8[(c >> 1) & 7], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
       const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const bool need = mt > m_used + thr;
@@ -293,17 +344,25 @@ __global__ void __maxnreg__(136)
         tmem_wait_st();
       }
       const float msc = m_used * sc;
-      float sum4[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums
-      uint32_t pk[FA_BN / 4];
+      float2 sum4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};  // independent partial sums
+      uint32_t pk[FA_BN / 8];
+      const float2 sc2 = make_float2(sc, sc), nmsc2 = make_float2(-msc, -msc);
+      auto expo = [&](int c, uint32_t s0, uint32_t s1) {
+        const float2 x = ffma2(make_float2(__uint_as_float(s0), __uint_as_float(s1)), sc2, nmsc2);
+        float2 p;
+        if (DS_FA_EMU_MOD && (c % (DS_FA_EMU_MOD > 0 ? DS_FA_EMU_MOD : 1)) == DS_FA_EMU_MOD - 1)
+          p = exp2_fma2(x);
+        else
+          p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+        sum4[c & 3] = fadd2(sum4[c & 3], p);
+        pk[c & 15] = pack_bf16x2(p.x, p.y);
+      };
       // pass 2: lower half from registers -> P columns [0, 32) (over consumed S)
 #pragma unroll
       for (int c = 0; c < FA_BN / 4; ++c) {
-        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * c]), sc, -msc));
-        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc));
-        sum4[c & 3] += p0 + p1;
-        pk[c] = pack_bf16x2(p0, p1);
+        expo(c, sr[2 * c], sr[2 * c + 1]);
+        if ((c & 15) == 15) tmem_st16_nowait(tS + (c & ~15), pk);  // P columns as they complete
       }
-      tmem_st32_nowait(tS, pk);
       // upper half re-read -> P columns [32, 64) (S columns 32..63 are consumed)
       tmem_ld32_nowait(tS + 64, sr);
       tmem_ld32_nowait(tS + 96, sr + 32);
@@ -315,13 +374,11 @@ __global__ void __maxnreg__(136)
       }
 #pragma unroll
       for (int c = 0; c < FA_BN / 4; ++c) {
-        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * c]), sc, -msc));
-        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * c + 1]), sc, -msc));
-        sum4[c & 3] += p0 + p1;
-        pk[c] = pack_bf16x2(p0, p1);
+        expo(c, sr[2 * c], sr[2 * c + 1]);
+        if ((c & 15) == 15) tmem_st16_nowait(tS + 32 + (c & ~15), pk);
       }
-      l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
-      tmem_st32_nowait(tS + 32, pk);
+      const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+      l += s2.x + s2.y;
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
