@@ -273,7 +273,7 @@ def run_ours(args, world, rank, local):
     lib = _lib.lib()
     pk = peaks()
     n, k = args.n, args.k
-    cfg = P.ModelConfig(max_seq=max(n, 8192), base_seed=0, mlp_kind=args.mlp, **dict(SHAPE, vocab_size=args.vocab))
+    cfg = P.ModelConfig(max_seq=max(n, 8192) + 64, base_seed=0, mlp_kind=args.mlp, **dict(SHAPE, vocab_size=args.vocab))
     L = cfg.n_layers
     dev = torch.device("cuda", local)
     A = P.random_model(cfg, seed=1000 + rank, device=dev)
@@ -403,6 +403,15 @@ def run_ours(args, world, rank, local):
         agree += int(mixed_i.token == own_i.token)
         agree_sel += int(sel_i.token == own_i.token)
         del prod_i, mixed_i, own_i, sel_i
+    # the reference's quality proxy (agreement_score, model.py:810-831): greedy
+    # decode over a 32-token horizon after the partial prefill vs the receiver's own
+    from paper_2411_02820_b200.quality import agreement_score
+    t0 = time.perf_counter()
+    ag = agreement_score(A, B, np.random.default_rng(100).integers(0, cfg.vocab_size, size=n, dtype=np.int64), rc,
+                         horizon=32)
+    torch.cuda.synchronize()
+    agreement = {"score": ag.score, "first_divergence": ag.first_divergence, "horizon": 32,
+                 "wall_s": round(time.perf_counter() - t0, 3)}
 
     # ---- per-kernel rooflines (CUDA events on the launching stream, same shapes as the step)
     Pn = n - 1
@@ -464,6 +473,7 @@ def run_ours(args, world, rank, local):
             "first_token": token,
             "first_token_agreement": {"partial_vs_own_full_prefill": agree, "prefixes": n_pref,
                                       "note": "random-init pair: B = A + noise on the recomputed suffix"},
+            "agreement_score": agreement,
             "gpu_launches": int(launches),
             "e2e": {"value": world * n / e2e_ttft, "unit": "tok/s", "ttft_p50_ms": e2e_ttft * 1e3,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * cfg.vocab_size + 4},

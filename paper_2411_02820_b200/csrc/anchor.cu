@@ -193,9 +193,24 @@ DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEM
   const bf16* wr[GEMV_ROWS];
 #pragma unroll
   for (int r = 0; r < GEMV_ROWS; ++r) wr[r] = a.W + (long long)gemv_row(a, t, r) * a.ldw;
-  float s[GEMV_ROWS];
+  // even / odd element partial sums per row on packed fp32 pairs; the chunk of
+  // x is unpacked once and serves all 8 rows
+  float2 s2[GEMV_ROWS];
 #pragma unroll
-  for (int r = 0; r < GEMV_ROWS; ++r) s[r] = 0.f;
+  for (int r = 0; r < GEMV_ROWS; ++r) s2[r] = make_float2(0.f, 0.f);
+  auto fma_chunk = [&](const uint4& w, const float2* xf, float2& acc) {
+    acc = ffma2(bf16x2_to_float2(w.x), xf[0], acc);
+    acc = ffma2(bf16x2_to_float2(w.y), xf[1], acc);
+    acc = ffma2(bf16x2_to_float2(w.z), xf[2], acc);
+    acc = ffma2(bf16x2_to_float2(w.w), xf[3], acc);
+  };
+  auto unpack_x = [&](int chunk, float2* xf) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(xs + chunk * 8);
+    xf[0] = bf16x2_to_float2(xv.x);
+    xf[1] = bf16x2_to_float2(xv.y);
+    xf[2] = bf16x2_to_float2(xv.z);
+    xf[3] = bf16x2_to_float2(xv.w);
+  };
   int c = tid;
   for (; c + (UNROLL - 1) * GEMV_THREADS < nchunk; c += UNROLL * GEMV_THREADS) {
     uint4 w[UNROLL][GEMV_ROWS];
@@ -205,16 +220,21 @@ DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEM
       for (int r = 0; r < GEMV_ROWS; ++r) w[u][r] = ld_stream16(wr[r] + (c + u * GEMV_THREADS) * 8);
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      const uint4 xv = *reinterpret_cast<const uint4*>(xs + (c + u * GEMV_THREADS) * 8);
+      float2 xf[4];
+      unpack_x(c + u * GEMV_THREADS, xf);
 #pragma unroll
-      for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(w[u][r], xv);
+      for (int r = 0; r < GEMV_ROWS; ++r) fma_chunk(w[u][r], xf, s2[r]);
     }
   }
   for (; c < nchunk; c += GEMV_THREADS) {
-    const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
+    float2 xf[4];
+    unpack_x(c, xf);
 #pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) s[r] += dot8(ld_stream16(wr[r] + c * 8), xv);
+    for (int r = 0; r < GEMV_ROWS; ++r) fma_chunk(ld_stream16(wr[r] + c * 8), xf, s2[r]);
   }
+  float s[GEMV_ROWS];
+#pragma unroll
+  for (int r = 0; r < GEMV_ROWS; ++r) s[r] = s2[r].x + s2[r].y;
 #pragma unroll
   for (int r = 0; r < GEMV_ROWS; ++r) {
 #pragma unroll

@@ -31,29 +31,6 @@ namespace ds {
 // ======================================================================
 
 
-// ---------------------------------------------------------------- packed softmax math
-// sm_100 issues two fp32 lanes per instruction (FFMA2 / FADD2) and a 3-input
-// max (FMNMX3): the softmax's non-MUFU work roughly halves.
-DS_DEV float2 ffma2(float2 a, float2 b, float2 c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&r);
-}
-DS_DEV float2 fadd2(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
-}
-DS_DEV float fmax3(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
 // 2^x for a pair on the FMA pipe (x <= ~2^8 here): round-to-nearest split
 // x = k + f, f in [-0.5, 0.5], 2^f by a degree-3 polynomial (rel. error < 7e-4,
 // below the bf16 rounding P gets anyway), k added into the exponent bits.
