@@ -116,12 +116,12 @@ enum { DS_TRACE_INGEST = 1, DS_TRACE_QKV = 1000, DS_TRACE_LAYER = 2000, DS_TRACE
 DS_API int ds_trace_begin(void);
 DS_API int ds_trace_end(float* ms_out, int32_t* tag_out, int32_t cap);
 /* SM id of each CTA of the last persistent anchor launch that used this
- * workspace (one CTA per SM is the design; profiling aid).  Returns the count. */
+ * workspace (one CTA per SM is the design; profiling aid).  Returns the count, or -1. */
 DS_API int ds_anchor_placement(const ds_dims* dims, int32_t n_tokens, const void* workspace, int32_t* sm_out,
                                int32_t cap);
 /* Global-timer ns of the last persistent anchor launch on this workspace: after
  * its seed, then after each of the 5 phases (qkv, attention, o-proj, w1, w2) of
- * every layer.  Returns the count (1 + 5 * n_layers). */
+ * every layer.  Returns the count (1 + 5 * n_layers), or -1. */
 DS_API int ds_anchor_timeline(const ds_dims* dims, int32_t n_tokens, const void* workspace, uint64_t* ns_out,
                               int32_t cap);
 

@@ -664,21 +664,22 @@ extern "C" {
 int ds_abi_version(void) { return DS_ABI_VERSION; }
 int ds_anchor_placement(const ds_dims* dims, int32_t n_tokens, const void* workspace, int32_t* sm_out, int32_t cap) {
   g_err.clear();
-  if (!dims || !workspace || !sm_out || n_tokens < 1) return fail(DS_ERR_INVALID, "bad placement arguments");
+  if (!dims || !workspace || !sm_out || n_tokens < 1) return fail(DS_ERR_INVALID, "bad placement arguments"), -1;
   Workspace w = carve(*dims, n_tokens, const_cast<void*>(workspace));
   const int n = num_sms() < cap ? num_sms() : cap;
   if (cudaMemcpy(sm_out, w.an_ctl + kMaxLayers + 2, 4ull * n, cudaMemcpyDeviceToHost) != cudaSuccess)
-    return cuda_fail("placement copy");
+    return cuda_fail("placement copy"), -1;
   return n;
 }
 
 int ds_anchor_timeline(const ds_dims* dims, int32_t n_tokens, const void* workspace, uint64_t* ns_out, int32_t cap) {
   g_err.clear();
-  if (!dims || !workspace || !ns_out || n_tokens < 1) return fail(DS_ERR_INVALID, "bad timeline arguments");
+  if (!dims || !workspace || !ns_out || n_tokens < 1) return fail(DS_ERR_INVALID, "bad timeline arguments"), -1;
   Workspace w = carve(*dims, n_tokens, const_cast<void*>(workspace));
   int n = 1 + 5 * dims->n_layers;
   if (n > cap) n = cap;
-  if (cudaMemcpy(ns_out, w.an_stamps, 8ull * n, cudaMemcpyDeviceToHost) != cudaSuccess) return cuda_fail("timeline copy");
+  if (cudaMemcpy(ns_out, w.an_stamps, 8ull * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return cuda_fail("timeline copy"), -1;
   return n;
 }
 

@@ -55,6 +55,12 @@ def test_host_only_entry_points(lib):
     with pytest.raises(ValueError):
         lib.check(rc)
     assert b"ingest" in L.ds_last_error()
+    # profiling aids: no events recorded -> empty trace; bad arguments -> -1
+    assert L.ds_trace_begin() == 0
+    assert L.ds_trace_end(None, None, 0) == 0
+    assert L.ds_anchor_placement(None, 8, None, None, 0) == -1
+    assert b"placement" in L.ds_last_error()
+    assert L.ds_anchor_timeline(ctypes.byref(dims), 0, None, None, 0) == -1
 
 
 def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
