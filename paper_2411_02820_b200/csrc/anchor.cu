@@ -147,26 +147,30 @@ DS_DEV void gemv_prefetch(const GemvArgs& a, int t) {
 }
 
 // Stage the input vector in shared memory as bf16 (RMSNorm fused when a.gain).
+// `sync`: a barrier over the 128 staging threads (default: the whole CTA).
+DS_DEV void cta_sync() { __syncthreads(); }
+template <void (*Sync)() = cta_sync>
 DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool active = tid < GEMV_THREADS;
   if (a.x_f32) {
     float inv = 1.f;
     if (a.gain) {
       float ss = 0.f;
-      for (int k = tid * 4; k < a.K; k += GEMV_THREADS * 4) {
+      for (int k = tid * 4; active && k < a.K; k += GEMV_THREADS * 4) {
         const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k));
         ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) ssq[warp] = ss;
-      __syncthreads();
+      if (lane == 0 && active) ssq[warp] = ss;
+      Sync();
       float t = 0.f;
 #pragma unroll
       for (int w = 0; w < GEMV_WARPS; ++w) t += ssq[w];
       inv = 1.0f / sqrtf(t / (float)a.K + 1e-6f);
     }
-    for (int k = tid * 4; k < a.K; k += GEMV_THREADS * 4) {
+    for (int k = tid * 4; active && k < a.K; k += GEMV_THREADS * 4) {
       const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k));
       const float4 g = a.gain ? __ldg(reinterpret_cast<const float4*>(a.gain + k)) : make_float4(1.f, 1.f, 1.f, 1.f);
       uint2 p;
@@ -175,10 +179,76 @@ DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
       *reinterpret_cast<uint2*>(xs + k) = p;
     }
   } else {
-    for (int k = tid * 8; k < a.K; k += GEMV_THREADS * 8)
+    for (int k = tid * 8; active && k < a.K; k += GEMV_THREADS * 8)
       *reinterpret_cast<uint4*>(xs + k) = ld_cg16(a.x_bf16 + k);
   }
-  __syncthreads();
+  Sync();
+}
+
+// The 128 accumulating threads' per-row pair sums -> row results (warp
+// shuffles, then the 4 warps in order) -> the fused epilogue.  `sync`: a
+// barrier over (at least) the 128 threads.
+template <typename Sync>
+DS_DEV void gemv_finish(const GemvArgs& a, int t, const float2* s2, float (*red)[GEMV_ROWS], unsigned long long& best,
+                        Sync sync) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float s[GEMV_ROWS];
+#pragma unroll
+  for (int r = 0; r < GEMV_ROWS; ++r) s[r] = s2[r].x + s2[r].y;
+#pragma unroll
+  for (int r = 0; r < GEMV_ROWS; ++r) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < GEMV_ROWS; ++r) red[warp][r] = s[r];
+  }
+  sync();
+  if (tid < GEMV_ROWS) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < GEMV_WARPS; ++w) v += red[w][tid];
+    red[0][tid] = v;  // only thread tid touches column tid
+  }
+  sync();
+  if (a.mode == EPI_QKV_ROPE) {
+    if (tid < 4) {
+      const int r0 = gemv_row(a, t, tid);
+      const int head = r0 / a.head_dim, j = r0 - head * a.head_dim, half = a.head_dim >> 1;
+      float lo = red[0][tid], hi = red[0][tid + 4];
+      const bool is_q = head < a.n_heads, is_k = !is_q && head < a.n_heads + a.n_kv_heads;
+      if (is_q || is_k) {
+        const float cs = a.rope_cos[(long long)a.pos * half + j], sn = a.rope_sin[(long long)a.pos * half + j];
+        const float x1 = lo, x2 = hi;
+        lo = x1 * cs - x2 * sn;
+        hi = x1 * sn + x2 * cs;
+      }
+      bf16* dst = is_q ? a.q_out + (long long)head * a.head_dim
+                       : (is_k ? a.kv.k + a.kv.off(head - a.n_heads, a.pos)
+                               : a.kv.v + a.kv.off(head - a.n_heads - a.n_kv_heads, a.pos));
+      dst[j] = __float2bfloat16_rn(lo);
+      dst[j + half] = __float2bfloat16_rn(hi);
+    }
+  } else if (a.mode == EPI_SWIGLU_BF16) {
+    if (tid < 4) {
+      const int o = (t >> 2) * 16 + (t & 3) * 4 + tid;
+      a.out_bf16[o] = __float2bfloat16_rn(silu(red[0][tid]) * red[0][tid + 4]);
+    }
+  } else if (tid < GEMV_ROWS) {
+    const int row = t * GEMV_ROWS + tid;
+    const float v = red[0][tid];
+    if (a.mode == EPI_RESID_F32) {
+      a.out_f32[row] = __ldcg(a.resid + row) + v;
+    } else if (a.mode == EPI_SILU_BF16) {
+      a.out_bf16[row] = __float2bfloat16_rn(silu(v));
+    } else {
+      a.out_f32[row] = v;
+      const unsigned long long p = pack_argmax(v, row);
+      best = p > best ? p : best;
+    }
+  }
+  sync();  // red[] reused by the next tile
 }
 
 // One tile of 8 weight rows against the staged x, with its epilogue.  UNROLL
@@ -232,63 +302,7 @@ DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEM
 #pragma unroll
     for (int r = 0; r < GEMV_ROWS; ++r) fma_chunk(ld_stream16(wr[r] + c * 8), xf, s2[r]);
   }
-  float s[GEMV_ROWS];
-#pragma unroll
-  for (int r = 0; r < GEMV_ROWS; ++r) s[r] = s2[r].x + s2[r].y;
-#pragma unroll
-  for (int r = 0; r < GEMV_ROWS; ++r) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) red[warp][r] = s[r];
-  }
-  __syncthreads();
-  if (tid < GEMV_ROWS) {
-    float v = 0.f;
-#pragma unroll
-    for (int w = 0; w < GEMV_WARPS; ++w) v += red[w][tid];
-    red[0][tid] = v;  // only thread tid touches column tid
-  }
-  __syncthreads();
-  if (a.mode == EPI_QKV_ROPE) {
-    if (tid < 4) {
-      const int r0 = gemv_row(a, t, tid);
-      const int head = r0 / a.head_dim, j = r0 - head * a.head_dim, half = a.head_dim >> 1;
-      float lo = red[0][tid], hi = red[0][tid + 4];
-      const bool is_q = head < a.n_heads, is_k = !is_q && head < a.n_heads + a.n_kv_heads;
-      if (is_q || is_k) {
-        const float cs = a.rope_cos[(long long)a.pos * half + j], sn = a.rope_sin[(long long)a.pos * half + j];
-        const float x1 = lo, x2 = hi;
-        lo = x1 * cs - x2 * sn;
-        hi = x1 * sn + x2 * cs;
-      }
-      bf16* dst = is_q ? a.q_out + (long long)head * a.head_dim
-                       : (is_k ? a.kv.k + a.kv.off(head - a.n_heads, a.pos)
-                               : a.kv.v + a.kv.off(head - a.n_heads - a.n_kv_heads, a.pos));
-      dst[j] = __float2bfloat16_rn(lo);
-      dst[j + half] = __float2bfloat16_rn(hi);
-    }
-  } else if (a.mode == EPI_SWIGLU_BF16) {
-    if (tid < 4) {
-      const int o = (t >> 2) * 16 + (t & 3) * 4 + tid;
-      a.out_bf16[o] = __float2bfloat16_rn(silu(red[0][tid]) * red[0][tid + 4]);
-    }
-  } else if (tid < GEMV_ROWS) {
-    const int row = t * GEMV_ROWS + tid;
-    const float v = red[0][tid];
-    if (a.mode == EPI_RESID_F32) {
-      a.out_f32[row] = __ldcg(a.resid + row) + v;
-    } else if (a.mode == EPI_SILU_BF16) {
-      a.out_bf16[row] = __float2bfloat16_rn(silu(v));
-    } else {
-      a.out_f32[row] = v;
-      const unsigned long long p = pack_argmax(v, row);
-      best = p > best ? p : best;
-    }
-  }
-  __syncthreads();  // red[] reused by the next tile
+  gemv_finish(a, t, s2, red, best, [] { __syncthreads(); });
 }
 
 // Every tile of one GEMV, strided over the grid; the next tile's weights are
@@ -328,6 +342,104 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------- TMA-staged stand-alone GEMV
+//
+// One CTA per SM: a producer warp streams each tile's 8 weight rows through a
+// shared-memory ring in K-slices of TMA_KS columns (`cp.async.bulk`, one
+// elected thread, complete_tx on the slot's mbarrier), so ~160 KB per SM are in
+// flight without a register per byte; the 4 consumer warps read the slices
+// from shared memory.  Thread t still accumulates its chunks c = t, t+128, ...
+// in ascending order and the reduction is gemv_finish, so the results are the
+// register-streaming gemv_tile's bit for bit.  Used alone (not beside the
+// recompute), for K a multiple of TMA_KS.
+constexpr int TMA_KS = 1024;                     // columns per ring slot (128 threads x 8)
+constexpr int TMA_SLOT = GEMV_ROWS * TMA_KS * 2;  // 16 KB
+constexpr int TMA_THREADS = GEMV_THREADS + 32;   // + producer warp
+
+DS_DEV void named_sync_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(GEMV_THREADS) : "memory"); }
+
+__global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, int slots) {
+  extern __shared__ __align__(128) uint8_t smem_dyn[];
+  uint8_t* ring = smem_dyn;
+  bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * TMA_SLOT);
+  __shared__ __align__(8) uint64_t full[16], empty[16];
+  __shared__ float red[GEMV_WARPS][GEMV_ROWS];
+  __shared__ float ssq[GEMV_WARPS];
+  const int tid = threadIdx.x;
+  const int tiles = a.N / GEMV_ROWS, ks = a.K / TMA_KS;
+  if (tid == GEMV_THREADS) {
+    for (int i = 0; i < slots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], GEMV_WARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  if (tid >= GEMV_THREADS) {
+    // producer: weights never depend on the predecessor -- start before the PDL wait
+    if (tid == GEMV_THREADS) {
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int s = 0; s < ks; ++s) {
+          mbar_wait(&empty[slot], phase ^ 1);
+          mbar_expect_tx(&full[slot], TMA_SLOT);
+#pragma unroll
+          for (int r = 0; r < GEMV_ROWS; ++r)
+            bulk_g2s(ring + slot * TMA_SLOT + r * TMA_KS * 2,
+                     a.W + (long long)gemv_row(a, t, r) * a.ldw + (long long)s * TMA_KS, TMA_KS * 2, &full[slot]);
+          if (++slot == slots) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+    }
+    return;
+  }
+  pdl_wait();
+  gemv_stage_x<named_sync_consumers>(a, xs, ssq);
+  int slot = 0;
+  uint32_t phase = 0;
+  unsigned long long best = 0ull;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    float2 s2[GEMV_ROWS];
+#pragma unroll
+    for (int r = 0; r < GEMV_ROWS; ++r) s2[r] = make_float2(0.f, 0.f);
+    for (int s = 0; s < ks; ++s) {
+      mbar_wait(&full[slot], phase);
+      const int c = s * (TMA_KS / 8) + tid;  // this thread's chunk in the slice
+      const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
+      const float2 xf[4] = {bf16x2_to_float2(xv.x), bf16x2_to_float2(xv.y), bf16x2_to_float2(xv.z),
+                            bf16x2_to_float2(xv.w)};
+#pragma unroll
+      for (int r = 0; r < GEMV_ROWS; ++r) {
+        const uint4 w = *reinterpret_cast<const uint4*>(ring + slot * TMA_SLOT + r * TMA_KS * 2 + tid * 16);
+        s2[r] = ffma2(bf16x2_to_float2(w.x), xf[0], s2[r]);
+        s2[r] = ffma2(bf16x2_to_float2(w.y), xf[1], s2[r]);
+        s2[r] = ffma2(bf16x2_to_float2(w.z), xf[2], s2[r]);
+        s2[r] = ffma2(bf16x2_to_float2(w.w), xf[3], s2[r]);
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+      if (++slot == slots) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+    gemv_finish(a, t, s2, red, best, [] { named_sync_consumers(); });
+  }
+  if (a.mode == EPI_STORE_F32 && a.argmax && tid < GEMV_ROWS) {
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0x000000ffu, best, o);
+      best = other > best ? other : best;
+    }
+    if (tid == 0 && best) atomicMax(a.argmax, best);
+  }
+}
+
 __global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t* token, int64_t* token64) {
   const int32_t t = (int32_t)(0xFFFFFFFFu - (uint32_t)(*packed & 0xFFFFFFFFull));
   if (token) *token = t;
@@ -349,9 +461,41 @@ int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaSt
   return launch_status();
 }
 
+static int gemv_tma_launch(const GemvArgs& a, cudaStream_t stream) {
+  const int xbytes = (a.K * 2 + 127) & ~127;
+  int slots = (200 * 1024 - xbytes) / TMA_SLOT;
+  slots = slots > 16 ? 16 : slots;
+  if (slots < 4) return DS_ERR_INVALID;
+  const int smem = slots * TMA_SLOT + xbytes;
+  static int attr = 0;
+  if (smem > attr) {
+    if (int rc_ = launch_status(cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)))
+      return rc_;
+    attr = smem;
+  }
+  static const bool c0 = prefer_max_smem(gemv_tma_kernel);
+  (void)c0;
+  const int tiles = a.N / GEMV_ROWS;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  count_launch();
+  return launch_status(launch_pdl(gemv_tma_kernel, dim3(grid), dim3(TMA_THREADS), smem, stream, a, slots));
+}
+
+// DS_GEMV_TMA=0: the register-streaming kernel for every stand-alone GEMV (A/B).
+static bool gemv_tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_GEMV_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
   if ((a.N % GEMV_ROWS) || (a.K & 7) || (a.mode == EPI_SWIGLU_BF16 && a.N % 32)) return DS_ERR_INVALID;
   if (a.mode == EPI_QKV_ROPE && (a.head_dim % 8 || a.N % a.head_dim)) return DS_ERR_INVALID;
+  if (gemv_tma_enabled() && a.K % TMA_KS == 0 && a.N / GEMV_ROWS >= 148)
+    if (gemv_tma_launch(a, stream) == DS_OK) return DS_OK;
   const int tiles = a.N / GEMV_ROWS;
   const int smem = a.K * 2;
   static int attr = 0;
@@ -756,10 +900,10 @@ __global__ void __maxnreg__(88) anchor_persistent_kernel(const __grid_constant__
   const int hd = a.n_heads * D, kvd = a.n_kv_heads * D;
   const bool swiglu = a.mlp_kind == DS_MLP_SWIGLU;
   const int n_items = a.n_kv_heads * a.splits;
-  // One working CTA per SM: a CTA that finds another of this grid on its SM
-  // (the scheduler packed them onto an idle SM) leaves after the first
-  // barrier, so the SM's resources go back to the other stream's GEMM / FA;
-  // the work is spread over the CTAs that stay (rank / nranks).
+  // At most per_sm working CTAs per SM (1 beside the recompute, 4 alone): a
+  // CTA that finds the SM already full (the scheduler packed CTAs onto an idle
+  // SM) leaves after the first barrier, so the SM's resources go back to the
+  // other stream's GEMM / FA; the work is spread over the CTAs that stay.
   __shared__ int s_rank;
   __shared__ unsigned int s_nranks;
   unsigned int gen = 0;
@@ -768,8 +912,8 @@ __global__ void __maxnreg__(88) anchor_persistent_kernel(const __grid_constant__
     gen = ld_acquire_u32(a.bar + 1);
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     a.bar[2 + blockIdx.x] = smid;  // placement record (ds_anchor_placement)
-    const bool first = atomicAdd(a.claim + (smid & (kAnchorClaimSlots - 1)), 1u) == 0u;
-    s_rank = first ? (int)atomicAdd(a.n_active, 1u) : -1;
+    const bool keep = atomicAdd(a.claim + (smid & (kAnchorClaimSlots - 1)), 1u) < (unsigned)a.per_sm;
+    s_rank = keep ? (int)atomicAdd(a.n_active, 1u) : -1;
   }
   grid_sync(a.bar, gen, gridDim.x);
   const int rank = s_rank;
@@ -918,9 +1062,9 @@ int anchor_persistent_smem(const ds_dims& d, int n_keys) {
 // Largest dynamic shared memory that still lets the kernel share an SM with
 // a tcgen05 GEMM or flash-attention CTA (each ~198.9 KB incl. its reservation).
 constexpr int kAnchorSmemMax = 32 * 1024;
-// Alone on the GPU: more than half an SM's shared memory, so the scheduler
-// cannot pack two CTAs onto one SM (the grid is one CTA per SM).
-constexpr int kAnchorSmemAlone = 120 * 1024;
+// Alone on the GPU: 4 CTAs per SM (16 warps), so the weight streams are not
+// latency-bound; same work split per rank, same results.
+constexpr int kAnchorAlonePerSm = 4;
 
 bool anchor_persistent_fits(const ds_dims& d, int n_keys) {
   if (d.n_kv_heads < 1) return false;
@@ -934,13 +1078,13 @@ static cudaError_t anchor_launch_t(const AnchorArgs& a, int smem, cudaStream_t s
   auto kern = anchor_persistent_kernel<D, R>;
   static bool init = false;
   if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAnchorSmemAlone);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAnchorSmemMax);
     if (e != cudaSuccess) return e;
     prefer_max_smem(kern);
     init = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(num_sms());
+  cfg.gridDim = dim3(num_sms() * a.per_sm);
   cfg.blockDim = dim3(GEMV_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -962,9 +1106,9 @@ int anchor_persistent_launch(AnchorArgs a, cudaStream_t stream, bool co_resident
   d.head_dim = D;
   d.d_model = a.d_model;
   d.d_ff = a.d_ff;
-  int smem = anchor_persistent_smem(d, a.pos + 1);
+  const int smem = anchor_persistent_smem(d, a.pos + 1);
   if (smem > kAnchorSmemMax) return DS_ERR_INVALID;
-  if (!co_resident) smem = kAnchorSmemAlone;
+  a.per_sm = co_resident ? 1 : kAnchorAlonePerSm;
   a.split_keys = attn_split_keys(a.pos + 1, a.n_kv_heads, R);
   a.splits = (a.pos + 1 + a.split_keys - 1) / a.split_keys;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)D));

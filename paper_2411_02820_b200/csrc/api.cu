@@ -516,11 +516,21 @@ int zero_anchor_ctl(Ctx& c, cudaStream_t s) {
 int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* token,
                 const AnchorPlan* plan = nullptr, int64_t* token64 = nullptr) {
   const ds_dims& d = c.d;
-  // The persistent kernel is the shape for running beside the recompute; alone,
-  // one 4-warp CTA per SM is latency-bound, so the per-launch kernels (up to 16
-  // GEMV CTAs per SM) run the pass -- same device functions, same results.
-  if (plan && plan->co_resident && anchor_persistent_fits(d, P + 1)) {
-    if (!plan->ctl_zeroed)
+  // The persistent kernel runs the pass beside the recompute (one CTA per SM).
+  // Alone, the per-launch kernels are faster (PDL-chained, TMA-staged GEMVs:
+  // 4.05 ms vs 4.94 ms for the persistent kernel at four CTAs per SM, whose 592
+  // grid barriers and uneven tile counts cost more than the kernel boundaries);
+  // DS_ANCHOR_ALONE=persistent selects it for measurements.  Same device
+  // functions everywhere, same results.
+  static int alone_persistent = -1;
+  if (alone_persistent < 0) {
+    const char* e = getenv("DS_ANCHOR_ALONE");
+    alone_persistent = (e && e[0] == 'p') ? 1 : 0;
+  }
+  const bool co = plan && plan->co_resident;
+  const bool alone = !(plan && plan->wait_for) && !co && alone_persistent;
+  if ((co || alone) && anchor_persistent_fits(d, P + 1)) {
+    if (!(plan && plan->ctl_zeroed))
       if (int rc = zero_anchor_ctl(c, c.s)) return rc;
     DS_TRY(anchor_persistent(c, token_id, P, plan), "anchor");
     trace(c.s, DS_TRACE_ANCHOR + d.n_layers - 1);

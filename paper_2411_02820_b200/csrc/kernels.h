@@ -204,7 +204,8 @@ struct AnchorArgs {
   unsigned int* bar;         // [2] grid barrier (count zero), then [gridDim] SM id of each CTA
   unsigned long long* stamps;  // [1 + 5 * n_layers] global ns after the seed and each phase (rank 0)
   unsigned int* claim;       // [kAnchorClaimSlots] CTAs seen per SM id, zero
-  unsigned int* n_active;    // [1] working CTAs (one per SM), zero
+  unsigned int* n_active;    // [1] working CTAs, zero
+  int per_sm;                // working CTAs per SM (set by the launcher)
   int splits, split_keys;    // set by the launcher
   float scale_log2;
 };
