@@ -575,6 +575,7 @@ DS_DEV void attn_prefetch(const AttnArgs& a, int item, int D) {
     const int key = k0 + (p >> 1) * 32;
     int cnt = min(32, k0 + nk - key);
     if (key < a.n_lo && key + cnt > a.n_lo) cnt = a.n_lo - key;
+    if (key < a.n_lo && a.lo_remote) continue;  // peer memory: plain loads only
     prefetch_l2(attn_row(a, p & 1, g, key), (uint32_t)cnt * D * 2);
   }
 }
@@ -970,6 +971,7 @@ __global__ void __maxnreg__(88) anchor_persistent_kernel(const __grid_constant__
       t.lo = W.src;
       t.hi = W.dst;
       t.copy_lo = W.copy;
+      t.lo_remote = W.src_remote;
       t.n_lo = a.pos;
       t.n_keys = a.pos + 1;
       t.n_heads = a.n_heads;

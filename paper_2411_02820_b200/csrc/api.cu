@@ -305,6 +305,17 @@ int window_layer(Ctx& c, int l, int rows, bool kv_only, const int32_t* row_pos =
 }
 
 // The single anchor row at position `pos` through layer l (_layer_single, model.py:547-562).
+// A producer export on another GPU (DS_FORCE_REMOTE=1 treats every sender as
+// remote: single-GPU validation of that path).
+bool sender_is_remote(const void* p) {
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("DS_FORCE_REMOTE");
+    force = (e && e[0] == '1') ? 1 : 0;
+  }
+  return force || !ptr_on_this_device(p);
+}
+
 // sender (optional): keys 0..pos-1 are read from the producer's export and
 // copied into the consumer cache as they are read (the fused KV ingest).
 int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender = nullptr) {
@@ -334,6 +345,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   at.lo = sender ? layer_addr(*sender, l, d.head_dim) : ka;
   at.hi = ka;
   at.copy_lo = sender ? 1 : 0;
+  at.lo_remote = sender && sender_is_remote(at.lo.k) ? 1 : 0;
   at.n_lo = pos;
   at.n_keys = pos + 1;
   at.n_heads = d.n_heads;
@@ -473,6 +485,7 @@ int anchor_persistent(Ctx& c, const int64_t* token_id, int P, const AnchorPlan* 
     const bool from_sender = plan && plan->sender && plan->reused && plan->reused[l];
     al.src = from_sender ? layer_addr(*plan->sender, l, d.head_dim) : al.dst;
     al.copy = from_sender ? 1 : 0;
+    al.src_remote = from_sender && sender_is_remote(al.src.k) ? 1 : 0;
     al.wait = plan ? plan->wait[l] : 0u;
   }
   A.n_layers = d.n_layers;

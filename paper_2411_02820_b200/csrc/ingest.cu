@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(PEER_THREADS) kv_ingest_peer_kernel(const __gr
   }
 }
 
-static bool on_this_device(const void* p) {
+bool ptr_on_this_device(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
@@ -160,7 +160,7 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   const int stage_bytes = kPage * head_dim * 2;
   // DS_INGEST_PEER_KERNEL=1 forces the peer-source kernel (single-GPU validation of that path)
   static const bool force_peer = getenv("DS_INGEST_PEER_KERNEL") && atoi(getenv("DS_INGEST_PEER_KERNEL"));
-  if (force_peer || !on_this_device(a.src_k[0])) {
+  if (force_peer || !ptr_on_this_device(a.src_k[0])) {
     const long long units = (long long)n_layers * 2 * n_kv_heads * a.n_pages;
     const int cpu = stage_bytes / 16;
     long long grid = (units * cpu + 4LL * PEER_THREADS - 1) / (4LL * PEER_THREADS);

@@ -107,6 +107,9 @@ int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int 
 unsigned int gemm_done_target(int M, int N);
 int gemm_col_tile(int M, int N);  // output columns per epilogue tile (the ssq partial granularity)
 
+// False when p is device memory of another GPU (a peer export mapped through
+// CUDA IPC / peer access): kernels then read it with plain loads only.
+bool ptr_on_this_device(const void* p);
 int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32_t* layers_host, int n_layers,
                      int n_kv_heads, int head_dim, int window, cudaStream_t stream, bool background = false);
 
@@ -160,6 +163,7 @@ struct AttnArgs {
   const bf16* q;  // [H*D], RoPE applied
   KvAddr lo, hi;
   int copy_lo;
+  int lo_remote;             // lo is a peer GPU's memory: no bulk L2 prefetch of its rows
   int n_lo, n_keys, n_heads, n_kv_heads;
   int splits, split_keys;    // set by the launcher
   float* part_o;             // [H][splits][D]
@@ -185,6 +189,7 @@ struct AnchorLayer {
   KvAddr dst;         // the consumer cache layer (the anchor's own key goes here)
   unsigned int wait;  // > 0: GemmEpi::done arrivals to wait for before the attention
   int copy;           // store the src rows into dst while reading them (fused ingest)
+  int src_remote;     // src lives on a peer GPU (plain loads only)
 };
 struct AnchorArgs {
   AnchorLayer layer[kMaxLayers];
