@@ -1,0 +1,47 @@
+"""The persistent co-resident anchor on shapes other than the 8B headline.
+
+At n = 4096 with two of eight layers recomputed (k * P >= 800 * L) the
+two-stream call runs the persistent anchor beside the recompute; the
+single-stream call runs the per-launch anchor kernels.  Both use the same
+device functions, so logits and caches must agree bit for bit -- for the
+ungated and SwiGLU MLPs, GQA ratios 4 and 8, and head_dim 128 and 64.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+N = 4096
+SHAPES = [
+    dict(n_layers=8, d_model=1024, n_heads=8, n_kv_heads=2, head_dim=128, d_ff=2816, vocab_size=4096),
+    dict(n_layers=8, d_model=1024, n_heads=8, n_kv_heads=1, head_dim=128, d_ff=2816, vocab_size=4096,
+         mlp_kind="swiglu"),
+    dict(n_layers=8, d_model=1024, n_heads=16, n_kv_heads=4, head_dim=64, d_ff=2816, vocab_size=4096),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=["ungated-r4-d128", "swiglu-r8-d128", "ungated-r4-d64"])
+def test_persistent_anchor_matches_per_launch(shape):
+    import paper_2411_02820_b200 as P
+    cfg = P.ModelConfig(max_seq=N + 64, base_seed=0, **shape)
+    A = P.random_model(cfg, seed=5)
+    B = P.random_model(cfg, seed=6, base=A, perturb_layers=range(6, 8), eps=0.5)
+    ids = np.random.default_rng(9).integers(0, cfg.vocab_size, size=N, dtype=np.int64)
+    rc = P.RecomputeConfig([(6, 7)])
+    prod = P.full_prefill(A, ids, e_layers=rc.transition_layers)
+    one = P.partial_prefill(B, ids, rc, prod.kv, prod.e_map())
+    two = P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), copy_stream=torch.cuda.Stream())
+    torch.cuda.synchronize()
+    assert torch.isfinite(one.logits).all()
+    assert torch.equal(one.logits, two.logits)
+    d1, d2 = one.kv.dense(), two.kv.dense()
+    assert torch.equal(d1.k, d2.k) and torch.equal(d1.v, d2.v)
+    # reused layers placed bit-exactly by the anchor's fused copy
+    assert torch.equal(d2.k[:6, :, :N - 1], prod.kv.k[:6, :, :N - 1])
+    # recompute-all through the persistent path == the full prefill (same structure)
+    full = P.full_prefill(B, ids, e_layers=(), copy_stream=torch.cuda.Stream())
+    mixed = P.partial_prefill(B, ids, P.RecomputeConfig.full(8), None, copy_stream=torch.cuda.Stream())
+    torch.cuda.synchronize()
+    assert torch.equal(full.logits, mixed.logits)
