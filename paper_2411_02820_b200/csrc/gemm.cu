@@ -58,6 +58,15 @@ DS_DEV float row_inv_rms(const GemmEpi& e, int row, bool row_ok) {
   return 1.0f / sqrtf(t / (float)e.norm_dim + 1e-6f);
 }
 
+// Epilogue warps: bring this thread's row of the tile's f32 residual into L2
+// while the tile's mainloop runs, so the residual epilogue's loads hit L2.
+template <int BN>
+DS_DEV void prefetch_resid(const GemmEpi& e, int row, int nb) {
+  if (e.mode != EPI_RESID_F32 || row >= e.M) return;
+  const int col0 = nb * BN, ncols = min(BN, e.N - col0);
+  if (ncols > 0) prefetch_l2(e.resid + (long long)row * e.ld_resid + col0, (uint32_t)ncols * 4);
+}
+
 template <int BN>
 DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
   const bool row_ok = row < e.M;
@@ -128,24 +137,22 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
     return;
   }
   if (e.mode == EPI_RESID_F32) {
-    // f32 residual add, 16 columns per step with the residual loads of the next
-    // two steps already in flight (the residual stream comes from HBM)
+    // f32 residual add, 16 columns per step with the next step's residual
+    // loads in flight (the residual stream comes from HBM; a third buffer
+    // spilled once the folded-RMSNorm outputs joined this epilogue)
     const int ncols = min(BN, e.N - col0);  // multiple of 16
     const float4* r = reinterpret_cast<const float4*>(e.resid + (long long)row * e.ld_resid + col0);
     float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long long)row * e.ld_out + col0);
-    float4 r0[4], r1[4], r2[4];
+    float4 r0[4], r1[4];
     if (row_ok) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        r0[i] = r[i];
-        if (ncols > 16) r1[i] = r[4 + i];
-      }
+      for (int i = 0; i < 4; ++i) r0[i] = r[i];
     }
     float ss = 0.f;
     for (int c = 0; c < ncols; c += 16) {
-      if (row_ok && c + 32 < ncols) {
+      if (row_ok && c + 16 < ncols) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) r2[i] = r[(c + 32) / 4 + i];
+        for (int i = 0; i < 4; ++i) r1[i] = r[(c + 16) / 4 + i];
       }
       float v[16];
       tmem_ld16(tbase + c, v);
@@ -174,10 +181,7 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        r0[i] = r1[i];
-        r1[i] = r2[i];
-      }
+      for (int i = 0; i < 4; ++i) r0[i] = r1[i];
     }
     if (e.ssq_out && row_ok) e.ssq_out[nb * e.ld_ssq + row] = ss;
     return;
@@ -345,6 +349,7 @@ __global__ void __maxnreg__(128)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, num_m, num_n, epi.group, mb, nb);
+      prefetch_resid<BN>(epi, mb * GEMM_BM + quarter * 32 + lane, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
@@ -557,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
     for (int t = pair; t < num_tiles; t += n_pairs) {
       int mb, nb;
       tile_coords(t, num_m, num_n, epi.group, mb, nb);
+      prefetch_resid<PAIR_BN>(epi, mb * 2 * GEMM_BM + (int)rank * GEMM_BM + quarter * 32 + lane, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * PAIR_BN;

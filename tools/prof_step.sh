@@ -13,3 +13,5 @@ timeout 900 $NCU -k regex:gemm_tc2 -c 4 -o $OUT/prof_gemm python tools/profile_s
 timeout 600 $NCU -k regex:fa_tc -c 1 -o $OUT/prof_fa python tools/profile_step.py --what partial > $OUT/ncu_fa.log 2>&1
 timeout 600 $NCU -k regex:anchor_persistent -c 1 -o $OUT/prof_anchor python tools/profile_step.py --what partial > $OUT/ncu_anchor.log 2>&1
 ls -la $OUT
+# the stand-alone anchor kernels (single stream): TMA-staged GEMV and split-KV attention
+timeout 600 $NCU -k regex:"gemv_tma|attn_decode" -c 5 -o $OUT/prof_anchor_launch python tools/profile_step.py --what partial --single > $OUT/ncu_anchor_launch.log 2>&1
