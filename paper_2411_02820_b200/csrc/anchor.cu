@@ -491,10 +491,14 @@ static bool gemv_tma_enabled() {
   return v == 1;
 }
 
-int gemv_launch(const GemvArgs& a, cudaStream_t stream) {
+// staged: the TMA-staged kernel may serve the call.  It wins inside the PDL
+// chain of the per-launch anchor (its producer streams weights before the
+// predecessor finishes); a GEMV that starts cold (the lm head after the
+// persistent anchor) is faster on the register-streaming kernel (177 vs 243 us).
+int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged) {
   if ((a.N % GEMV_ROWS) || (a.K & 7) || (a.mode == EPI_SWIGLU_BF16 && a.N % 32)) return DS_ERR_INVALID;
   if (a.mode == EPI_QKV_ROPE && (a.head_dim % 8 || a.N % a.head_dim)) return DS_ERR_INVALID;
-  if (gemv_tma_enabled() && a.K % TMA_KS == 0 && a.N / GEMV_ROWS >= 148)
+  if (staged && gemv_tma_enabled() && a.K % TMA_KS == 0 && a.N / GEMV_ROWS >= 148)
     if (gemv_tma_launch(a, stream) == DS_OK) return DS_OK;
   const int tiles = a.N / GEMV_ROWS;
   const int smem = a.K * 2;

@@ -403,7 +403,7 @@ int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token, int64_t* to
   g.mode = EPI_STORE_F32;
   g.out_f32 = logits;
   g.argmax = c.w.argmax;
-  DS_TRY(gemv_launch(g, c.s), "lm head");
+  DS_TRY(gemv_launch(g, c.s, /*staged=*/false), "lm head");
   if (token || token64) DS_TRY(argmax_finalize_launch(c.w.argmax, token, token64, c.s), "argmax");
   return DS_OK;
 }

@@ -152,7 +152,7 @@ struct GemvArgs {
   unsigned long long* argmax;  // EPI_STORE_F32: packed (orderable value, ~index) max
 };
 
-int gemv_launch(const GemvArgs& a, cudaStream_t stream);
+int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged = true);
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream);
 int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaStream_t stream);
 
