@@ -318,7 +318,10 @@ bool sender_is_remote(const void* p) {
 
 // sender (optional): keys 0..pos-1 are read from the producer's export and
 // copied into the consumer cache as they are read (the fused KV ingest).
-int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender = nullptr) {
+// wait (optional): an event the attention waits for (the layer's window K/V on
+// another stream); the QKV GEMV before it does not depend on it.
+int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender = nullptr,
+                 cudaEvent_t wait = nullptr) {
   const ds_dims& d = c.d;
   const ds_layer_weights& W = c.m->layers[l];
   const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
@@ -339,6 +342,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   g.rope_cos = c.m->rope_cos;
   g.rope_sin = c.m->rope_sin;
   DS_TRY(gemv_launch(g, c.s), "anchor qkv");
+  if (wait && cudaStreamWaitEvent(c.s, wait, 0) != cudaSuccess) return cuda_fail("wait");
   const KvAddr ka = g.kv;
   AttnArgs at{};
   at.q = c.w.q_a;
@@ -465,6 +469,8 @@ struct AnchorPlan {
   const cudaEvent_t* wait_for = nullptr;  // per-launch path: per-layer events to wait for
   bool ctl_zeroed = false;              // the caller zeroed the control block in stream order
   bool co_resident = false;             // runs beside the recompute (small footprint); else one CTA per SM forced
+  int persistent_layers = -1;           // co-resident: layers the persistent kernel runs (the rest per-launch)
+  const cudaEvent_t* layer_event = nullptr;  // per-launch tail: per-layer QKV events of the compute stream
 };
 
 // The whole anchor pass as one persistent kernel (anchor.cu).
@@ -488,7 +494,7 @@ int anchor_persistent(Ctx& c, const int64_t* token_id, int P, const AnchorPlan* 
     al.src_remote = from_sender && sender_is_remote(al.src.k) ? 1 : 0;
     al.wait = plan ? plan->wait[l] : 0u;
   }
-  A.n_layers = d.n_layers;
+  A.n_layers = (plan && plan->persistent_layers >= 0) ? plan->persistent_layers : d.n_layers;
   A.d_model = d.d_model;
   A.n_heads = d.n_heads;
   A.n_kv_heads = d.n_kv_heads;
@@ -546,7 +552,16 @@ int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* 
     if (!(plan && plan->ctl_zeroed))
       if (int rc = zero_anchor_ctl(c, c.s)) return rc;
     DS_TRY(anchor_persistent(c, token_id, P, plan), "anchor");
-    trace(c.s, DS_TRACE_ANCHOR + d.n_layers - 1);
+    const int done_layers = (plan && plan->persistent_layers >= 0) ? plan->persistent_layers : d.n_layers;
+    trace(c.s, DS_TRACE_ANCHOR + done_layers - 1);
+    // the tail layers on the per-launch kernels (whole SMs once the recompute is done)
+    for (int l = done_layers; l < d.n_layers; ++l) {
+      const bool from_sender = plan && plan->sender && plan->reused && plan->reused[l];
+      const cudaEvent_t ev = (plan && plan->layer_event && !from_sender) ? plan->layer_event[l] : nullptr;
+      int rc = anchor_layer(c, l, P, c.w.h_a, from_sender ? plan->sender : nullptr, ev);
+      if (rc) return rc;
+      trace(c.s, DS_TRACE_ANCHOR + l);
+    }
   } else {
     if (int rc = reset_counters(c)) return rc;
     DS_TRY(rmsnorm_launch(c.m->embed, true, token_id, 1, d.d_model, c.m->layers[0].g_attn, c.w.a_a, c.w.h_a, nullptr,
@@ -653,6 +668,12 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
       for (int l = groups[2 * i]; l <= groups[2 * i + 1]; ++l)
         plan.wait[l] = gemm_done_target(P, l == groups[2 * i + 1] ? 2 * kvd : hd + 2 * kvd);
     c.qkv_done = w.an_ctl;
+    // the last layer's anchor runs per-launch once the recompute is done
+    if (covered[L - 1] && L > 1) {
+      plan.persistent_layers = L - 1;
+      plan.layer_event = ev_layer;
+      c.layer_ready = ev_layer;
+    }
     // The anchor launches once the first QKV GEMM's CTAs (PDL-launched while
     // the seed kernel drains) hold every SM: its CTAs then land one per SM,
     // beside them, instead of packing onto idle SMs.
