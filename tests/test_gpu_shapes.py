@@ -45,3 +45,26 @@ def test_persistent_anchor_matches_per_launch(shape):
     mixed = P.partial_prefill(B, ids, P.RecomputeConfig.full(8), None, copy_stream=torch.cuda.Stream())
     torch.cuda.synchronize()
     assert torch.equal(full.logits, mixed.logits)
+
+
+@pytest.mark.parametrize("groups", [[(0, 1), (5, 6)], [(2, 3), (6, 7)]], ids=["from-embeddings", "two-transitions"])
+def test_persistent_anchor_multi_group(groups):
+    """Several recompute groups (one seeded from the embeddings, one ending before
+    the last layer): the persistent anchor waits on each group's layers and the
+    results equal the single-stream order bit for bit."""
+    import paper_2411_02820_b200 as P
+    cfg = P.ModelConfig(max_seq=N + 64, base_seed=0, **SHAPES[0])
+    A = P.random_model(cfg, seed=7)
+    B = P.random_model(cfg, seed=8, base=A, perturb_layers=[l for a, b in groups for l in range(a, b + 1)], eps=0.5)
+    ids = np.random.default_rng(11).integers(0, cfg.vocab_size, size=N, dtype=np.int64)
+    rc = P.RecomputeConfig(groups)
+    prod = P.full_prefill(A, ids, e_layers=rc.transition_layers)
+    one = P.partial_prefill(B, ids, rc, prod.kv, prod.e_map())
+    two = P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), copy_stream=torch.cuda.Stream())
+    torch.cuda.synchronize()
+    assert torch.equal(one.logits, two.logits)
+    d1, d2 = one.kv.dense(), two.kv.dense()
+    assert torch.equal(d1.k, d2.k) and torch.equal(d1.v, d2.v)
+    reused = [l for l in range(8) if not any(a <= l <= b for a, b in groups)]
+    for l in reused:
+        assert torch.equal(d2.k[l, :, :N - 1], prod.kv.k[l, :, :N - 1])
