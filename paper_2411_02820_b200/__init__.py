@@ -20,7 +20,7 @@ from .engine import (
     token_selective_prefill,
     workspace_bytes,
 )
-from .planner import CostModel, ScheduledRequest, estimate_ttft, plan
+from .planner import AdaptDecision, CostModel, ScheduledRequest, SloPolicy, adapt_config, estimate_ttft, plan
 from .selection import (build_frontier, enumerate_groups, load_profile, save_profile, select_by_layer_budget,
                         select_by_quality_floor)
 from .store import CacheKey, CacheStore, FetchedKV, KVSlice, context_hash, fetch_context_caches, store_prefill
@@ -34,7 +34,7 @@ __all__ = [
     "ModelConfig", "ModelWeights", "PagedKV", "PerturbationSpec", "PrefillResult", "RecomputeConfig",
     "SchemaError", "build_model", "check_tokens", "full_prefill", "make_synthetic_dataset", "model_ident",
     "partial_prefill", "random_model", "token_selective_prefill", "reference_weights", "workspace_bytes",
-    "CostModel", "ScheduledRequest", "estimate_ttft", "plan", "build_frontier", "enumerate_groups", "load_profile",
+    "AdaptDecision", "CostModel", "ScheduledRequest", "SloPolicy", "adapt_config", "estimate_ttft", "plan", "build_frontier", "enumerate_groups", "load_profile",
     "save_profile", "select_by_layer_budget", "select_by_quality_floor", "CacheKey", "CacheStore", "FetchedKV",
     "KVSlice", "context_hash", "fetch_context_caches", "store_prefill",
 ]

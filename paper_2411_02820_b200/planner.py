@@ -8,6 +8,7 @@ at a time, the anchor closes a request.
     bytes_of                             sched.py:115-123
     plan("naive"|"reuse_only"|"pipelined") sched.py:185-276
     estimate_ttft                        sched.py:279-281
+    SloPolicy, AdaptDecision, adapt_config   sim.py:84-104, 171-202
     demo_scenario                        sched.py:358-369 (Fig. 9: totals 47 / 30 / 17)
 
 The pipelined plan fixes the ORDER the GPU scheduler
@@ -235,3 +236,53 @@ def demo_scenario():
         ScheduledRequest("A", 0.0, "A", RecomputeConfig([(3, 9)]), 10),
         ScheduledRequest("B", 2.0, "B", RecomputeConfig([(0, 2)]), 10),
     ]
+
+
+# ---------------------------------------------------------------------------
+# SLO-adaptive recompute-set choice (sim.py:84-104, 171-202)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class SloPolicy:
+    slo: float
+    q_min: float
+    adaptation_enabled: bool = True
+
+    def __post_init__(self) -> None:
+        if self.slo <= 0:
+            raise ValueError("slo must be positive")
+        if not 0.0 <= self.q_min <= 1.0:
+            raise ValueError("q_min must lie in [0, 1]")
+
+
+@dataclass(frozen=True)
+class AdaptDecision:
+    config: RecomputeConfig
+    k: int
+    quality: float
+    slo_feasible: bool
+
+
+def adapt_config(queue_depth: int, request: ScheduledRequest, frontier, policy: SloPolicy,
+                 cost: CostModel) -> AdaptDecision:
+    """Pick a Pareto-frontier entry for one request given the replica's backlog
+    (sim.py:171-202).  Candidates: entries meeting q_min (else the terminal
+    recompute-all entry).  Loaded (queue_depth > 0) or adaptation off: the
+    cheapest candidate.  Idle: the largest candidate whose solitary pipelined
+    TTFT (estimate_ttft) fits the SLO, else the cheapest, flagged infeasible.
+    With ``CostModel.from_measured`` the TTFTs are the B200's measured times."""
+    qualifying = [e for e in frontier.entries if e.quality >= policy.q_min]
+    if not qualifying:
+        qualifying = [frontier.entries[-1]]
+    if not policy.adaptation_enabled or queue_depth > 0:
+        chosen = qualifying[0]
+        return AdaptDecision(chosen.config, chosen.k, chosen.quality, True)
+    best = None
+    for entry in qualifying:
+        trial = ScheduledRequest(request.id, 0.0, request.model, entry.config, request.n_layers)
+        if estimate_ttft(trial, cost) <= policy.slo:
+            best = entry  # entries ascend in k: the last fit is the largest
+    if best is not None:
+        return AdaptDecision(best.config, best.k, best.quality, True)
+    chosen = qualifying[0]
+    return AdaptDecision(chosen.config, chosen.k, chosen.quality, False)

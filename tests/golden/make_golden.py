@@ -25,6 +25,7 @@ sys.path.insert(0, REF)
 from crosskv import model as M  # noqa: E402
 from crosskv import profiler as PR  # noqa: E402
 from crosskv import sched as S  # noqa: E402
+from crosskv import sim as SIM  # noqa: E402
 from crosskv import store as ST  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -224,6 +225,41 @@ def sched_fixtures():
     (OUT / "sched.json").write_text(json.dumps(out, indent=0, sort_keys=True) + "\n")
 
 
+def adapt_fixtures():
+    """sim.adapt_config (sim.py:171-202) on random frontiers, policies, backlogs
+    and cost models: the SLO-adaptive recompute-set choice."""
+    rng = np.random.default_rng(77)
+    cases = []
+    for _ in range(80):
+        L = int(rng.integers(4, 13))
+        g = int(rng.integers(1, 3))
+        pts = []
+        for cfg in PR.enumerate_groups(L, g):
+            pts.append({"groups": [list(x) for x in cfg.groups], "k": cfg.recomputed_layer_count,
+                        "quality": 1.0 if cfg.is_full(L) else round(float(rng.uniform(0, 1)), 4)})
+        points = [PR.ProfilePoint(M.RecomputeConfig(p["groups"]), p["k"], p["quality"]) for p in pts]
+        frontier = PR.build_frontier(points)
+        if rng.random() < 0.5:
+            cost = S.CostModel.unit()
+        else:
+            cost = S.CostModel(link_bandwidth=float(rng.uniform(0.5, 8.0)), kv_layer_bytes=float(rng.uniform(0.5, 4.0)),
+                               e_layer_bytes=float(rng.uniform(0.5, 8.0)),
+                               layer_compute_time=float(rng.uniform(0.2, 3.0)),
+                               anchor_time=float(rng.uniform(0.0, 1.0)))
+        policy = SIM.SloPolicy(slo=float(rng.uniform(0.5, 40.0)), q_min=float(rng.uniform(0, 1)),
+                               adaptation_enabled=bool(rng.random() < 0.8))
+        qd = int(rng.integers(0, 3)) if rng.random() < 0.4 else 0
+        req = S.ScheduledRequest("r0", 0.0, "m0", M.RecomputeConfig.full(L), L)
+        dec = SIM.adapt_config(qd, req, frontier, policy, cost)
+        cases.append({"L": L, "points": pts,
+                      "cost": [cost.link_bandwidth, cost.kv_layer_bytes, cost.e_layer_bytes,
+                               cost.layer_compute_time, cost.anchor_time, cost.unit_mode],
+                      "policy": [policy.slo, policy.q_min, policy.adaptation_enabled], "queue_depth": qd,
+                      "decision": {"groups": [list(x) for x in dec.config.groups], "k": dec.k,
+                                   "quality": dec.quality, "slo_feasible": dec.slo_feasible}})
+    (OUT / "adapt.json").write_text(json.dumps({"cases": cases}, indent=0, sort_keys=True) + "\n")
+
+
 def store_fixtures():
     """Serving-mode filter and fetch assembly on TOY (store.py:199-221, 351-395)."""
     toy = SHAPES["toy"]
@@ -282,7 +318,7 @@ def selective_fixtures():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["config", "sched", "store", "engine", "profile", "selective"]
+    which = sys.argv[1:] or ["config", "sched", "store", "engine", "profile", "selective", "adapt"]
     if "config" in which:
         config_and_hash_fixtures()
     if "sched" in which:
@@ -295,4 +331,6 @@ if __name__ == "__main__":
         profile_fixtures()
     if "selective" in which:
         selective_fixtures()
+    if "adapt" in which:
+        adapt_fixtures()
     print("wrote", sorted(p.name for p in OUT.iterdir() if p.suffix in (".npz", ".json")))

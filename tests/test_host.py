@@ -288,3 +288,30 @@ def test_snapshot_index_matches_reference(toy_prefill, tmp_path):
     (tmp_path / "index.json").write_text(json.dumps(idx))
     with pytest.raises(P.SchemaError):
         ST.CacheStore.load_snapshot(tmp_path, cfg, device="cpu")
+
+
+def test_adapt_config_golden():
+    """SLO-adaptive choice over the Pareto frontier (sim.py:171-202): same
+    decision as the reference on 80 random frontiers / policies / backlogs."""
+    doc = json.loads((GOLDEN / "adapt.json").read_text())
+    largest_pick = 0
+    for case in doc["cases"]:
+        L = case["L"]
+        pts = [SEL.ProfilePoint(P.RecomputeConfig(p["groups"]), p["k"], p["quality"]) for p in case["points"]]
+        fr = SEL.build_frontier(pts)
+        bw, kvb, eb, lct, at, unit = case["cost"]
+        cost = S.CostModel.unit() if unit else S.CostModel(link_bandwidth=bw, kv_layer_bytes=kvb, e_layer_bytes=eb,
+                                                           layer_compute_time=lct, anchor_time=at)
+        slo, qmin, on = case["policy"]
+        req = S.ScheduledRequest("r0", 0.0, "m0", P.RecomputeConfig.full(L), L)
+        dec = S.adapt_config(case["queue_depth"], req, fr, S.SloPolicy(slo, qmin, on), cost)
+        want = case["decision"]
+        assert [list(g) for g in dec.config.groups] == want["groups"]
+        assert (dec.k, dec.quality, dec.slo_feasible) == (want["k"], want["quality"], want["slo_feasible"])
+        largest_pick += dec.k > min(e.k for e in fr.entries if e.quality >= qmin) if any(
+            e.quality >= qmin for e in fr.entries) else 0
+    assert largest_pick > 0  # the idle path that trades latency for quality is exercised
+    with pytest.raises(ValueError):
+        S.SloPolicy(0.0, 0.5)
+    with pytest.raises(ValueError):
+        S.SloPolicy(1.0, 1.5)
