@@ -36,21 +36,19 @@ namespace ds {
 // below the bf16 rounding P gets anyway), k added into the exponent bits.
 // Takes a share of the exponentials off the MUFU pipe.
 DS_DEV float2 exp2_fma2(float2 x) {
-  const float2 shift = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
-  const float x0 = x.x, x1 = x.y;
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 j = fadd2(x, shift);
+  // j = x + 1.5*2^23 puts round(x) in j's low mantissa bits; since
+  // 0x4B400000 << 23 == 0 (mod 2^32), (bits(j) << 23) is round(x) moved into the
+  // exponent field: one shift-add per element inserts it into 2^f.
+  const float2 j = fadd2(x, make_float2(12582912.f, 12582912.f));
   const float2 k = fadd2(j, make_float2(-12582912.f, -12582912.f));  // round(x)
-  const float2 f = ffma2(k, make_float2(-1.f, -1.f), x);               // x - round(x)
-  float2 p = make_float2(0.0555041087f, 0.0555041087f);
-  p = ffma2(p, f, make_float2(0.2402265070f, 0.2402265070f));
+  const float2 f = ffma2(k, make_float2(-1.f, -1.f), x);               // x - round(x), in [-0.5, 0.5]
+  float2 p = ffma2(make_float2(0.0555041087f, 0.0555041087f), f, make_float2(0.2402265070f, 0.2402265070f));
   p = ffma2(p, f, make_float2(0.6931471806f, 0.6931471806f));
   p = ffma2(p, f, make_float2(1.f, 1.f));
-  const int kx = __float_as_int(j.x) - 0x4B400000, ky = __float_as_int(j.y) - 0x4B400000;  // round(x) as int
+  const float rx = __int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23));
+  const float ry = __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23));
   // below 2^-126 (masked scores are -inf): exactly 0, as ex2.approx.ftz gives
-  return make_float2(x0 > -126.f ? __int_as_float(__float_as_int(p.x) + (kx << 23)) : 0.f,
-                     x1 > -126.f ? __int_as_float(__float_as_int(p.y) + (ky << 23)) : 0.f);
+  return make_float2(x.x > -126.f ? rx : 0.f, x.y > -126.f ? ry : 0.f);
 }
 #ifndef DS_FA_EMU_MOD
 #define DS_FA_EMU_MOD 4  // one pair in DS_FA_EMU_MOD on the FMA pipe (0: all on MUFU)
