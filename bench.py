@@ -448,6 +448,24 @@ def run_ours(args, world, rank, local):
     agreement = {"score": ag.score, "first_divergence": ag.first_divergence, "horizon": 32,
                  "wall_s": round(time.perf_counter() - t0, 3)}
 
+    # ---- greedy decode after the partial prefill (f1: decode_greedy, model.py:751-788):
+    # each token is one anchor pass over the paged cache (every weight + every
+    # layer's K/V once), timed with events over 32 steps
+    from paper_2411_02820_b200.quality import decode_greedy
+    dsteps = 32
+    dcache = P.PagedKV.allocate(cfg, n + dsteps, dev)
+    dstream = torch.cuda.Stream(device=dev)  # its own workspace: the captured step's stays untouched
+    with torch.cuda.stream(dstream):
+        dres = P.partial_prefill(B, ids, rc, prod.kv, e_map, out=dcache, stream=dstream, tokens_dev=tok_dev)
+        decode_greedy(B, dcache, dres, steps=dsteps + 1)  # warm-up (workspace sized for the run)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(dstream)
+        decode_greedy(B, dcache, dres, steps=dsteps + 1)
+        e1.record(dstream)
+    torch.cuda.synchronize()
+    dec_ms = e0.elapsed_time(e1) / dsteps
+    del dcache, dres
+
     # ---- per-kernel rooflines (CUDA events on the launching stream, same shapes as the step)
     Pn = n - 1
     d, F, HD, KVD = cfg.d_model, cfg.d_ff, cfg.n_heads * cfg.head_dim, cfg.n_kv_heads * cfg.head_dim
@@ -524,6 +542,10 @@ def run_ours(args, world, rank, local):
             "first_token_agreement": {"partial_vs_own_full_prefill": agree, "prefixes": n_pref,
                                       "note": "random-init pair: B = A + noise on the recomputed suffix"},
             "agreement_score": agreement,
+            "decode": {"steps": dsteps, "context": n, "ms_per_token": dec_ms, "tok_s": 1e3 / dec_ms,
+                       "gbs": kern["anchor_pass"]["bytes"] / dec_ms / 1e6,
+                       "note": "greedy decode after the partial prefill, one anchor pass per token; "
+                               "the token stream is copied to the host once, at the end"},
             "gpu_launches": int(launches),
             "e2e": {"value": world * n / e2e_ttft, "unit": "tok/s", "ttft_p50_ms": e2e_ttft * 1e3,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * cfg.vocab_size + 4},

@@ -188,9 +188,31 @@ DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
 // The 128 accumulating threads' per-row pair sums -> row results (warp
 // shuffles, then the 4 warps in order) -> the fused epilogue.  `sync`: a
 // barrier over (at least) the 128 threads.
+// The epilogue's own global inputs for tile t (RoPE cos/sin of the row pair,
+// the residual of the row), loaded by threads 0..7 when the tile starts so
+// their latency hides under the weight stream instead of following it.
+struct EpiPre {
+  float a, b;
+};
+DS_DEV EpiPre gemv_epi_pre(const GemvArgs& a, int t) {
+  EpiPre e{0.f, 0.f};
+  const int tid = threadIdx.x;
+  if (a.mode == EPI_QKV_ROPE) {
+    if (tid < 4) {
+      const int r0 = gemv_row(a, t, tid);
+      const int half = a.head_dim >> 1, j = r0 % a.head_dim;
+      e.a = __ldg(a.rope_cos + (long long)a.pos * half + j);
+      e.b = __ldg(a.rope_sin + (long long)a.pos * half + j);
+    }
+  } else if (a.mode == EPI_RESID_F32) {
+    if (tid < GEMV_ROWS) e.a = __ldcg(a.resid + t * GEMV_ROWS + tid);
+  }
+  return e;
+}
+
 template <typename Sync>
 DS_DEV void gemv_finish(const GemvArgs& a, int t, const float2* s2, float (*red)[GEMV_ROWS], unsigned long long& best,
-                        Sync sync) {
+                        const EpiPre& pre, Sync sync) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   float s[GEMV_ROWS];
 #pragma unroll
@@ -219,7 +241,7 @@ DS_DEV void gemv_finish(const GemvArgs& a, int t, const float2* s2, float (*red)
       float lo = red[0][tid], hi = red[0][tid + 4];
       const bool is_q = head < a.n_heads, is_k = !is_q && head < a.n_heads + a.n_kv_heads;
       if (is_q || is_k) {
-        const float cs = a.rope_cos[(long long)a.pos * half + j], sn = a.rope_sin[(long long)a.pos * half + j];
+        const float cs = pre.a, sn = pre.b;
         const float x1 = lo, x2 = hi;
         lo = x1 * cs - x2 * sn;
         hi = x1 * sn + x2 * cs;
@@ -239,7 +261,7 @@ DS_DEV void gemv_finish(const GemvArgs& a, int t, const float2* s2, float (*red)
     const int row = t * GEMV_ROWS + tid;
     const float v = red[0][tid];
     if (a.mode == EPI_RESID_F32) {
-      a.out_f32[row] = __ldcg(a.resid + row) + v;
+      a.out_f32[row] = pre.a + v;
     } else if (a.mode == EPI_SILU_BF16) {
       a.out_bf16[row] = __float2bfloat16_rn(silu(v));
     } else {
@@ -265,6 +287,7 @@ DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEM
   for (int r = 0; r < GEMV_ROWS; ++r) wr[r] = a.W + (long long)gemv_row(a, t, r) * a.ldw;
   // even / odd element partial sums per row on packed fp32 pairs; the chunk of
   // x is unpacked once and serves all 8 rows
+  const EpiPre pre = gemv_epi_pre(a, t);
   float2 s2[GEMV_ROWS];
 #pragma unroll
   for (int r = 0; r < GEMV_ROWS; ++r) s2[r] = make_float2(0.f, 0.f);
@@ -302,7 +325,7 @@ DS_DEV void gemv_tile(const GemvArgs& a, int t, const bf16* xs, float (*red)[GEM
 #pragma unroll
     for (int r = 0; r < GEMV_ROWS; ++r) fma_chunk(ld_stream16(wr[r] + c * 8), xf, s2[r]);
   }
-  gemv_finish(a, t, s2, red, best, [] { __syncthreads(); });
+  gemv_finish(a, t, s2, red, best, pre, [] { __syncthreads(); });
 }
 
 // Every tile of one GEMV, strided over the grid; the next tile's weights are
@@ -346,28 +369,32 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_kernel(GemvArgs a) {
 // ---------------------------------------------------------------- TMA-staged stand-alone GEMV
 //
 // One CTA per SM: a producer warp streams each tile's 8 weight rows through a
-// shared-memory ring in K-slices of TMA_KS columns (`cp.async.bulk`, one
+// shared-memory ring in K-slices of KS columns (`cp.async.bulk`, one
 // elected thread, complete_tx on the slot's mbarrier), so ~160 KB per SM are in
 // flight without a register per byte; the 4 consumer warps read the slices
 // from shared memory.  Thread t still accumulates its chunks c = t, t+128, ...
 // in ascending order and the reduction is gemv_finish, so the results are the
 // register-streaming gemv_tile's bit for bit.  Used alone (not beside the
-// recompute), for K a multiple of TMA_KS.
-constexpr int TMA_KS = 1024;                     // columns per ring slot (128 threads x 8)
-constexpr int TMA_SLOT = GEMV_ROWS * TMA_KS * 2;  // 16 KB
+// recompute), for K a multiple of 1024.
 constexpr int TMA_THREADS = GEMV_THREADS + 32;   // + producer warp
 
 DS_DEV void named_sync_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(GEMV_THREADS) : "memory"); }
 
+// KS: columns per ring slot (a multiple of 128 threads x 8); each row's slice
+// is one bulk copy of KS*2 bytes.  Thread t's chunks stay t, t+128, ... in
+// ascending order for every KS.
+template <int KS>
 __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, int slots) {
+  constexpr int SLOT = GEMV_ROWS * KS * 2;
+  constexpr int CPT = KS / (GEMV_THREADS * 8);  // chunks per thread per slot
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* ring = smem_dyn;
-  bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * TMA_SLOT);
+  bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * SLOT);
   __shared__ __align__(8) uint64_t full[16], empty[16];
   __shared__ float red[GEMV_WARPS][GEMV_ROWS];
   __shared__ float ssq[GEMV_WARPS];
   const int tid = threadIdx.x;
-  const int tiles = a.N / GEMV_ROWS, ks = a.K / TMA_KS;
+  const int tiles = a.N / GEMV_ROWS, ks = a.K / KS;
   if (tid == GEMV_THREADS) {
     for (int i = 0; i < slots; ++i) {
       mbar_init(&full[i], 1);
@@ -385,11 +412,11 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, in
       for (int t = blockIdx.x; t < tiles; t += gridDim.x)
         for (int s = 0; s < ks; ++s) {
           mbar_wait(&empty[slot], phase ^ 1);
-          mbar_expect_tx(&full[slot], TMA_SLOT);
+          mbar_expect_tx(&full[slot], SLOT);
 #pragma unroll
           for (int r = 0; r < GEMV_ROWS; ++r)
-            bulk_g2s(ring + slot * TMA_SLOT + r * TMA_KS * 2,
-                     a.W + (long long)gemv_row(a, t, r) * a.ldw + (long long)s * TMA_KS, TMA_KS * 2, &full[slot]);
+            bulk_g2s(ring + slot * SLOT + r * KS * 2, a.W + (long long)gemv_row(a, t, r) * a.ldw + (long long)s * KS,
+                     KS * 2, &full[slot]);
           if (++slot == slots) {
             slot = 0;
             phase ^= 1;
@@ -404,22 +431,27 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, in
   uint32_t phase = 0;
   unsigned long long best = 0ull;
   for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const EpiPre pre = gemv_epi_pre(a, t);
     float2 s2[GEMV_ROWS];
 #pragma unroll
     for (int r = 0; r < GEMV_ROWS; ++r) s2[r] = make_float2(0.f, 0.f);
     for (int s = 0; s < ks; ++s) {
       mbar_wait(&full[slot], phase);
-      const int c = s * (TMA_KS / 8) + tid;  // this thread's chunk in the slice
-      const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
-      const float2 xf[4] = {bf16x2_to_float2(xv.x), bf16x2_to_float2(xv.y), bf16x2_to_float2(xv.z),
-                            bf16x2_to_float2(xv.w)};
 #pragma unroll
-      for (int r = 0; r < GEMV_ROWS; ++r) {
-        const uint4 w = *reinterpret_cast<const uint4*>(ring + slot * TMA_SLOT + r * TMA_KS * 2 + tid * 16);
-        s2[r] = ffma2(bf16x2_to_float2(w.x), xf[0], s2[r]);
-        s2[r] = ffma2(bf16x2_to_float2(w.y), xf[1], s2[r]);
-        s2[r] = ffma2(bf16x2_to_float2(w.z), xf[2], s2[r]);
-        s2[r] = ffma2(bf16x2_to_float2(w.w), xf[3], s2[r]);
+      for (int cc = 0; cc < CPT; ++cc) {
+        const int c = s * (KS / 8) + cc * GEMV_THREADS + tid;  // this thread's chunk
+        const uint4 xv = *reinterpret_cast<const uint4*>(xs + c * 8);
+        const float2 xf[4] = {bf16x2_to_float2(xv.x), bf16x2_to_float2(xv.y), bf16x2_to_float2(xv.z),
+                              bf16x2_to_float2(xv.w)};
+#pragma unroll
+        for (int r = 0; r < GEMV_ROWS; ++r) {
+          const uint4 w =
+              *reinterpret_cast<const uint4*>(ring + slot * SLOT + r * KS * 2 + (cc * GEMV_THREADS + tid) * 16);
+          s2[r] = ffma2(bf16x2_to_float2(w.x), xf[0], s2[r]);
+          s2[r] = ffma2(bf16x2_to_float2(w.y), xf[1], s2[r]);
+          s2[r] = ffma2(bf16x2_to_float2(w.z), xf[2], s2[r]);
+          s2[r] = ffma2(bf16x2_to_float2(w.w), xf[3], s2[r]);
+        }
       }
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
@@ -428,7 +460,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, in
         phase ^= 1;
       }
     }
-    gemv_finish(a, t, s2, red, best, [] { named_sync_consumers(); });
+    gemv_finish(a, t, s2, red, best, pre, [] { named_sync_consumers(); });
   }
   if (a.mode == EPI_STORE_F32 && a.argmax && tid < GEMV_ROWS) {
 #pragma unroll
@@ -461,24 +493,43 @@ int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaSt
   return launch_status();
 }
 
-static int gemv_tma_launch(const GemvArgs& a, cudaStream_t stream) {
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+template <int KS>
+static int gemv_tma_launch_t(const GemvArgs& a, cudaStream_t stream, int ctas_per_sm) {
+  constexpr int SLOT = GEMV_ROWS * KS * 2;
   const int xbytes = (a.K * 2 + 127) & ~127;
-  int slots = (200 * 1024 - xbytes) / TMA_SLOT;
+  static const int budget = env_int("DS_GEMV_SMEM_KB", 200) * 1024;  // experiments
+  int slots = (budget / ctas_per_sm - xbytes) / SLOT;
   slots = slots > 16 ? 16 : slots;
-  if (slots < 4) return DS_ERR_INVALID;
-  const int smem = slots * TMA_SLOT + xbytes;
+  if (slots < 2) return DS_ERR_INVALID;
+  const int smem = slots * SLOT + xbytes;
+  auto kern = gemv_tma_kernel<KS>;
   static int attr = 0;
   if (smem > attr) {
-    if (int rc_ = launch_status(cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)))
+    if (int rc_ = launch_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)))
       return rc_;
     attr = smem;
   }
-  static const bool c0 = prefer_max_smem(gemv_tma_kernel);
+  static const bool c0 = prefer_max_smem(kern);
   (void)c0;
-  const int tiles = a.N / GEMV_ROWS;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int tiles = a.N / GEMV_ROWS, cap = num_sms() * ctas_per_sm;
+  const int grid = tiles < cap ? tiles : cap;
   count_launch();
-  return launch_status(launch_pdl(gemv_tma_kernel, dim3(grid), dim3(TMA_THREADS), smem, stream, a, slots));
+  return launch_status(launch_pdl(kern, dim3(grid), dim3(TMA_THREADS), smem, stream, a, slots));
+}
+
+// Slice width and CTAs per SM (DS_GEMV_KS, DS_GEMV_TMA_CTAS: experiments).
+static int gemv_tma_launch(const GemvArgs& a, cudaStream_t stream) {
+  static const int ks_max = env_int("DS_GEMV_KS", 4096);
+  static const int ctas = env_int("DS_GEMV_TMA_CTAS", 1) < 1 ? 1 : env_int("DS_GEMV_TMA_CTAS", 1);
+  if (ks_max >= 4096 && a.K % 4096 == 0) return gemv_tma_launch_t<4096>(a, stream, ctas);
+  if (ks_max >= 2048 && a.K % 2048 == 0) return gemv_tma_launch_t<2048>(a, stream, ctas);
+  if (a.K % 1024 == 0) return gemv_tma_launch_t<1024>(a, stream, ctas);
+  return DS_ERR_INVALID;
 }
 
 // DS_GEMV_TMA=0: the register-streaming kernel for every stand-alone GEMV (A/B).
@@ -491,14 +542,14 @@ static bool gemv_tma_enabled() {
   return v == 1;
 }
 
-// staged: the TMA-staged kernel may serve the call.  It wins inside the PDL
-// chain of the per-launch anchor (its producer streams weights before the
-// predecessor finishes); a GEMV that starts cold (the lm head after the
-// persistent anchor) is faster on the register-streaming kernel (177 vs 243 us).
+// staged: the TMA-staged kernel may serve the call (K a multiple of 1024, at
+// least one tile per SM).  With one bulk copy per 8 KB row slice it streams
+// faster than the register kernel (stand-alone anchor 2.79 vs 4.30 ms); with
+// 2 KB copies it did not (the bulk-copy count, not the bytes, was the limit).
 int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged) {
   if ((a.N % GEMV_ROWS) || (a.K & 7) || (a.mode == EPI_SWIGLU_BF16 && a.N % 32)) return DS_ERR_INVALID;
   if (a.mode == EPI_QKV_ROPE && (a.head_dim % 8 || a.N % a.head_dim)) return DS_ERR_INVALID;
-  if (staged && gemv_tma_enabled() && a.K % TMA_KS == 0 && a.N / GEMV_ROWS >= 148)
+  if (staged && gemv_tma_enabled() && a.K % 1024 == 0 && a.N / GEMV_ROWS >= 148)
     if (gemv_tma_launch(a, stream) == DS_OK) return DS_OK;
   const int tiles = a.N / GEMV_ROWS;
   const int smem = a.K * 2;
@@ -584,6 +635,130 @@ DS_DEV void attn_prefetch(const AttnArgs& a, int item, int D) {
   }
 }
 
+// Softmax of each head over the item's nk scores (log2 domain, in place):
+// stat = (max, sum) per head.
+template <int R>
+DS_DEV void attn_softmax(int nk, int sk, float* sc, float* stat) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < R; r += ATT_THREADS / 32) {
+    float m = -INFINITY;
+    for (int i = lane; i < nk; i += 32) m = fmaxf(m, sc[r * sk + i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.f;
+    for (int i = lane; i < nk; i += 32) {
+      const float e = exp2f(sc[r * sk + i] - m);
+      sc[r * sk + i] = e;
+      l += e;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) {
+      stat[2 * r] = m;
+      stat[2 * r + 1] = l;
+    }
+  }
+}
+
+// P.V partials of one thread (lane = (dim chunk, key stream)): reduce the key
+// streams with shuffles, store the item's unnormalised output.
+template <int D, int R>
+DS_DEV void attn_store_part(const AttnArgs& a, int g, int s, float (*acc)[8]) {
+  constexpr int CPW = D / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cw = lane % CPW, st = lane / CPW, chunk = warp * CPW + cw;
+#pragma unroll
+  for (int o = CPW; o < 32; o <<= 1)
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[r][e] += __shfl_xor_sync(0xffffffffu, acc[r][e], o);
+  if (st == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float4* po = reinterpret_cast<float4*>(a.part_o + ((long long)(g * R + r) * a.splits + s) * D + chunk * 8);
+      __stcg(po, make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
+      __stcg(po + 1, make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]));
+    }
+  }
+}
+
+// The item's (m, l); the last CTA of kv head g merges every split.
+// `sync`: a barrier over the CTA's 128 compute threads.
+template <int D, int R, typename Sync>
+DS_DEV void attn_finish(const AttnArgs& a, int g, int s, float* sc, const float* stat, unsigned int* is_last,
+                        Sync sync) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < R) {
+    float* ml = a.part_ml + ((long long)(g * R + tid) * a.splits + s) * 2;
+    __stcg(ml, stat[2 * tid]);
+    __stcg(ml + 1, stat[2 * tid + 1]);
+  }
+  // ---- the last CTA of this kv head merges every split (threadfence reduction)
+  __threadfence();
+  sync();
+  if (tid == 0) *is_last = (atomicAdd(a.counters + g, 1u) == (unsigned)a.splits - 1);
+  sync();
+  if (*is_last) {
+    __threadfence();
+    float* wts = sc;  // [R][splits] then den[R]
+    float* den = wts + R * a.splits;
+    for (int r = warp; r < R; r += ATT_THREADS / 32) {
+      const float* ml = a.part_ml + (long long)(g * R + r) * a.splits * 2;
+      float M = -INFINITY;
+      for (int s2 = lane; s2 < a.splits; s2 += 32) M = fmaxf(M, __ldcg(ml + 2 * s2));
+#pragma unroll
+      for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      float dn = 0.f;
+      for (int s2 = lane; s2 < a.splits; s2 += 32) {
+        const float w = exp2f(__ldcg(ml + 2 * s2) - M);
+        wts[r * a.splits + s2] = w;
+        dn += w * __ldcg(ml + 2 * s2 + 1);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
+      if (lane == 0) den[r] = dn;
+    }
+    sync();
+    // R*D outputs, R*D/128 per thread, each over every split: the loads of
+    // 8 splits x all of a thread's outputs are in flight together
+    constexpr int PER = (R * D + ATT_THREADS - 1) / ATT_THREADS;
+    float num[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) num[q] = 0.f;
+    for (int s0 = 0; s0 < a.splits; s0 += 8) {
+      float v[PER][8];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * ATT_THREADS;
+        const int r = idx / D, dd = idx % D;
+        const float* po = a.part_o + (long long)(g * R + r) * a.splits * D + dd;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[q][u] = (idx < R * D && s0 + u < a.splits) ? __ldcg(po + (long long)(s0 + u) * D) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * ATT_THREADS;
+        const int r = idx < R * D ? idx / D : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < a.splits) num[q] = fmaf(wts[r * a.splits + s0 + u], v[q][u], num[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int idx = tid + q * ATT_THREADS;
+      if (idx < R * D) {
+        const int r = idx / D, dd = idx % D;
+        a.out[(long long)(g * R + r) * D + dd] = __float2bfloat16_rn(num[q] / den[r]);
+      }
+    }
+    if (tid == 0) a.counters[g] = 0u;
+  }
+  sync();  // shared memory reused by the next item
+}
+
 // DEEP: rows in flight per lane doubled (the stand-alone kernel, no register
 // cap); batching only -- every score and every P.V accumulation keeps its order.
 template <int D, int R, bool DEEP = false>
@@ -645,25 +820,7 @@ DS_DEV void attn_item(const AttnArgs& a, int item, float* sc, float* stat, unsig
     }
   }
   __syncthreads();
-  // ---- softmax of each head over the item's keys
-  for (int r = warp; r < R; r += ATT_THREADS / 32) {
-    float m = -INFINITY;
-    for (int i = lane; i < nk; i += 32) m = fmaxf(m, sc[r * sk + i]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float l = 0.f;
-    for (int i = lane; i < nk; i += 32) {
-      const float e = exp2f(sc[r * sk + i] - m);
-      sc[r * sk + i] = e;
-      l += e;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) {
-      stat[2 * r] = m;
-      stat[2 * r + 1] = l;
-    }
-  }
+  attn_softmax<R>(nk, sk, sc, stat);
   __syncthreads();
   // ---- P.V: warp w owns dim chunks [w*CPW, (w+1)*CPW)
   {
@@ -710,89 +867,9 @@ DS_DEV void attn_item(const AttnArgs& a, int item, float* sc, float* stat, unsig
         }
       }
     }
-#pragma unroll
-    for (int o = CPW; o < 32; o <<= 1)
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[r][e] += __shfl_xor_sync(0xffffffffu, acc[r][e], o);
-    if (st == 0) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float4* po = reinterpret_cast<float4*>(a.part_o + ((long long)(g * R + r) * a.splits + s) * D + chunk * 8);
-        __stcg(po, make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
-        __stcg(po + 1, make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]));
-      }
-    }
+    attn_store_part<D, R>(a, g, s, acc);
   }
-  if (tid < R) {
-    float* ml = a.part_ml + ((long long)(g * R + tid) * a.splits + s) * 2;
-    __stcg(ml, stat[2 * tid]);
-    __stcg(ml + 1, stat[2 * tid + 1]);
-  }
-  // ---- the last CTA of this kv head merges every split (threadfence reduction)
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) *is_last = (atomicAdd(a.counters + g, 1u) == (unsigned)a.splits - 1);
-  __syncthreads();
-  if (*is_last) {
-    __threadfence();
-    float* wts = sc;  // [R][splits] then den[R]
-    float* den = wts + R * a.splits;
-    for (int r = warp; r < R; r += ATT_THREADS / 32) {
-      const float* ml = a.part_ml + (long long)(g * R + r) * a.splits * 2;
-      float M = -INFINITY;
-      for (int s2 = lane; s2 < a.splits; s2 += 32) M = fmaxf(M, __ldcg(ml + 2 * s2));
-#pragma unroll
-      for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-      float dn = 0.f;
-      for (int s2 = lane; s2 < a.splits; s2 += 32) {
-        const float w = exp2f(__ldcg(ml + 2 * s2) - M);
-        wts[r * a.splits + s2] = w;
-        dn += w * __ldcg(ml + 2 * s2 + 1);
-      }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
-      if (lane == 0) den[r] = dn;
-    }
-    __syncthreads();
-    // R*D outputs, R*D/128 per thread, each over every split: the loads of
-    // 8 splits x all of a thread's outputs are in flight together
-    constexpr int PER = (R * D + ATT_THREADS - 1) / ATT_THREADS;
-    float num[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) num[q] = 0.f;
-    for (int s0 = 0; s0 < a.splits; s0 += 8) {
-      float v[PER][8];
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int idx = tid + q * ATT_THREADS;
-        const int r = idx / D, dd = idx % D;
-        const float* po = a.part_o + (long long)(g * R + r) * a.splits * D + dd;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          v[q][u] = (idx < R * D && s0 + u < a.splits) ? __ldcg(po + (long long)(s0 + u) * D) : 0.f;
-      }
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int idx = tid + q * ATT_THREADS;
-        const int r = idx < R * D ? idx / D : 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (s0 + u < a.splits) num[q] = fmaf(wts[r * a.splits + s0 + u], v[q][u], num[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int idx = tid + q * ATT_THREADS;
-      if (idx < R * D) {
-        const int r = idx / D, dd = idx % D;
-        a.out[(long long)(g * R + r) * D + dd] = __float2bfloat16_rn(num[q] / den[r]);
-      }
-    }
-    if (tid == 0) a.counters[g] = 0u;
-  }
-  __syncthreads();  // shared memory reused by the next item
+  attn_finish<D, R>(a, g, s, sc, stat, is_last, [] { __syncthreads(); });
 }
 
 template <int D, int R>
@@ -806,6 +883,230 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_decode_kernel(AttnArgs a) {
   pdl_trigger();
   pdl_wait();
   attn_item<D, R, true>(a, blockIdx.x, sc, stat, &is_last);
+}
+
+// ---------------------------------------------------------------- TMA-staged stand-alone attention
+//
+// The per-launch kernel's memory side as a ring: a producer warp bulk-copies
+// the item's K rows, then its V rows, in 32-key pieces (one copy per piece and
+// source; never across a page or the lo/hi boundary) into ATT_SLOTS shared
+// slots, so the whole item streams from the first cycle -- every row except
+// those the predecessor writes (keys >= n_lo, the anchor's own) is issued
+// before the PDL wait.  The 4 compute warps run attn_item's arithmetic on the
+// staged rows: each key's score from the same LPK lanes and butterfly, each
+// lane's P.V keys in the same ascending order, the same softmax and merge --
+// so results are the register kernel's (and the persistent kernel's) bit for
+// bit.  With copy_lo, one thread bulk-stores each staged lo piece into hi (the
+// fused KV ingest) before the slot is released.
+// Reading lo rows before the PDL wait requires them complete before the
+// kernel's own predecessor started, which every caller guarantees: lo is the
+// sender's export (an input of the call), or cache rows written before the
+// anchor chain began (anchor_pass starts with a memset, a full stream
+// barrier) or by a recompute the chain waited on with an event before the
+// layer's QKV GEMV / this kernel launched.
+constexpr int ATT_PIECE = 32;  // keys per ring piece (pages are 64-key aligned)
+constexpr int ATT_SLOTS_MAX = 16;
+
+template <int D, int R>
+__global__ void __launch_bounds__(ATT_THREADS + 32) attn_decode_tma_kernel(AttnArgs a, int slots, int prefetch) {
+  constexpr int ROWB = D * 2, PIECE_B = ATT_PIECE * ROWB;
+  constexpr int LPK = D / 8, KPW = 32 / LPK, UK = (ATT_PIECE / 4) / KPW;  // scores: 8 keys of a piece per warp
+  constexpr int CPW = LPK / 4, NS = 32 / CPW, UV = ATT_PIECE / NS;        // P.V: keys per lane per piece
+  extern __shared__ __align__(128) uint8_t smem_dyn[];
+  uint8_t* ring = smem_dyn;
+  float* sc = reinterpret_cast<float*>(smem_dyn + slots * PIECE_B);
+  __shared__ __align__(8) uint64_t full[ATT_SLOTS_MAX], empty[ATT_SLOTS_MAX];
+  __shared__ float stat[2 * R];
+  __shared__ unsigned int is_last;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = blockIdx.x / a.splits, s = blockIdx.x - g * a.splits;
+  const int k0 = s * a.split_keys;
+  const int nk = min(a.split_keys, a.n_keys - k0);
+  const int sk = a.split_keys;
+  const int np = (nk + ATT_PIECE - 1) / ATT_PIECE;
+  if (tid == ATT_THREADS) {
+    for (int i = 0; i < slots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], ATT_THREADS / 32);
+    }
+    fence_mbar_init();
+  }
+  // optionally pull the whole item toward L2 first (the ring then reads L2)
+  if (prefetch) attn_prefetch(a, blockIdx.x, D);
+  __syncthreads();
+  pdl_trigger();
+  if (tid >= ATT_THREADS) {
+    if (tid == ATT_THREADS) {
+      bool waited = false;
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int p = 0; p < 2 * np; ++p) {
+        const bool v = p >= np;
+        const int a0 = k0 + (v ? p - np : p) * ATT_PIECE;
+        const int a1 = a0 + min(ATT_PIECE, k0 + nk - a0);
+        mbar_wait(&empty[slot], phase ^ 1);
+        mbar_expect_tx(&full[slot], (uint32_t)(a1 - a0) * ROWB);
+        uint8_t* dst = ring + slot * PIECE_B;
+        const int lo_end = min(a1, a.n_lo), hi0 = max(a0, a.n_lo);
+        if (lo_end > a0) bulk_g2s(dst, attn_row(a, v, g, a0), (uint32_t)(lo_end - a0) * ROWB, &full[slot]);
+        if (a1 > hi0) {  // rows the predecessor writes
+          if (!waited) {
+            pdl_wait();
+            waited = true;
+          }
+          bulk_g2s(dst + (hi0 - a0) * ROWB, attn_row(a, v, g, hi0), (uint32_t)(a1 - hi0) * ROWB, &full[slot]);
+        }
+        if (++slot == slots) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  pdl_wait();
+  int slot = 0;
+  uint32_t phase = 0;
+  // one thread stores a staged lo piece into hi (fused ingest); the slot is
+  // released only after the store has read it
+  auto ingest = [&](bool v, int a0, int cnt, const uint8_t* src) {
+    if (a.copy_lo && tid == 0) {
+      const int lo_cnt = min(a0 + cnt, a.n_lo) - a0;
+      if (lo_cnt > 0) {
+        bulk_s2g((v ? a.hi.v : a.hi.k) + a.hi.off(g, a0), src, (uint32_t)lo_cnt * ROWB);
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+    }
+  };
+  // ---- scores
+  {
+    const int c = lane % LPK, kk = lane / LPK;
+    uint4 qv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) qv[r] = ld_cg16(a.q + (long long)(g * R + r) * D + c * 8);
+    for (int p = 0; p < np; ++p) {
+      const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
+      mbar_wait(&full[slot], phase);
+      const uint8_t* src = ring + slot * PIECE_B;
+      uint4 kv[UK];
+#pragma unroll
+      for (int j = 0; j < UK; ++j) {
+        const int key = warp * (ATT_PIECE / 4) + j * KPW + kk;
+        kv[j] = key < cnt ? *reinterpret_cast<const uint4*>(src + key * ROWB + c * 16) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      float pr[UK][R];
+#pragma unroll
+      for (int j = 0; j < UK; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r) pr[j][r] = dot8(kv[j], qv[r]);
+#pragma unroll
+      for (int o = LPK / 2; o; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < UK; ++j)
+#pragma unroll
+          for (int r = 0; r < R; ++r) pr[j][r] += __shfl_xor_sync(0xffffffffu, pr[j][r], o);
+#pragma unroll
+      for (int j = 0; j < UK; ++j) {
+        const int key = warp * (ATT_PIECE / 4) + j * KPW + kk;
+        float v = pr[j][0];
+#pragma unroll
+        for (int r = 1; r < R; ++r)
+          if (c == r) v = pr[j][r];
+        if (key < cnt && c < R) sc[c * sk + pk0 + key] = v * a.scale_log2;
+      }
+      ingest(false, k0 + pk0, cnt, src);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == slots) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  named_sync_consumers();
+  attn_softmax<R>(nk, sk, sc, stat);
+  named_sync_consumers();
+  // ---- P.V: warp w owns dim chunks [w*CPW, (w+1)*CPW); lane keys st, st+NS, ...
+  {
+    const int cw = lane % CPW, st = lane / CPW;
+    const int chunk = warp * CPW + cw;
+    float acc[R][8];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[r][e] = 0.f;
+    for (int p = 0; p < np; ++p) {
+      const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
+      mbar_wait(&full[slot], phase);
+      const uint8_t* src = ring + slot * PIECE_B;
+      uint4 vv[UV];
+#pragma unroll
+      for (int j = 0; j < UV; ++j) {
+        const int key = st + j * NS;
+        vv[j] = key < cnt ? *reinterpret_cast<const uint4*>(src + key * ROWB + chunk * 16) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < UV; ++j) {
+        const int key = st + j * NS;
+        if (key < cnt) {
+          const float2 v0 = unpack_bf16x2(vv[j].x), v1 = unpack_bf16x2(vv[j].y);
+          const float2 v2 = unpack_bf16x2(vv[j].z), v3 = unpack_bf16x2(vv[j].w);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float pp = sc[r * sk + pk0 + key];
+            acc[r][0] = fmaf(pp, v0.x, acc[r][0]);
+            acc[r][1] = fmaf(pp, v0.y, acc[r][1]);
+            acc[r][2] = fmaf(pp, v1.x, acc[r][2]);
+            acc[r][3] = fmaf(pp, v1.y, acc[r][3]);
+            acc[r][4] = fmaf(pp, v2.x, acc[r][4]);
+            acc[r][5] = fmaf(pp, v2.y, acc[r][5]);
+            acc[r][6] = fmaf(pp, v3.x, acc[r][6]);
+            acc[r][7] = fmaf(pp, v3.y, acc[r][7]);
+          }
+        }
+      }
+      ingest(true, k0 + pk0, cnt, src);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == slots) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+    attn_store_part<D, R>(a, g, s, acc);
+  }
+  attn_finish<D, R>(a, g, s, sc, stat, &is_last, [] { named_sync_consumers(); });
+  if (a.copy_lo && tid == 0) bulk_wait<0>();  // the ingest stores land before the grid completes
+}
+
+template <int D, int R>
+static cudaError_t attn_tma_launch_t(const AttnArgs& a, int smem, cudaStream_t stream) {
+  // ring slots and L2 prefetch (DS_ATT_SLOTS, DS_ATT_PREFETCH: experiments)
+  static const int slots_env = env_int("DS_ATT_SLOTS", 12);
+  static const int prefetch = env_int("DS_ATT_PREFETCH", 0);
+  const int slots = slots_env < 2 ? 2 : (slots_env > ATT_SLOTS_MAX ? ATT_SLOTS_MAX : slots_env);
+  auto kern = attn_decode_tma_kernel<D, R>;
+  static int attr = 0;
+  const int total = slots * ATT_PIECE * D * 2 + smem;
+  if (total > attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, total);
+    if (e != cudaSuccess) return e;
+    attr = total;
+  }
+  static const bool c0 = prefer_max_smem(kern);
+  (void)c0;
+  return launch_pdl(kern, dim3(a.n_kv_heads * a.splits), dim3(ATT_THREADS + 32), total, stream, a, slots, prefetch);
+}
+
+// DS_ATTN_TMA=0: the register-streaming kernel (A/B).
+static bool attn_tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_ATTN_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 template <int D, int R>
@@ -826,8 +1127,9 @@ int decode_attention_launch(AttnArgs a, int head_dim, cudaStream_t stream) {
   const int smem = attn_smem_bytes(R, a.split_keys, a.splits);
   count_launch();
   cudaError_t e = cudaErrorInvalidValue;
+  const bool tma = attn_tma_enabled();
 #define DS_ATT_CASE(DD, RR) \
-  if (head_dim == DD && R == RR) e = attn_launch_t<DD, RR>(a, smem, stream);
+  if (head_dim == DD && R == RR) e = tma ? attn_tma_launch_t<DD, RR>(a, smem, stream) : attn_launch_t<DD, RR>(a, smem, stream);
   DS_ATT_CASE(128, 1) DS_ATT_CASE(128, 2) DS_ATT_CASE(128, 4) DS_ATT_CASE(128, 8)
   DS_ATT_CASE(64, 1) DS_ATT_CASE(64, 2) DS_ATT_CASE(64, 4) DS_ATT_CASE(64, 8)
 #undef DS_ATT_CASE

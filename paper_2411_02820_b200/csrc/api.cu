@@ -320,9 +320,22 @@ bool sender_is_remote(const void* p) {
 // copied into the consumer cache as they are read (the fused KV ingest).
 // wait (optional): an event the attention waits for (the layer's window K/V on
 // another stream); the QKV GEMV before it does not depend on it.
+// DS_ABLATE_ANCHOR=<mask>: timing ablation of the per-launch anchor kernels
+// (1 qkv, 2 attention, 4 o-proj, 8 w1, 16 w2 skipped).  The results are wrong
+// under it; tools/ab_anchor.sh uses it to price each kernel inside the chain.
+static int ablate_anchor() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DS_ABLATE_ANCHOR");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender = nullptr,
                  cudaEvent_t wait = nullptr) {
   const ds_dims& d = c.d;
+  const int skip = ablate_anchor();
   const ds_layer_weights& W = c.m->layers[l];
   const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
   GemvArgs g{};
@@ -341,7 +354,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   g.kv = layer_addr(*c.kv, l, d.head_dim);
   g.rope_cos = c.m->rope_cos;
   g.rope_sin = c.m->rope_sin;
-  DS_TRY(gemv_launch(g, c.s), "anchor qkv");
+  if (!(skip & 1)) DS_TRY(gemv_launch(g, c.s), "anchor qkv");
   if (wait && cudaStreamWaitEvent(c.s, wait, 0) != cudaSuccess) return cuda_fail("wait");
   const KvAddr ka = g.kv;
   AttnArgs at{};
@@ -358,8 +371,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   at.part_ml = c.w.part_ml;
   at.counters = c.w.dec_count;
   at.out = c.w.o_a;
-  DS_TRY(decode_attention_launch(at, d.head_dim, c.s),
-         "anchor attention");
+  if (!(skip & 2)) DS_TRY(decode_attention_launch(at, d.head_dim, c.s), "anchor attention");
   GemvArgs o{};
   o.W = static_cast<const bf16*>(W.wo);
   o.ldw = hd;
@@ -369,7 +381,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   o.mode = EPI_RESID_F32;
   o.out_f32 = h_a;
   o.resid = h_a;
-  DS_TRY(gemv_launch(o, c.s), "anchor o-proj");
+  if (!(skip & 4)) DS_TRY(gemv_launch(o, c.s), "anchor o-proj");
   GemvArgs f{};
   f.W = static_cast<const bf16*>(W.w1);
   f.ldw = d.d_model;
@@ -379,7 +391,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   f.gain = W.g_mlp;
   f.mode = d.mlp_kind == DS_MLP_SWIGLU ? EPI_SWIGLU_BF16 : EPI_SILU_BF16;
   f.out_bf16 = c.w.u_a;
-  DS_TRY(gemv_launch(f, c.s), "anchor w1");
+  if (!(skip & 8)) DS_TRY(gemv_launch(f, c.s), "anchor w1");
   GemvArgs s2{};
   s2.W = static_cast<const bf16*>(W.w2);
   s2.ldw = d.d_ff;
@@ -389,7 +401,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   s2.mode = EPI_RESID_F32;
   s2.out_f32 = h_a;
   s2.resid = h_a;
-  DS_TRY(gemv_launch(s2, c.s), "anchor w2");
+  if (!(skip & 16)) DS_TRY(gemv_launch(s2, c.s), "anchor w2");
   return DS_OK;
 }
 
@@ -407,7 +419,8 @@ int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token, int64_t* to
   g.mode = EPI_STORE_F32;
   g.out_f32 = logits;
   g.argmax = c.w.argmax;
-  DS_TRY(gemv_launch(g, c.s, /*staged=*/false), "lm head");
+  static const bool lm_tma = !(getenv("DS_LMHEAD_TMA") && getenv("DS_LMHEAD_TMA")[0] == '0');  // A/B switch
+  DS_TRY(gemv_launch(g, c.s, /*staged=*/lm_tma), "lm head");
   if (token || token64) DS_TRY(argmax_finalize_launch(c.w.argmax, token, token64, c.s), "argmax");
   return DS_OK;
 }
