@@ -30,6 +30,7 @@
 //                  it.  A recomputed layer's attention waits on the counter the
 //                  recompute's QKV GEMM epilogue bumps (GemmEpi::done), not on
 //                  a stream event.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -662,21 +663,22 @@ DS_DEV void attn_softmax(int nk, int sk, float* sc, float* stat) {
 
 // P.V partials of one thread (lane = (dim chunk, key stream)): reduce the key
 // streams with shuffles, store the item's unnormalised output.
-template <int D, int R>
-DS_DEV void attn_store_part(const AttnArgs& a, int g, int s, float (*acc)[8]) {
+// NR heads from r0 (of the kv head's R), dim chunk `chunk`.
+template <int D, int R, int NR = R>
+DS_DEV void attn_store_part(const AttnArgs& a, int g, int s, float (*acc)[8], int chunk, int r0 = 0) {
   constexpr int CPW = D / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cw = lane % CPW, st = lane / CPW, chunk = warp * CPW + cw;
+  const int lane = threadIdx.x & 31, st = lane / CPW;
 #pragma unroll
   for (int o = CPW; o < 32; o <<= 1)
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+    for (int r = 0; r < NR; ++r)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[r][e] += __shfl_xor_sync(0xffffffffu, acc[r][e], o);
   if (st == 0) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      float4* po = reinterpret_cast<float4*>(a.part_o + ((long long)(g * R + r) * a.splits + s) * D + chunk * 8);
+    for (int r = 0; r < NR; ++r) {
+      float4* po =
+          reinterpret_cast<float4*>(a.part_o + ((long long)(g * R + r0 + r) * a.splits + s) * D + chunk * 8);
       __stcg(po, make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
       __stcg(po + 1, make_float4(acc[r][4], acc[r][5], acc[r][6], acc[r][7]));
     }
@@ -867,7 +869,7 @@ DS_DEV void attn_item(const AttnArgs& a, int item, float* sc, float* stat, unsig
         }
       }
     }
-    attn_store_part<D, R>(a, g, s, acc);
+    attn_store_part<D, R>(a, g, s, acc, chunk);
   }
   attn_finish<D, R>(a, g, s, sc, stat, is_last, [] { __syncthreads(); });
 }
@@ -906,16 +908,121 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_decode_kernel(AttnArgs a) {
 // layer's QKV GEMV / this kernel launched.
 constexpr int ATT_PIECE = 32;  // keys per ring piece (pages are 64-key aligned)
 constexpr int ATT_SLOTS_MAX = 16;
+constexpr int ATT_TW = 8;                         // compute warps
+constexpr int ATT_TTHREADS = ATT_TW * 32 + 32;  // + producer warp
+
+DS_DEV void named_sync_compute() { asm volatile("bar.sync 2, %0;" ::"n"(ATT_TW * 32) : "memory"); }
+
+// attn_finish for the 8-warp stand-alone kernel: the same (m, l) store,
+// arrival count and merge arithmetic (same max, same lane-strided sums, each
+// output accumulated over the splits in ascending order).  The merging CTA
+// stages the kv head's partial outputs in the (idle) ring with one bulk copy
+// and its (m, l) with one load per thread, so the merge costs one round trip
+// instead of one per group of splits.
+template <int D, int R>
+DS_DEV void attn_finish_wide(const AttnArgs& a, int g, int s, float* sc, const float* stat, unsigned int* is_last,
+                             uint8_t* stage, int stage_bytes, uint64_t* bar) {
+  constexpr int NT = ATT_TW * 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < R) {
+    float* ml = a.part_ml + ((long long)(g * R + tid) * a.splits + s) * 2;
+    __stcg(ml, stat[2 * tid]);
+    __stcg(ml + 1, stat[2 * tid + 1]);
+  }
+  __threadfence();
+  named_sync_compute();
+  if (tid == 0) *is_last = (atomicAdd(a.counters + g, 1u) == (unsigned)a.splits - 1);
+  named_sync_compute();
+  if (!*is_last) return;
+  __threadfence();
+  const int n_ml = R * a.splits * 2;
+  const uint32_t o_bytes = (uint32_t)R * a.splits * D * 4;
+  const bool staged = (int)o_bytes + 4 * n_ml <= stage_bytes;
+  float* po_s = reinterpret_cast<float*>(stage);
+  float* ml_s = po_s + (size_t)R * a.splits * D;
+  const float* po_g = a.part_o + (long long)g * R * a.splits * D;
+  const float* ml_g = a.part_ml + (long long)g * R * a.splits * 2;
+  if (staged) {
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // the other CTAs' generic stores, acquired above
+      mbar_expect_tx(bar, o_bytes);
+      bulk_g2s(po_s, po_g, o_bytes, bar);
+    }
+    for (int i = tid; i < n_ml; i += NT) ml_s[i] = __ldcg(ml_g + i);
+    named_sync_compute();
+  }
+  const float* ml_src = staged ? ml_s : ml_g;
+  float* wts = sc;  // [R][splits] then den[R]
+  float* den = wts + R * a.splits;
+  if (warp < ATT_THREADS / 32) {  // warps 0..3, as attn_finish
+    for (int r = warp; r < R; r += ATT_THREADS / 32) {
+      const float* ml = ml_src + (long long)r * a.splits * 2;
+      float M = -INFINITY;
+      for (int s2 = lane; s2 < a.splits; s2 += 32) M = fmaxf(M, staged ? ml[2 * s2] : __ldcg(ml + 2 * s2));
+#pragma unroll
+      for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      float dn = 0.f;
+      for (int s2 = lane; s2 < a.splits; s2 += 32) {
+        const float w = exp2f((staged ? ml[2 * s2] : __ldcg(ml + 2 * s2)) - M);
+        wts[r * a.splits + s2] = w;
+        dn += w * (staged ? ml[2 * s2 + 1] : __ldcg(ml + 2 * s2 + 1));
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
+      if (lane == 0) den[r] = dn;
+    }
+  }
+  if (staged) mbar_wait(bar, 0);
+  named_sync_compute();  // wts / den written, partial outputs landed
+  constexpr int PER = (R * D + NT - 1) / NT;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int idx = tid + q * NT;
+    if (idx < R * D) {
+      const int r = idx / D, dd = idx % D;
+      const float* po = (staged ? po_s : po_g) + (long long)r * a.splits * D + dd;
+      float num = 0.f;
+      for (int s2 = 0; s2 < a.splits; ++s2)
+        num = fmaf(wts[r * a.splits + s2], staged ? po[(long long)s2 * D] : __ldcg(po + (long long)s2 * D), num);
+      a.out[(long long)(g * R + r) * D + dd] = __float2bfloat16_rn(num / den[r]);
+    }
+  }
+  if (tid == 0) a.counters[g] = 0u;
+}
+
+#if DS_ATT_STAMPS
+// Debug timeline (build with DS_NVCC_EXTRA=-DDS_ATT_STAMPS=1): a few CTAs of
+// one launch print global-timer stamps of their phases.
+__device__ unsigned int g_att_launch;
+#define ATT_STAMP(i) \
+  do {                \
+    if (tid == 0) st_ns[i] = global_ns(); \
+  } while (0)
+#else
+#define ATT_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
 
 template <int D, int R>
-__global__ void __launch_bounds__(ATT_THREADS + 32) attn_decode_tma_kernel(AttnArgs a, int slots, int prefetch) {
+__global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnArgs a, int slots, int prefetch) {
+#if DS_ATT_STAMPS
+  unsigned long long st_ns[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   constexpr int ROWB = D * 2, PIECE_B = ATT_PIECE * ROWB;
-  constexpr int LPK = D / 8, KPW = 32 / LPK, UK = (ATT_PIECE / 4) / KPW;  // scores: 8 keys of a piece per warp
-  constexpr int CPW = LPK / 4, NS = 32 / CPW, UV = ATT_PIECE / NS;        // P.V: keys per lane per piece
+  // scores: each warp takes ATT_PIECE / ATT_TW keys of a piece, LPK lanes per key
+  constexpr int LPK = D / 8, KPW = 32 / LPK, UK = (ATT_PIECE / ATT_TW) / KPW;
+  static_assert(UK >= 1, "piece too small for the warp count");
+  // P.V: warps (w & 3) own dim chunks like attn_item's 4 warps; warps >= 4
+  // take the upper half of the heads (R >= 2), so every accumulator sums the
+  // same keys in the same order
+  constexpr int CPW = LPK / 4, NS = 32 / CPW, UV = ATT_PIECE / NS;
+  constexpr int HR = R >= 2 ? R / 2 : 1;
+  constexpr int RP = R >= 2 ? R / 2 : 1;  // head pairs (scores, packed)
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* ring = smem_dyn;
   float* sc = reinterpret_cast<float*>(smem_dyn + slots * PIECE_B);
-  __shared__ __align__(8) uint64_t full[ATT_SLOTS_MAX], empty[ATT_SLOTS_MAX];
+  __shared__ __align__(8) uint64_t full[ATT_SLOTS_MAX], empty[ATT_SLOTS_MAX], merge_bar;
   __shared__ float stat[2 * R];
   __shared__ unsigned int is_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -924,19 +1031,20 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) attn_decode_tma_kernel(AttnA
   const int nk = min(a.split_keys, a.n_keys - k0);
   const int sk = a.split_keys;
   const int np = (nk + ATT_PIECE - 1) / ATT_PIECE;
-  if (tid == ATT_THREADS) {
+  if (tid == ATT_TW * 32) {
     for (int i = 0; i < slots; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], ATT_THREADS / 32);
+      mbar_init(&empty[i], ATT_TW);
     }
+    mbar_init(&merge_bar, 1);
     fence_mbar_init();
   }
   // optionally pull the whole item toward L2 first (the ring then reads L2)
   if (prefetch) attn_prefetch(a, blockIdx.x, D);
   __syncthreads();
   pdl_trigger();
-  if (tid >= ATT_THREADS) {
-    if (tid == ATT_THREADS) {
+  if (warp == ATT_TW) {
+    if (lane == 0) {
       bool waited = false;
       int slot = 0;
       uint32_t phase = 0;
@@ -964,7 +1072,9 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) attn_decode_tma_kernel(AttnA
     }
     return;
   }
+  ATT_STAMP(0);
   pdl_wait();
+  ATT_STAMP(1);
   int slot = 0;
   uint32_t phase = 0;
   // one thread stores a staged lo piece into hi (fused ingest); the slot is
@@ -979,105 +1089,151 @@ __global__ void __launch_bounds__(ATT_THREADS + 32) attn_decode_tma_kernel(AttnA
       }
     }
   };
-  // ---- scores
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == slots) {
+      slot = 0;
+      phase ^= 1;
+    }
+  };
+  // ---- scores (dot8's order per key and head; head pairs on packed lanes)
   {
     const int c = lane % LPK, kk = lane / LPK;
-    uint4 qv[R];
+    float2 qf[RP][8];  // (head 2i, head 2i+1) per element; R == 1: (head 0, head 0)
 #pragma unroll
-    for (int r = 0; r < R; ++r) qv[r] = ld_cg16(a.q + (long long)(g * R + r) * D + c * 8);
+    for (int i = 0; i < RP; ++i) {
+      const int r0 = R >= 2 ? 2 * i : 0, r1 = R >= 2 ? 2 * i + 1 : 0;
+      const uint4 q0 = ld_cg16(a.q + (long long)(g * R + r0) * D + c * 8);
+      const uint4 q1 = ld_cg16(a.q + (long long)(g * R + r1) * D + c * 8);
+      const uint32_t w0[4] = {q0.x, q0.y, q0.z, q0.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f0 = unpack_bf16x2(w0[k]), f1 = unpack_bf16x2(w1[k]);
+        qf[i][2 * k] = make_float2(f0.x, f1.x);
+        qf[i][2 * k + 1] = make_float2(f0.y, f1.y);
+      }
+    }
     for (int p = 0; p < np; ++p) {
       const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
       mbar_wait(&full[slot], phase);
+      if (p == 0) ATT_STAMP(2);
       const uint8_t* src = ring + slot * PIECE_B;
-      uint4 kv[UK];
+      float2 pr[UK][RP];
 #pragma unroll
       for (int j = 0; j < UK; ++j) {
-        const int key = warp * (ATT_PIECE / 4) + j * KPW + kk;
-        kv[j] = key < cnt ? *reinterpret_cast<const uint4*>(src + key * ROWB + c * 16) : make_uint4(0u, 0u, 0u, 0u);
+        const int key = warp * (ATT_PIECE / ATT_TW) + j * KPW + kk;
+        const uint4 kv =
+            key < cnt ? *reinterpret_cast<const uint4*>(src + key * ROWB + c * 16) : make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+        float kf[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = unpack_bf16x2(kw[k]);
+          kf[2 * k] = f.x;
+          kf[2 * k + 1] = f.y;
+        }
+#pragma unroll
+        for (int i = 0; i < RP; ++i) {
+          float2 acc = fmul2(make_float2(kf[0], kf[0]), qf[i][0]);
+#pragma unroll
+          for (int e = 1; e < 8; ++e) acc = ffma2(make_float2(kf[e], kf[e]), qf[i][e], acc);
+          pr[j][i] = acc;
+        }
       }
-      float pr[UK][R];
-#pragma unroll
-      for (int j = 0; j < UK; ++j)
-#pragma unroll
-        for (int r = 0; r < R; ++r) pr[j][r] = dot8(kv[j], qv[r]);
 #pragma unroll
       for (int o = LPK / 2; o; o >>= 1)
 #pragma unroll
         for (int j = 0; j < UK; ++j)
 #pragma unroll
-          for (int r = 0; r < R; ++r) pr[j][r] += __shfl_xor_sync(0xffffffffu, pr[j][r], o);
+          for (int i = 0; i < RP; ++i) {
+            pr[j][i].x += __shfl_xor_sync(0xffffffffu, pr[j][i].x, o);
+            if (R >= 2) pr[j][i].y += __shfl_xor_sync(0xffffffffu, pr[j][i].y, o);
+          }
 #pragma unroll
       for (int j = 0; j < UK; ++j) {
-        const int key = warp * (ATT_PIECE / 4) + j * KPW + kk;
-        float v = pr[j][0];
+        const int key = warp * (ATT_PIECE / ATT_TW) + j * KPW + kk;
+        float v = pr[j][0].x;
 #pragma unroll
         for (int r = 1; r < R; ++r)
-          if (c == r) v = pr[j][r];
+          if (c == r) v = (r & 1) ? pr[j][r >> 1].y : pr[j][r >> 1].x;
         if (key < cnt && c < R) sc[c * sk + pk0 + key] = v * a.scale_log2;
       }
       ingest(false, k0 + pk0, cnt, src);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == slots) {
-        slot = 0;
-        phase ^= 1;
-      }
+      release();
     }
   }
-  named_sync_consumers();
-  attn_softmax<R>(nk, sk, sc, stat);
-  named_sync_consumers();
-  // ---- P.V: warp w owns dim chunks [w*CPW, (w+1)*CPW); lane keys st, st+NS, ...
+  named_sync_compute();
+  ATT_STAMP(3);
+  if (warp < ATT_THREADS / 32) attn_softmax<R>(nk, sk, sc, stat);
+  named_sync_compute();
+  ATT_STAMP(4);
+  // ---- P.V
   {
     const int cw = lane % CPW, st = lane / CPW;
-    const int chunk = warp * CPW + cw;
-    float acc[R][8];
+    const int chunk = (warp & 3) * CPW + cw;
+    const int r0 = (warp >> 2) * HR;
+    const bool active = R >= 2 || warp < 4;
+    float2 acc[HR][4];
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+    for (int r = 0; r < HR; ++r)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[r][e] = 0.f;
+      for (int e = 0; e < 4; ++e) acc[r][e] = make_float2(0.f, 0.f);
     for (int p = 0; p < np; ++p) {
       const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
       mbar_wait(&full[slot], phase);
       const uint8_t* src = ring + slot * PIECE_B;
-      uint4 vv[UV];
+      if (active) {
 #pragma unroll
-      for (int j = 0; j < UV; ++j) {
-        const int key = st + j * NS;
-        vv[j] = key < cnt ? *reinterpret_cast<const uint4*>(src + key * ROWB + chunk * 16) : make_uint4(0u, 0u, 0u, 0u);
-      }
+        for (int j = 0; j < UV; ++j) {
+          const int key = st + j * NS;
+          if (key < cnt) {
+            const uint4 vv = *reinterpret_cast<const uint4*>(src + key * ROWB + chunk * 16);
+            const float2 v0 = unpack_bf16x2(vv.x), v1 = unpack_bf16x2(vv.y);
+            const float2 v2 = unpack_bf16x2(vv.z), v3 = unpack_bf16x2(vv.w);
 #pragma unroll
-      for (int j = 0; j < UV; ++j) {
-        const int key = st + j * NS;
-        if (key < cnt) {
-          const float2 v0 = unpack_bf16x2(vv[j].x), v1 = unpack_bf16x2(vv[j].y);
-          const float2 v2 = unpack_bf16x2(vv[j].z), v3 = unpack_bf16x2(vv[j].w);
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float pp = sc[r * sk + pk0 + key];
-            acc[r][0] = fmaf(pp, v0.x, acc[r][0]);
-            acc[r][1] = fmaf(pp, v0.y, acc[r][1]);
-            acc[r][2] = fmaf(pp, v1.x, acc[r][2]);
-            acc[r][3] = fmaf(pp, v1.y, acc[r][3]);
-            acc[r][4] = fmaf(pp, v2.x, acc[r][4]);
-            acc[r][5] = fmaf(pp, v2.y, acc[r][5]);
-            acc[r][6] = fmaf(pp, v3.x, acc[r][6]);
-            acc[r][7] = fmaf(pp, v3.y, acc[r][7]);
+            for (int r = 0; r < HR; ++r) {
+              const float pp = sc[(r0 + r) * sk + pk0 + key];
+              const float2 p2 = make_float2(pp, pp);
+              acc[r][0] = ffma2(p2, v0, acc[r][0]);
+              acc[r][1] = ffma2(p2, v1, acc[r][1]);
+              acc[r][2] = ffma2(p2, v2, acc[r][2]);
+              acc[r][3] = ffma2(p2, v3, acc[r][3]);
+            }
           }
         }
       }
       ingest(true, k0 + pk0, cnt, src);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == slots) {
-        slot = 0;
-        phase ^= 1;
-      }
+      release();
     }
-    attn_store_part<D, R>(a, g, s, acc);
+    if (active) {
+      float accs[HR][8];
+#pragma unroll
+      for (int r = 0; r < HR; ++r)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          accs[r][2 * e] = acc[r][e].x;
+          accs[r][2 * e + 1] = acc[r][e].y;
+        }
+      attn_store_part<D, R, HR>(a, g, s, accs, chunk, r0);
+    }
   }
-  attn_finish<D, R>(a, g, s, sc, stat, &is_last, [] { named_sync_consumers(); });
+  __threadfence();
+  named_sync_compute();  // every part_o store is fenced before the arrival count
+  ATT_STAMP(5);
+  // every piece is consumed: the ring is free to stage the merge
+  attn_finish_wide<D, R>(a, g, s, sc, stat, &is_last, ring, slots * PIECE_B, &merge_bar);
   if (a.copy_lo && tid == 0) bulk_wait<0>();  // the ingest stores land before the grid completes
+  ATT_STAMP(6);
+#if DS_ATT_STAMPS
+  if (tid == 0) {
+    const unsigned int launch = *(volatile unsigned int*)&g_att_launch;
+    if (launch == 100 && (s == 0 || s == a.splits - 1 || is_last))
+      printf("ATT %d %d %d last=%d %llu %llu %llu %llu %llu %llu %llu\n", launch, g, s, (int)is_last, st_ns[0], st_ns[1],
+             st_ns[2], st_ns[3], st_ns[4], st_ns[5], st_ns[6]);
+    if (blockIdx.x == 0) atomicAdd(&g_att_launch, 1u);
+  }
+#endif
 }
 
 template <int D, int R>
@@ -1096,7 +1252,7 @@ static cudaError_t attn_tma_launch_t(const AttnArgs& a, int smem, cudaStream_t s
   }
   static const bool c0 = prefer_max_smem(kern);
   (void)c0;
-  return launch_pdl(kern, dim3(a.n_kv_heads * a.splits), dim3(ATT_THREADS + 32), total, stream, a, slots, prefetch);
+  return launch_pdl(kern, dim3(a.n_kv_heads * a.splits), dim3(ATT_TTHREADS), total, stream, a, slots, prefetch);
 }
 
 // DS_ATTN_TMA=0: the register-streaming kernel (A/B).
