@@ -457,10 +457,10 @@ def run_ours(args, world, rank, local):
     dstream = torch.cuda.Stream(device=dev)  # its own workspace: the captured step's stays untouched
     with torch.cuda.stream(dstream):
         dres = P.partial_prefill(B, ids, rc, prod.kv, e_map, out=dcache, stream=dstream, tokens_dev=tok_dev)
-        decode_greedy(B, dcache, dres, steps=dsteps + 1)  # warm-up (workspace sized for the run)
+        decode_greedy(B, dcache, dres, steps=dsteps + 1, positions=n)  # warm-up (workspace sized for the run)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(dstream)
-        decode_greedy(B, dcache, dres, steps=dsteps + 1)
+        decode_greedy(B, dcache, dres, steps=dsteps + 1, positions=n)
         e1.record(dstream)
     torch.cuda.synchronize()
     dec_ms = e0.elapsed_time(e1) / dsteps
