@@ -1040,7 +1040,9 @@ __global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnAr
     fence_mbar_init();
   }
   // optionally pull the whole item toward L2 first (the ring then reads L2)
-  if (prefetch) attn_prefetch(a, blockIdx.x, D);
+  if (prefetch & 1) attn_prefetch(a, blockIdx.x, D);
+  // timing experiments (results are wrong): data movement only, or no scores / no P.V math
+  const bool no_scores = prefetch & 6, no_pv = prefetch & 10;
   __syncthreads();
   pdl_trigger();
   if (warp == ATT_TW) {
@@ -1119,6 +1121,10 @@ __global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnAr
       mbar_wait(&full[slot], phase);
       if (p == 0) ATT_STAMP(2);
       const uint8_t* src = ring + slot * PIECE_B;
+      if (no_scores) {
+        release();
+        continue;
+      }
       float2 pr[UK][RP];
 #pragma unroll
       for (int j = 0; j < UK; ++j) {
@@ -1183,7 +1189,7 @@ __global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnAr
       const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
       mbar_wait(&full[slot], phase);
       const uint8_t* src = ring + slot * PIECE_B;
-      if (active) {
+      if (active && !no_pv) {
 #pragma unroll
         for (int j = 0; j < UV; ++j) {
           const int key = st + j * NS;
@@ -1240,7 +1246,7 @@ template <int D, int R>
 static cudaError_t attn_tma_launch_t(const AttnArgs& a, int smem, cudaStream_t stream) {
   // ring slots and L2 prefetch (DS_ATT_SLOTS, DS_ATT_PREFETCH: experiments)
   static const int slots_env = env_int("DS_ATT_SLOTS", 12);
-  static const int prefetch = env_int("DS_ATT_PREFETCH", 0);
+  static const int prefetch = env_int("DS_ATT_PREFETCH", 0);  // bit 0 L2 prefetch; bits 1-3 timing experiments
   const int slots = slots_env < 2 ? 2 : (slots_env > ATT_SLOTS_MAX ? ATT_SLOTS_MAX : slots_env);
   auto kern = attn_decode_tma_kernel<D, R>;
   static int attr = 0;
