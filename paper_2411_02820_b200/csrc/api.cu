@@ -612,6 +612,10 @@ int check_cache(const ds_kv_cache* c, const ds_dims& d, int n, const char* what)
 // ds_full_prefill (= every layer recomputed, no sender: the reference's
 // full_prefill is _mixed_prefill over the same window + anchor structure,
 // model.py:641-649, so recompute-all is the full prefill bit for bit).
+// Persistent co-resident anchor when the recompute covers at least this many
+// row-layers per model layer (k * P >= kFuseRowLayers * L); measured crossover.
+constexpr long long kFuseRowLayers = 800;
+
 int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n_groups,
                  const std::vector<const ds_e_cache*>& seed, const ds_kv_cache* sender_kv,
                  const std::vector<int32_t>& reused, const std::vector<char>& covered, float* logits_out,
@@ -634,7 +638,14 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
   // k * P ~ 800 * L recomputed row-layers.
   long long recomputed = 0;
   for (int l = 0; l < L; ++l) recomputed += covered[l];
-  const bool fused = anchor_persistent_fits(d, n) && recomputed * P >= 800LL * L;
+  // DS_ANCHOR_SHAPE=persistent|launch overrides the rule (crossover measurements)
+  static int shape = -1;
+  if (shape < 0) {
+    const char* e = getenv("DS_ANCHOR_SHAPE");
+    shape = !e ? 0 : (e[0] == 'p' ? 1 : (e[0] == 'l' ? 2 : 0));
+  }
+  const bool fused = anchor_persistent_fits(d, n) &&
+                     (shape == 1 || (shape == 0 && recomputed * P >= (long long)kFuseRowLayers * L));
   std::vector<char> reused_flag(L, 0);
   for (int l : reused) reused_flag[l] = 1;
   AnchorPlan plan;
