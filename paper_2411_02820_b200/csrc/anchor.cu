@@ -1304,8 +1304,18 @@ int decode_attention_launch(AttnArgs a, int head_dim, cudaStream_t stream) {
 // bar[1] is the generation; `gen` is thread 0's copy of the generation.
 // Spins are bounded: a barrier (or a wait on the other stream) that has not
 // completed within 10 s traps instead of hanging the GPU.
-DS_DEV void spin_check(unsigned long long t0) {
-  if (global_ns() - t0 > 10000000000ull) __trap();
+DS_DEV unsigned int sm_id() {
+  unsigned int v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+// On a timeout the spinning thread reports what it waited for, then traps.
+DS_DEV void spin_check(unsigned long long t0, const unsigned int* word, unsigned int want, const char* what) {
+  if (global_ns() - t0 > 10000000000ull) {
+    printf("anchor: %s timed out in CTA %d (SM %u): word %u, waiting for %u\n", what, (int)blockIdx.x, sm_id(),
+           *(volatile const unsigned int*)word, want);
+    __trap();
+  }
 }
 
 DS_DEV void grid_sync(unsigned int* bar, unsigned int& gen, unsigned int nblocks) {
@@ -1327,7 +1337,7 @@ DS_DEV void grid_sync(unsigned int* bar, unsigned int& gen, unsigned int nblocks
           __nanosleep(ns);
           ns = ns < 512 ? 2 * ns : 512;
         }
-        if ((it & 255u) == 0) spin_check(t0);
+        if ((it & 255u) == 0) spin_check(t0, bar, nblocks, "grid barrier (arrivals)");
       }
     }
     gen = g + 1;
@@ -1349,7 +1359,7 @@ DS_DEV void wait_count(const unsigned int* counter, unsigned int target) {
     unsigned int it = 0;
     while (ld_acquire_u32(counter) < target) {
       __nanosleep(500);
-      if ((++it & 255u) == 0) spin_check(t0);
+      if ((++it & 255u) == 0) spin_check(t0, counter, target, "wait on the recompute's GEMM counter");
     }
     __threadfence();
   }

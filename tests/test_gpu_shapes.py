@@ -68,3 +68,31 @@ def test_persistent_anchor_multi_group(groups):
     reused = [l for l in range(8) if not any(a <= l <= b for a, b in groups)]
     for l in reused:
         assert torch.equal(d2.k[l, :, :N - 1], prod.kv.k[l, :, :N - 1])
+
+
+@pytest.mark.parametrize("shape", [
+    dict(n_layers=8, d_model=1024, n_heads=8, n_kv_heads=8, head_dim=128, d_ff=2816, vocab_size=4096),
+    dict(n_layers=8, d_model=1024, n_heads=16, n_kv_heads=8, head_dim=64, d_ff=2816, vocab_size=4096),
+], ids=["r1-d128", "r2-d64"])
+def test_per_launch_attention_ragged(shape):
+    """GQA ratios 1 and 2 at a prompt length that is not a multiple of the
+    32-key ring piece (n = 3001): the per-launch anchor (TMA-staged split-KV
+    attention, single stream) equals the persistent kernel (two streams) bit
+    for bit, including the reused layers it bulk-stores into the cache."""
+    import paper_2411_02820_b200 as P
+    n = 3001
+    cfg = P.ModelConfig(max_seq=n + 64, base_seed=0, **shape)
+    A = P.random_model(cfg, seed=15)
+    B = P.random_model(cfg, seed=16, base=A, perturb_layers=range(5, 8), eps=0.5)
+    ids = np.random.default_rng(19).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
+    rc = P.RecomputeConfig([(5, 7)])
+    prod = P.full_prefill(A, ids, e_layers=rc.transition_layers)
+    one = P.partial_prefill(B, ids, rc, prod.kv, prod.e_map())
+    two = P.partial_prefill(B, ids, rc, prod.kv, prod.e_map(), copy_stream=torch.cuda.Stream())
+    torch.cuda.synchronize()
+    assert torch.isfinite(one.logits).all()
+    assert torch.equal(one.logits, two.logits)
+    d1, d2 = one.kv.dense(), two.kv.dense()
+    assert torch.equal(d1.k, d2.k) and torch.equal(d1.v, d2.v)
+    assert torch.equal(d1.k[:5, :, :n - 1], prod.kv.k[:5, :, :n - 1])
+    assert torch.equal(d1.v[:5, :, :n - 1], prod.kv.v[:5, :, :n - 1])

@@ -56,6 +56,7 @@ def main():
         ids = np.random.default_rng(n).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
         tok = torch.from_numpy(ids).cuda()
         prod = P.full_prefill(A, ids, e_layers=[L - k for k in ks], tokens_dev=tok)
+        torch.cuda.synchronize()  # the producer ran on the default stream: finish it before timing
         full = timed(lambda: P.full_prefill(B, ids, e_layers=(), stream=stream, copy_stream=side, tokens_dev=tok), 1 + args.steps,
                      stream)
         cache = P.PagedKV.allocate(cfg, n)
