@@ -503,7 +503,12 @@ template <int KS>
 static int gemv_tma_launch_t(const GemvArgs& a, cudaStream_t stream, int ctas_per_sm) {
   constexpr int SLOT = GEMV_ROWS * KS * 2;
   const int xbytes = (a.K * 2 + 127) & ~127;
-  static const int budget = env_int("DS_GEMV_SMEM_KB", 200) * 1024;  // experiments
+  // 196 KB: one CTA fits beside a persistent anchor CTA (28 KB + reservations)
+  // on an SM, so this kernel on another stream can always be placed while a
+  // fused call's anchor holds every SM -- a 200 KB ring could not, and the GPU's
+  // CTA dispatch then starved the fused call's GEMMs (deadlock, 10 s trap).
+  // 1% slower alone than 200 KB (DS_GEMV_SMEM_KB: experiments).
+  static const int budget = env_int("DS_GEMV_SMEM_KB", 196) * 1024;
   int slots = (budget / ctas_per_sm - xbytes) / SLOT;
   slots = slots > 16 ? 16 : slots;
   if (slots < 2) return DS_ERR_INVALID;

@@ -207,7 +207,8 @@ def _workspace(model: ModelWeights, n: int, stream=None) -> torch.Tensor:
     key = (model.device, id(model), s.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=model.device)
+        with torch.cuda.stream(s):  # owned by the stream that uses it (allocator reuse across streams)
+            ws = torch.empty(need, dtype=torch.uint8, device=model.device)
         _WS[key] = ws
     return ws
 
@@ -237,11 +238,12 @@ def full_prefill(model: ModelWeights, tokens, e_layers: Iterable[int] | None = N
     ids = check_tokens(tokens, cfg)
     n = ids.shape[0]
     layers = list(range(cfg.n_layers)) if e_layers is None else sorted(set(int(l) for l in e_layers))
-    kv = out if out is not None else LayerKV.empty(cfg, n, model.device)
-    e_bufs = [torch.empty(n - 1, cfg.d_model, dtype=torch.float32, device=model.device) for _ in layers]
-    logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=model.device)
-    tok = torch.empty(1, dtype=torch.int32, device=model.device)
     s = stream if stream is not None else torch.cuda.current_stream(model.device)
+    with torch.cuda.stream(s):  # outputs belong to the stream that writes them (allocator reuse)
+        kv = out if out is not None else LayerKV.empty(cfg, n, model.device)
+        e_bufs = [torch.empty(n - 1, cfg.d_model, dtype=torch.float32, device=model.device) for _ in layers]
+        logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=model.device)
+        tok = torch.empty(1, dtype=torch.int32, device=model.device)
     ws = _workspace(model, n, s)
     la = (C.c_int32 * max(1, len(layers)))(*layers)
     ptrs = (C.c_void_p * max(1, len(layers)))(*[b.data_ptr() for b in e_bufs])
@@ -268,10 +270,11 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
     config.validate_for(cfg.n_layers)
     n = ids.shape[0]
     e_map = _normalize_e(sender_e)
-    cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
-    logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
-    tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
     s = stream if stream is not None else torch.cuda.current_stream(receiver.device)
+    with torch.cuda.stream(s):  # outputs belong to the stream that writes them (allocator reuse)
+        cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
+        logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
+        tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
     ws = _workspace(receiver, n, s)
     groups = [x for g in config.groups for x in g]
     ga = (C.c_int32 * max(1, len(groups)))(*groups)
@@ -361,10 +364,11 @@ def token_selective_prefill(receiver: ModelWeights, tokens, sender_kv: LayerKV, 
     n = ids.shape[0]
     if sender_kv is None:
         raise CacheMissError(0, "kv", "sender cache missing layers")
-    cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
-    logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
-    tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
     s = stream if stream is not None else torch.cuda.current_stream(receiver.device)
+    with torch.cuda.stream(s):  # outputs belong to the stream that writes them (allocator reuse)
+        cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
+        logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
+        tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
     ws = _workspace(receiver, n, s)
     skv, odesc = sender_kv.desc(), cache.desc()
     ml, nsel = C.c_int32(-1), C.c_int32(0)
