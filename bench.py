@@ -169,78 +169,181 @@ def max_over_ranks(x: float, world: int) -> float:
 # ---------------------------------------------------------------------------
 
 
-def cpu_reference_sample(n: int, k: int, budget_s: float, max_steps: int | None = None):
-    """Time the reference algorithm on the host cores on a bounded sample.
-
-    One sample = one recomputed 8B-shaped layer over the full n-1 window +
-    one anchor layer (attending over n keys) + 1/8 of the lm head + one
-    reused layer's KV copy, extrapolated to the full consumer TTFT:
-    k*t_layer + L*t_anchor + 8*t_lm8 + (L-k)*t_copy.  Returns per-sample TTFT
-    estimates (seconds) and the thread count used.
-    """
+def cpu_env() -> dict:
+    """What the CPU numbers were measured on."""
     import numpy as np
-    from oracle import crosskv_oracle as O
+    env = {"cores": len(os.sched_getaffinity(0)), "numpy": np.__version__,
+           "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+           "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS")}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                env["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        env["blas"] = [{"lib": d.get("internal_api"), "version": d.get("version"), "threads": d.get("num_threads")}
+                       for d in threadpool_info() if d.get("user_api") == "blas"]
+    except Exception:  # informational only
+        pass
+    return env
 
-    d, H, G, D, F, V, L = (SHAPE[x] for x in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff",
-                                              "vocab_size", "n_layers"))
-    dims = O.Dims(1, d, H, G, D, F, V, n, 0)
-    rng = np.random.default_rng(0)
 
-    def mat(r, c, std):
-        return (rng.standard_normal((r, c), dtype=np.float32) * np.float32(std))
+class CpuSample:
+    """The reference algorithm on the host cores, on a bounded sample of the
+    8B-shaped consumer step (SURVEY §8d "CPU baseline timing").
 
-    lw = {"wq": mat(d, H * D, d ** -0.5), "wk": mat(d, G * D, d ** -0.5), "wv": mat(d, G * D, d ** -0.5),
-          "wo": mat(H * D, d, d ** -0.5), "w1": mat(d, F, d ** -0.5), "w2": mat(F, d, F ** -0.5),
-          "g_attn": np.ones(d, np.float32), "g_mlp": np.ones(d, np.float32)}
-    unembed8 = mat(d, V // 8, d ** -0.5)
-    P = n - 1
-    h = rng.standard_normal((P, d), dtype=np.float32)
-    kv_src = rng.standard_normal((2, G, P, D), dtype=np.float32)
-    samples = []
-    t_start = time.perf_counter()
-    while True:
+    The model is the reference block at Llama-3-8B width with TWO layers and the
+    full 128256-token lm head; one sample is a real 2-layer consumer partial
+    prefill at the full n, run op for op like the oracle's mixed_prefill
+    (model.py:574-638): layer 0 reused (its K/V copied from the sender
+    export), layer 1 recomputed over the n-1 window from E(1), the anchor row
+    through both layers over the mixed cache, the logits.  Every stage is
+    timed, so the 32-layer, k-recomputed TTFT is
+        t_copy * (L-k) + t_window * k + mean(t_anchor) * L + t_lm
+    (linear in L and k: SURVEY Appendix B measured 12 s/layer at n = 2048 for
+    both L = 1 and L = 2).  The window attention is the oracle port's blocked
+    BLAS matmuls; ``einsum_layer_s`` times the reference's own single-threaded
+    einsum attention (model.py:491-519) for one of the 8 KV groups of one
+    layer at the full n, times 8 (the groups are independent), for the
+    reference-faithful estimate."""
+
+    def __init__(self, n: int):
+        import numpy as np
+        from oracle import crosskv_oracle as O
+        self.O, self.np = O, np
+        d, H, G, D, F, V = (SHAPE[x] for x in ("d_model", "n_heads", "n_kv_heads", "head_dim", "d_ff", "vocab_size"))
+        self.dims = O.Dims(2, d, H, G, D, F, V, n, 0)
+        rng = np.random.default_rng(0)
+
+        def mat(r, c, std):
+            return rng.standard_normal((r, c), dtype=np.float32) * np.float32(std)
+
+        def layer():
+            return {"wq": mat(d, H * D, d ** -0.5), "wk": mat(d, G * D, d ** -0.5), "wv": mat(d, G * D, d ** -0.5),
+                    "wo": mat(H * D, d, d ** -0.5), "w1": mat(d, F, d ** -0.5), "w2": mat(F, d, F ** -0.5),
+                    "g_attn": np.ones(d, np.float32), "g_mlp": np.ones(d, np.float32)}
+
+        self.w = {"dims": self.dims, "layers": [layer(), layer()], "g_final": np.ones(d, np.float32),
+                  "embed": mat(V, d, 1.0), "unembed": mat(d, V, d ** -0.5)}
+        self.n, self.P = n, n - 1
+        self.ids = rng.integers(0, V, size=n, dtype=np.int64)
+        self.e1 = rng.standard_normal((self.P, d), dtype=np.float32)  # the sender's E at the transition layer
+        self.sk = rng.standard_normal((1, G, n, D), dtype=np.float32)  # the sender's layer-0 K/V export
+        self.sv = rng.standard_normal((1, G, n, D), dtype=np.float32)
+
+    def sample(self) -> dict:
+        O, np, w, P = self.O, self.np, self.w, self.P
+        G, D = self.dims.n_kv_heads, self.dims.head_dim
+        t = {}
         t0 = time.perf_counter()
-        _, kt, vt = O.block_forward(h, lw, dims, np.arange(P))
+        k_all = np.zeros((2, G, self.n, D), np.float32)
+        v_all = np.zeros_like(k_all)
+        k_all[0, :, :P] = self.sk[0, :, :P]  # reuse copy (model.py:602-603)
+        v_all[0, :, :P] = self.sv[0, :, :P]
         t1 = time.perf_counter()
-        O.block_forward(h[:1], lw, dims, np.array([P]), k_ctx=kt, v_ctx=vt)
+        _, kt, vt = O.block_forward(self.e1, w["layers"][1], self.dims, np.arange(P))  # full block, as _layer_window
+        k_all[1, :, :P], v_all[1, :, :P] = kt, vt
         t2 = time.perf_counter()
-        O.rms_norm(h[0], lw["g_attn"]) @ unembed8
+        h = w["embed"][self.ids[P]][None, :]
+        ta = []
+        for l in range(2):
+            s0 = time.perf_counter()
+            h, ko, vo = O.block_forward(h, w["layers"][l], self.dims, np.array([P]), k_ctx=k_all[l, :, :P],
+                                        v_ctx=v_all[l, :, :P])
+            k_all[l, :, P], v_all[l, :, P] = ko[:, 0], vo[:, 0]
+            ta.append(time.perf_counter() - s0)
         t3 = time.perf_counter()
-        dst = np.empty_like(kv_src)
-        dst[...] = kv_src
+        O.final_logits(h[0], w)
         t4 = time.perf_counter()
-        samples.append(k * (t1 - t0) + L * (t2 - t1) + 8 * (t3 - t2) + (L - k) * (t4 - t3))
-        if max_steps is not None and len(samples) >= max_steps:
+        return {"copy": t1 - t0, "window": t2 - t1, "anchor": sum(ta) / 2, "lm": t4 - t3, "total": t4 - t0}
+
+    @staticmethod
+    def ttft(s: dict, k: int, L: int = 32) -> float:
+        return s["copy"] * (L - k) + s["window"] * k + s["anchor"] * L + s["lm"]
+
+    def window_attention(self, einsum: bool) -> float:
+        """Seconds of one layer's causal window attention at the full n: one KV
+        group (R = H/G query heads) timed, times G."""
+        O, np, P = self.O, self.np, self.P
+        G, D, H = self.dims.n_kv_heads, self.dims.head_dim, self.dims.n_heads
+        R = H // G
+        rng = np.random.default_rng(1)
+        q = rng.standard_normal((P, R, D), dtype=np.float32)
+        k = rng.standard_normal((1, P, D), dtype=np.float32)
+        v = rng.standard_normal((1, P, D), dtype=np.float32)
+        pos = np.arange(P)
+        t0 = time.perf_counter()
+        if einsum:
+            O.attend_einsum(q, k, v, pos[None, :] <= pos[:, None])
+        else:
+            O.attend(q, k, v, pos)
+        return (time.perf_counter() - t0) * G
+
+
+def cpu_reference(n: int, k: int, budget_s: float, max_samples: int, warmup: int, einsum: bool) -> dict:
+    """Bounded CPU run: up to ``warmup`` untimed samples and ``max_samples``
+    timed ones, stopping when the next would exceed ``budget_s``.  Reports
+    exactly what ran."""
+    t_build = time.perf_counter()
+    cs = CpuSample(n)
+    build_s = time.perf_counter() - t_build
+    t_start = time.perf_counter()
+    done_warm, samples = 0, []
+    while True:
+        s = cs.sample()
+        if done_warm < warmup:
+            done_warm += 1
+        else:
+            samples.append(s)
+        elapsed = time.perf_counter() - t_start
+        if len(samples) >= max_samples or (samples and elapsed + s["total"] > budget_s):
             break
-        if time.perf_counter() - t_start + (t4 - t0) > budget_s:
-            break
-    threads = len(os.sched_getaffinity(0))
-    return samples, threads
+    med = {key: statistics.median(x[key] for x in samples) for key in samples[0]}
+    out = {"samples": len(samples), "warmup": done_warm, "sample_s": med["total"], "stage_s": med,
+           "ttft_s": CpuSample.ttft(med, k), "build_s": round(build_s, 2), "env": cpu_env()}
+    if einsum:
+        blas = cs.window_attention(einsum=False)
+        ein = cs.window_attention(einsum=True)
+        out["attention_layer_s"] = {"blas_port": blas, "reference_einsum": ein}
+        out["ttft_einsum_s"] = out["ttft_s"] + k * (ein - blas)
+    return out
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    total = args.steps + args.warmup
-    samples, threads = cpu_reference_sample(args.n, args.k, args.cpu_budget, max_steps=total)
-    timed = samples[args.warmup:] if len(samples) > args.warmup else samples[-1:]
-    ttft = statistics.median(timed)
+    r = cpu_reference(args.n, args.k, args.cpu_budget, max_samples=max(1, args.steps), warmup=min(args.warmup, 1),
+                      einsum=True)
+    ttft = r["ttft_s"]
     value = args.n / ttft
+    sample = (f"reference algorithm (oracle port of crosskv _mixed_prefill, numpy f32, BLAS window attention) on a "
+              f"2-layer 8B-width model at n={args.n}: one reused layer copied, one layer recomputed over the "
+              f"{args.n - 1}-row window, the anchor through both layers, the full lm head; stage times scaled to "
+              f"k={args.k} recomputed + {32 - args.k} reused + 32 anchor layers")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus,
-        "steps": len(timed), "warmup": min(args.warmup, len(samples) - len(timed)),
-        "ms_per_step": ttft * 1e3, "ttft_p50_ms": ttft * 1e3, "higher_is_better": True,
+        "steps": r["samples"], "warmup": r["warmup"], "requested": {"steps": args.steps, "warmup": args.warmup},
+        "ms_per_step": r["sample_s"] * 1e3, "ttft_p50_ms": ttft * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"8B-shaped consumer partial prefill, n={args.n}, k={args.k} of 32 recomputed "
                                "(BASELINE config 2)", "n_tokens": args.n, "recomputed_layers": args.k},
-        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": threads, "kind": "port",
-                         "sample": "oracle port of crosskv _mixed_prefill (numpy f32, BLAS): 1 recomputed layer "
-                                   f"over {args.n - 1} positions + 1 anchor layer + 1/8 lm head + 1 layer KV copy "
-                                   f"per step, extrapolated to k={args.k} recompute + 32 anchor layers"},
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": r["env"]["cores"], "kind": "port",
+                         "sample": sample, "stage_s": r["stage_s"], "env": r["env"],
+                         "attention_layer_s": r["attention_layer_s"],
+                         "value_einsum": args.n / r["ttft_einsum_s"],
+                         "ttft_einsum_ms": r["ttft_einsum_s"] * 1e3,
+                         "note": "value uses the port's BLAS window attention; value_einsum replaces it with the "
+                                 "reference's own single-threaded einsum attention (model.py:491-519), timed on one "
+                                 "KV group at the full n and scaled by 8"},
         "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    if len(samples) < total:
-        line["note"] = f"CPU budget {args.cpu_budget}s allowed {len(samples)} of {total} steps"
+    if r["samples"] < args.steps or r["warmup"] < args.warmup:
+        line["note"] = (f"bounded CPU run: {r['samples']} timed + {r['warmup']} warm-up samples of the requested "
+                        f"{args.steps} + {args.warmup} fit the {args.cpu_budget:.0f} s budget; ms_per_step is one "
+                        "sample's wall time, ttft_p50_ms the 32-layer estimate from its stage times")
     print(json.dumps(line), flush=True)
 
 
@@ -425,28 +528,38 @@ def run_ours(args, world, rank, local):
     sel_ttft = max_over_ranks(statistics.median(sel_ms), world)
     del sel_cache
 
-    # ---- greedy first-token agreement, consumer partial prefill vs its own full
-    # prefill, over a few 8K prefixes (outside the timed region)
-    agree, agree_sel, n_pref = 0, 0, 4
+    # ---- quality on a LOSSY pair (outside the timed region): B_q = A + small noise on
+    # EVERY layer + the large noise on the recomputed block, so the reused layers are
+    # not the receiver's own and agreement can fall below 1 (the timed pair's
+    # weight values do not affect its time).  First-token agreement of the
+    # partial prefill and of the token-selective baseline vs the receiver's own
+    # full prefill over a few 8K prefixes, and the reference's quality proxy
+    # (agreement_score, model.py:810-831) for the recompute set and for full reuse.
+    Bq = P.random_model(cfg, seed=3000 + rank, device=dev, base=A, perturb_layers=range(L), eps=0.03)
+    Bq = P.random_model(cfg, seed=4000 + rank, device=dev, base=Bq, perturb_layers=range(L - k, L), eps=0.5)
+    agree, agree_sel, agree_reuse, n_pref = 0, 0, 0, 4
     for i in range(n_pref):
         ids_i = np.random.default_rng(100 + i).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
         t_i = torch.from_numpy(ids_i).to(dev)
         prod_i = P.full_prefill(A, ids_i, e_layers=rc.transition_layers, tokens_dev=t_i)
-        mixed_i = P.partial_prefill(B, ids_i, rc, prod_i.kv, prod_i.e_map(), tokens_dev=t_i)
-        own_i = P.full_prefill(B, ids_i, e_layers=(), tokens_dev=t_i)
-        sel_i = P.token_selective_prefill(B, ids_i, prod_i.kv, args.sel_ratio, tokens_dev=t_i)
+        mixed_i = P.partial_prefill(Bq, ids_i, rc, prod_i.kv, prod_i.e_map(), tokens_dev=t_i)
+        reuse_i = P.partial_prefill(Bq, ids_i, P.RecomputeConfig.none(), prod_i.kv, {}, tokens_dev=t_i)
+        own_i = P.full_prefill(Bq, ids_i, e_layers=(), tokens_dev=t_i)
+        sel_i = P.token_selective_prefill(Bq, ids_i, prod_i.kv, args.sel_ratio, tokens_dev=t_i)
         agree += int(mixed_i.token == own_i.token)
         agree_sel += int(sel_i.token == own_i.token)
-        del prod_i, mixed_i, own_i, sel_i
-    # the reference's quality proxy (agreement_score, model.py:810-831): greedy
-    # decode over a 32-token horizon after the partial prefill vs the receiver's own
+        agree_reuse += int(reuse_i.token == own_i.token)
+        del prod_i, mixed_i, own_i, sel_i, reuse_i
     from paper_2411_02820_b200.quality import agreement_score
     t0 = time.perf_counter()
-    ag = agreement_score(A, B, np.random.default_rng(100).integers(0, cfg.vocab_size, size=n, dtype=np.int64), rc,
-                         horizon=32)
+    q_ids = np.random.default_rng(100).integers(0, cfg.vocab_size, size=n, dtype=np.int64)
+    ag = agreement_score(A, Bq, q_ids, rc, horizon=32)
+    ag_reuse = agreement_score(A, Bq, q_ids, P.RecomputeConfig.none(), horizon=32)
     torch.cuda.synchronize()
     agreement = {"score": ag.score, "first_divergence": ag.first_divergence, "horizon": 32,
-                 "wall_s": round(time.perf_counter() - t0, 3)}
+                 "full_reuse_score": ag_reuse.score, "wall_s": round(time.perf_counter() - t0, 3),
+                 "pair": "lossy: B = A + 0.03 noise on every layer + 0.5 on the recomputed block"}
+    del Bq
 
     # ---- greedy decode after the partial prefill (f1: decode_greedy, model.py:751-788):
     # each token is one anchor pass over the paged cache (every weight + every
@@ -539,8 +652,10 @@ def run_ours(args, world, rank, local):
                                 "note": "CacheBlend-style baseline (model.py:682-743): top-ratio positions by "
                                         "layer-0 KV deviation recomputed through all layers"},
             "first_token": token,
-            "first_token_agreement": {"partial_vs_own_full_prefill": agree, "prefixes": n_pref,
-                                      "note": "random-init pair: B = A + noise on the recomputed suffix"},
+            "first_token_agreement": {"partial_vs_own_full_prefill": agree, "full_reuse_vs_own": agree_reuse,
+                                      "prefixes": n_pref,
+                                      "note": "lossy pair: B = A + 0.03 noise on every layer + 0.5 on the "
+                                              "recomputed block (reused layers are not the receiver's own)"},
             "agreement_score": agreement,
             "decode": {"steps": dsteps, "context": n, "ms_per_token": dec_ms, "tok_s": 1e3 / dec_ms,
                        "gbs": kern["anchor_pass"]["bytes"] / dec_ms / 1e6,
@@ -564,13 +679,14 @@ def run_ours(args, world, rank, local):
         line["kernels"]["attention_prefill"]["frac_bf16"] = round(kern["attention_prefill"]["tflops"] / pk["bf16"], 4)
         line["kernels"]["gemm_w2_resid"]["frac_bf16"] = round(kern["gemm_w2_resid"]["tflops"] / pk["bf16"], 4)
         if not args.no_cpu_baseline and world == 1:
-            samples, threads = cpu_reference_sample(n, k, min(args.cpu_budget, 60.0), max_steps=1)
-            v = n / statistics.median(samples)
+            r = cpu_reference(n, k, min(args.cpu_budget, 60.0), max_samples=1, warmup=0, einsum=False)
             line["cpu_baseline"] = {
-                "value": v, "unit": "tok/s", "cores": threads, "kind": "port",
-                "sample": f"oracle port (numpy f32/BLAS) of the reference path: 1 recomputed layer over {n - 1} "
-                          f"positions + 1 anchor layer + 1/8 lm head + 1 layer KV copy, extrapolated to "
-                          f"k={k} + 32 anchor layers"}
+                "value": n / r["ttft_s"], "unit": "tok/s", "cores": r["env"]["cores"], "kind": "port",
+                "sample": f"one 2-layer 8B-width consumer partial prefill at n={n} on the oracle port (numpy f32, "
+                          f"BLAS): 1 reused + 1 recomputed layer, anchor through both, full lm head "
+                          f"({r['sample_s']:.1f} s), stage times scaled to k={k} + 32 anchor layers; the "
+                          "reference's einsum attention is timed by --impl reference",
+                "stage_s": r["stage_s"], "env": r["env"]}
         print(json.dumps(line), flush=True)
 
 
@@ -708,18 +824,70 @@ def run_fanout(args, world, rank, local):
             if i >= args.warmup:
                 e2e.append(time.perf_counter() - w0)
     e2e_s = max_over_ranks(statistics.median(e2e), world)
-    # NVLink pull rate of the ingest alone (consumer 1): reused KV bytes crossing the link
+    # The §8(d) overlap metric on every consumer: TTFT over the mapped export
+    # (NVLink, TTFT_3) vs the same step on a local copy of the export (TTFT_2,
+    # same recompute set), and the transfer alone (T_xfer: the reused layers'
+    # KV pulled over the link by the ingest kernel + E at the transition layer):
+    # hidden = 1 - (TTFT_3 - TTFT_2) / T_xfer.  Single requests, graphed,
+    # interleaved so both see the same clocks.
     link = None
-    if args.transport == "p2p" and rank == 1:
-        reused = list(range(L - k))
-        xfer = len(reused) * 2 * cfg.n_kv_heads * cfg.head_dim * (n - 1) * 2
+    if args.transport == "p2p" and not producer:
         from paper_2411_02820_b200 import ops
-        d = cache.desc()
-        s = remote.kv.desc()
-        ms = time_kernel(lambda: ops.kv_ingest(s, d, reused, n - 1, cfg.n_kv_heads, cfg.head_dim, stream=stream),
-                         5, stream)
-        link = {"kernel": "kv_ingest (P2P pull over NVLink)", "ms": ms, "bytes": xfer, "gbs": xfer / ms / 1e6}
-    links = [None]
+        reused = list(range(L - k))
+        local_kv, local_e = remote.local_copy(stream)
+        torch.cuda.synchronize()
+
+        def one(kv, e):
+            return lambda: P.partial_prefill(B, ids, rc, kv, e, out=cache, stream=stream, copy_stream=side,
+                                             tokens_dev=tok_dev)
+
+        graphs = {}
+        for name, fn in (("remote", one(remote.kv, remote.e_map)), ("local", one(local_kv, local_e))):
+            with torch.cuda.stream(stream):
+                fn()
+            torch.cuda.synchronize()
+            if args.graph:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    fn()
+                graphs[name] = g.replay
+            else:
+                graphs[name] = fn
+        times = {"remote": [], "local": []}
+        for i in range(args.warmup + args.steps):
+            for name in ("remote", "local"):
+                a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_ev.record(stream)
+                with torch.cuda.stream(stream):
+                    graphs[name]()
+                b_ev.record(stream)
+                torch.cuda.synchronize()
+                if i >= args.warmup:
+                    times[name].append(a_ev.elapsed_time(b_ev))
+        scratch = P.PagedKV.allocate(cfg, n, dev)
+        e_dst = {l: torch.empty_like(e.hidden) for l, e in local_e.items()}
+        from paper_2411_02820_b200.transport import peer_view
+        e_src = {l: peer_view(e.hidden.data_ptr(), e.hidden.shape, torch.float32) for l, e in remote.e_map.items()}
+        sd, rd = scratch.desc(), remote.kv.desc()
+
+        def pull():
+            for l in e_dst:
+                e_dst[l].copy_(e_src[l], non_blocking=True)
+            ops.kv_ingest(rd, sd, reused, n - 1, cfg.n_kv_heads, cfg.head_dim, stream=stream)
+
+        with torch.cuda.stream(stream):
+            t_xfer = time_kernel(pull, 5, stream)
+            t_kv = time_kernel(lambda: ops.kv_ingest(rd, sd, reused, n - 1, cfg.n_kv_heads, cfg.head_dim,
+                                                     stream=stream), 5, stream)
+        kv_bytes = len(reused) * 2 * cfg.n_kv_heads * cfg.head_dim * (n - 1) * 2
+        e_bytes = sum(int(t.nbytes) for t in e_dst.values())
+        t3, t2 = statistics.median(times["remote"]), statistics.median(times["local"])
+        link = {"rank": rank, "kernel": "kv_ingest (P2P pull over NVLink) + E copy", "ttft_remote_ms": t3,
+                "ttft_local_ms": t2, "t_xfer_ms": t_xfer, "xfer_bytes": kv_bytes + e_bytes,
+                "gbs": (kv_bytes + e_bytes) / t_xfer / 1e6, "kv_ms": t_kv, "kv_gbs": kv_bytes / t_kv / 1e6,
+                "hidden_fraction": 1.0 - (t3 - t2) / t_xfer}
+        del local_kv, local_e, scratch, e_dst, graphs
+    links = [link]
     if world > 1:
         gathered = [None] * world
         dist.all_gather_object(gathered, link)
@@ -743,14 +911,23 @@ def run_fanout(args, world, rank, local):
             "gpu_launches": launches,
             "e2e": {"value": nc * n / e2e_s if e2e_s > 0 else None, "unit": "tok/s", "ttft_p50_ms": e2e_s * 1e3,
                     "h2d_bytes_per_step": 8 * n * nc, "d2h_bytes_per_step": (4 * cfg.vocab_size + 4) * nc},
+            "overlap": ({"hidden_fraction": min(x["hidden_fraction"] for x in links),
+                         "per_consumer": [{kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in x.items()}
+                                          for x in links],
+                         "definition": "1 - (TTFT_remote - TTFT_local) / T_xfer (SURVEY 8d): TTFT_remote on the "
+                                       "producer's mapped export, TTFT_local on a local copy, same recompute set; "
+                                       "T_xfer = reused-layer KV pulled by the ingest kernel + E copy, alone",
+                         "target": 0.9} if links else None),
             "roofline": (({"bound": "hbm", "kernel": links[0]["kernel"] + " (same device: debug run, not NVLink)",
-                           "achieved": 2 * links[0]["gbs"], "peak": peaks()["hbm"], "unit": "GB/s",
-                           "frac": 2 * links[0]["gbs"] / peaks()["hbm"], "traffic": None,
+                           "achieved": 2 * links[0]["kv_gbs"], "peak": peaks()["hbm"], "unit": "GB/s",
+                           "frac": 2 * links[0]["kv_gbs"] / peaks()["hbm"], "traffic": None,
                            "peak_source": f"{peaks()['src']} HBM copy (read + write counted)"}
                           if args.same_device else
-                          {"bound": "nvlink", "kernel": links[0]["kernel"], "achieved": links[0]["gbs"],
-                           "peak": 770.0, "unit": "GB/s", "frac": links[0]["gbs"] / 770.0, "traffic": None,
-                           "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900"})
+                          {"bound": "nvlink", "kernel": "kv_ingest (P2P pull over NVLink)",
+                           "achieved": links[0]["kv_gbs"], "peak": 900.0, "unit": "GB/s",
+                           "frac": links[0]["kv_gbs"] / 900.0, "traffic": None,
+                           "peak_source": "NVLink 5 per-direction spec (SURVEY 8d); bytes = reused-layer KV read "
+                                          "from the peer"})
                          if links else None),
             "clocks": clocks.summary(),
         }

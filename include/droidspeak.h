@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 1
+#define DS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define DS_API __attribute__((visibility("default")))
@@ -125,6 +125,18 @@ DS_API int ds_anchor_placement(const ds_dims* dims, int32_t n_tokens, const void
 DS_API int ds_anchor_timeline(const ds_dims* dims, int32_t n_tokens, const void* workspace, uint64_t* ns_out,
                               int32_t cap);
 
+/* Anchor-shape override for measurements and tests (process-wide):
+ * 0 = by workload (the persistent co-resident kernel when k * P >= 800 * L),
+ * 1 = always the persistent kernel when it fits, 2 = always the per-launch
+ * kernels.  Both shapes run the same arithmetic (bit-identical results).
+ * The DS_ANCHOR_SHAPE environment variable sets the initial value.  Returns
+ * the previous value, or -1 for an unknown shape. */
+DS_API int ds_set_anchor_shape(int32_t shape);
+/* Fused calls that ran the per-launch anchor because another call's fused step
+ * (persistent anchor) was still in flight on the same GPU on other streams
+ * (one persistent anchor per GPU at a time).  Process-wide count. */
+DS_API unsigned long long ds_fused_fallbacks(void);
+
 /* Bytes of device workspace ds_partial_prefill / ds_full_prefill need for n tokens. */
 DS_API size_t ds_workspace_size(const ds_dims* dims, int32_t n_tokens);
 
@@ -171,7 +183,7 @@ DS_API int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const 
 
 /* Selective recompute of ONE group [a, b] over the window positions 0..n-2
  * (model.py:607-625): h = embed[tokens[0..n-1)] (a == 0, tokens_dev required)
- * or the sender's E at layer a (seed: bf16 [seed_positions >= n-1][d], may live
+ * or the sender's E at layer a (seed: f32 [seed_positions >= n-1][d], may live
  * in a peer GPU's HBM); layers a..b run over the window and write K/V of
  * positions 0..n-2 into out_kv.  The E read is the first kernel of the group, so
  * a peer-resident seed is pulled over NVLink by the compute itself. */
@@ -191,10 +203,13 @@ DS_API int ds_anchor(const ds_model* m, const int64_t* tokens_dev, int32_t n_tok
  * sender's K/V; the ceil(ratio * (n-1)) window positions whose receiver layer-0
  * K/V deviate most from the sender's (L2 over heads x head_dim, ties to the
  * lowest position) are recomputed through the whole stack, then the anchor.
- * *n_selected receives the count.  Misses: layer count first, then positions
+ * *n_selected receives the count.  ratio is a double and the count is
+ * ceil(ratio * (n-1)) in double precision, as the reference's math.ceil (a
+ * float32 ratio would select one position more whenever ratio * (n-1) is an
+ * integer in double, e.g. 0.1 * 10).  Misses: layer count first, then positions
  * (CacheMissError(layer, "kv")). */
 DS_API int ds_token_selective_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev,
-                                      int32_t n_tokens, const ds_kv_cache* sender_kv, float ratio,
+                                      int32_t n_tokens, const ds_kv_cache* sender_kv, double ratio,
                                       const ds_kv_cache* out_kv, float* logits_out, int32_t* token_out,
                                       int32_t* n_selected, void* workspace, size_t workspace_bytes, void* stream,
                                       int32_t* miss_layer);

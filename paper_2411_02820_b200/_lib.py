@@ -19,6 +19,8 @@ MISS_KIND = {1: "kv", 2: "e"}
 # epilogue modes of ds_gemm
 EPI_STORE_BF16, EPI_RESID_F32, EPI_SILU_BF16, EPI_QKV_ROPE, EPI_STORE_F32, EPI_SWIGLU_BF16 = range(6)
 MLP_KINDS = {"ungated": 0, "swiglu": 1}
+ABI_VERSION = 2  # include/droidspeak.h DS_ABI_VERSION
+ANCHOR_SHAPES = {"auto": 0, "persistent": 1, "launch": 2}
 
 
 class Dims(C.Structure):
@@ -68,6 +70,8 @@ def lib() -> C.CDLL:
             "ds_anchor_placement": (I32, [C.POINTER(Dims), I32, P, P, I32]),
             "ds_anchor_timeline": (I32, [C.POINTER(Dims), I32, P, P, I32]),
             "ds_workspace_size": (SZ, [C.POINTER(Dims), I32]),
+            "ds_set_anchor_shape": (I32, [I32]),
+            "ds_fused_fallbacks": (C.c_uint64, []),
             "ds_kv_ingest": (I32, [C.POINTER(KvCache), C.POINTER(KvCache), P, I32, I32, I32, I32, P,
                                    C.POINTER(I32)]),
             "ds_partial_prefill": (I32, [C.POINTER(Model), P, P, I32, P, I32, C.POINTER(KvCache),
@@ -76,7 +80,7 @@ def lib() -> C.CDLL:
             "ds_full_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), P, I32, P, P, P, P, SZ, P, P]),
             "ds_recompute_group": (I32, [C.POINTER(Model), P, I32, I32, I32, P, I32, C.POINTER(KvCache), P, SZ, P]),
             "ds_anchor": (I32, [C.POINTER(Model), P, I32, C.POINTER(KvCache), P, P, P, SZ, P]),
-            "ds_token_selective_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), C.c_float,
+            "ds_token_selective_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), C.c_double,
                                                  C.POINTER(KvCache), P, P, C.POINTER(I32), P, SZ, P, C.POINTER(I32)]),
             "ds_decode_greedy": (I32, [C.POINTER(Model), C.POINTER(KvCache), I32, P, I32, P, P, SZ, P]),
             "ds_ipc_export": (I32, [P, P, C.POINTER(C.c_uint64)]),
@@ -90,7 +94,7 @@ def lib() -> C.CDLL:
             fn = getattr(h, name)
             fn.restype = res
             fn.argtypes = args
-        if h.ds_abi_version() != 1:
+        if h.ds_abi_version() != ABI_VERSION:
             raise RuntimeError("droidspeak ABI version mismatch")
         _lib = h
     return _lib
@@ -113,4 +117,20 @@ def check(rc: int, miss_layer: int | None = None, miss_kind: int | None = None) 
 EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_launch_count", "ds_workspace_size", "ds_kv_ingest", "ds_partial_prefill",
                     "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill", "ds_recompute_group",
                     "ds_anchor", "ds_token_selective_prefill", "ds_decode_greedy", "ds_ipc_export", "ds_ipc_open", "ds_ipc_close",
-                    "ds_trace_begin", "ds_trace_end", "ds_anchor_placement", "ds_anchor_timeline")
+                    "ds_trace_begin", "ds_trace_end", "ds_anchor_placement", "ds_anchor_timeline",
+                    "ds_set_anchor_shape", "ds_fused_fallbacks")
+
+
+class anchor_shape:
+    """Context manager forcing the anchor shape (ds_set_anchor_shape): "auto",
+    "persistent" or "launch".  Process-wide; for measurements and tests."""
+
+    def __init__(self, shape: str):
+        self.shape = ANCHOR_SHAPES[shape]
+
+    def __enter__(self):
+        self.prev = lib().ds_set_anchor_shape(self.shape)
+        return self
+
+    def __exit__(self, *exc):
+        lib().ds_set_anchor_shape(self.prev)

@@ -488,8 +488,8 @@ __global__ void token_copy_kernel(const int32_t* src, int32_t* dst32, int64_t* d
 
 int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaStream_t stream) {
   count_launch();
-  static const bool c0 = prefer_max_smem(token_copy_kernel);
-  (void)c0;
+  static PerDevice carve;
+  prefer_max_smem_once(token_copy_kernel, carve);
   token_copy_kernel<<<1, 1, 0, stream>>>(src, dst32, dst64);
   return launch_status();
 }
@@ -514,14 +514,8 @@ static int gemv_tma_launch_t(const GemvArgs& a, cudaStream_t stream, int ctas_pe
   if (slots < 2) return DS_ERR_INVALID;
   const int smem = slots * SLOT + xbytes;
   auto kern = gemv_tma_kernel<KS>;
-  static int attr = 0;
-  if (smem > attr) {
-    if (int rc_ = launch_status(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)))
-      return rc_;
-    attr = smem;
-  }
-  static const bool c0 = prefer_max_smem(kern);
-  (void)c0;
+  static PerDevice attr;
+  if (int rc_ = launch_status(ensure_smem_attr(kern, smem, attr))) return rc_;
   const int tiles = a.N / GEMV_ROWS, cap = num_sms() * ctas_per_sm;
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
@@ -559,11 +553,8 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged) {
     if (gemv_tma_launch(a, stream) == DS_OK) return DS_OK;
   const int tiles = a.N / GEMV_ROWS;
   const int smem = a.K * 2;
-  static int attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    if (int rc_ = launch_status(cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return rc_;
-    attr = smem;
-  }
+  static PerDevice attr;
+  if (int rc_ = launch_status(ensure_smem_attr(gemv_kernel, smem > 48 * 1024 ? smem : 48 * 1024, attr))) return rc_;
   static int per_sm_cap = -1;
   if (per_sm_cap < 0) {
     const char* v = getenv("DS_GEMV_PER_SM");  // experiments
@@ -575,15 +566,15 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged) {
   const int cap = num_sms() * per_sm;
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
-  static const bool c0 = prefer_max_smem(gemv_kernel);
-  (void)c0;
+  static PerDevice carve;
+  prefer_max_smem_once(gemv_kernel, carve);
   return launch_status(launch_pdl(gemv_kernel, dim3(grid), dim3(GEMV_THREADS), smem, stream, a));
 }
 
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream) {
   count_launch();
-  static const bool c0 = prefer_max_smem(argmax_finalize_kernel);
-  (void)c0;
+  static PerDevice carve;
+  prefer_max_smem_once(argmax_finalize_kernel, carve);
   argmax_finalize_kernel<<<1, 1, 0, stream>>>(packed, token, token64);
   return launch_status();
 }
@@ -1254,15 +1245,9 @@ static cudaError_t attn_tma_launch_t(const AttnArgs& a, int smem, cudaStream_t s
   static const int prefetch = env_int("DS_ATT_PREFETCH", 0);  // bit 0 L2 prefetch; bits 1-3 timing experiments
   const int slots = slots_env < 2 ? 2 : (slots_env > ATT_SLOTS_MAX ? ATT_SLOTS_MAX : slots_env);
   auto kern = attn_decode_tma_kernel<D, R>;
-  static int attr = 0;
+  static PerDevice attr;
   const int total = slots * ATT_PIECE * D * 2 + smem;
-  if (total > attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, total);
-    if (e != cudaSuccess) return e;
-    attr = total;
-  }
-  static const bool c0 = prefer_max_smem(kern);
-  (void)c0;
+  if (cudaError_t e = ensure_smem_attr(kern, total, attr)) return e;
   return launch_pdl(kern, dim3(a.n_kv_heads * a.splits), dim3(ATT_TTHREADS), total, stream, a, slots, prefetch);
 }
 
@@ -1279,8 +1264,8 @@ static bool attn_tma_enabled() {
 template <int D, int R>
 static cudaError_t attn_launch_t(const AttnArgs& a, int smem, cudaStream_t stream) {
   auto kern = attn_decode_kernel<D, R>;
-  static const bool c0 = prefer_max_smem(kern);
-  (void)c0;
+  static PerDevice carve;
+  prefer_max_smem_once(kern, carve);
   return launch_pdl(kern, dim3(a.n_kv_heads * a.splits), dim3(ATT_THREADS), smem, stream, a);
 }
 
@@ -1561,13 +1546,8 @@ bool anchor_persistent_fits(const ds_dims& d, int n_keys) {
 template <int D, int R>
 static cudaError_t anchor_launch_t(const AnchorArgs& a, int smem, cudaStream_t stream) {
   auto kern = anchor_persistent_kernel<D, R>;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kAnchorSmemMax);
-    if (e != cudaSuccess) return e;
-    prefer_max_smem(kern);
-    init = true;
-  }
+  static PerDevice smem_set;
+  if (cudaError_t e = ensure_smem_attr(kern, kAnchorSmemMax, smem_set)) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(num_sms() * a.per_sm);
   cfg.blockDim = dim3(GEMV_THREADS);

@@ -9,6 +9,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -608,6 +610,75 @@ int check_cache(const ds_kv_cache* c, const ds_dims& d, int n, const char* what)
   return DS_OK;
 }
 
+// Anchor-shape override (ds_set_anchor_shape; initial value from DS_ANCHOR_SHAPE).
+std::atomic<int> g_anchor_shape{-1};
+int anchor_shape() {
+  int v = g_anchor_shape.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("DS_ANCHOR_SHAPE");
+    v = !e ? 0 : (e[0] == 'p' ? 1 : (e[0] == 'l' ? 2 : 0));
+    int expect = -1;
+    g_anchor_shape.compare_exchange_strong(expect, v);
+    v = g_anchor_shape.load(std::memory_order_relaxed);
+  }
+  return v;
+}
+
+// One persistent (co-resident) anchor in flight per GPU.  The persistent
+// kernel spins on its own recompute's GEMM counters, which is safe beside any
+// other kernel of this library (each fits beside one anchor CTA per SM) but
+// not beside a second persistent anchor: two of them could hold the slots
+// each other's GEMMs need.  A fused call therefore takes the per-device slot;
+// while another call's fused step (on other streams) has not finished on the
+// GPU, a new call runs the per-launch anchor instead (event waits, no spins;
+// same arithmetic, same bits).  Calls on the same stream pair are ordered
+// behind the previous one and keep the fused shape.  Under stream capture the
+// slot is neither checked nor armed: the replays' order is the caller's.
+struct FusedSlot {
+  std::mutex mu;
+  cudaEvent_t done = nullptr;
+  cudaStream_t cs = nullptr, xs = nullptr;
+  bool armed = false;
+};
+constexpr int kMaxDevices = 64;
+FusedSlot g_fused[kMaxDevices];
+std::atomic<unsigned long long> g_fused_denied{0};
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  return dev % kMaxDevices;
+}
+
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+}
+
+bool fused_slot_free(cudaStream_t cs, cudaStream_t xs) {
+  if (capturing(cs)) return true;
+  FusedSlot& f = g_fused[current_device()];
+  std::lock_guard<std::mutex> lk(f.mu);
+  if (!f.armed || (f.cs == cs && f.xs == xs)) return true;
+  if (cudaEventQuery(f.done) == cudaErrorNotReady) {
+    g_fused_denied.fetch_add(1, std::memory_order_relaxed);
+    return false;
+  }
+  return true;
+}
+
+int fused_slot_arm(cudaStream_t cs, cudaStream_t xs) {
+  if (capturing(cs)) return DS_OK;
+  FusedSlot& f = g_fused[current_device()];
+  std::lock_guard<std::mutex> lk(f.mu);
+  if (!f.done && cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming) != cudaSuccess) return cuda_fail("event");
+  if (cudaEventRecord(f.done, cs) != cudaSuccess) return cuda_fail("event record");
+  f.cs = cs;
+  f.xs = xs;
+  f.armed = true;
+  return DS_OK;
+}
+
 // The prefill after validation, shared by ds_partial_prefill and
 // ds_full_prefill (= every layer recomputed, no sender: the reference's
 // full_prefill is _mixed_prefill over the same window + anchor structure,
@@ -638,14 +709,11 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
   // k * P ~ 800 * L recomputed row-layers.
   long long recomputed = 0;
   for (int l = 0; l < L; ++l) recomputed += covered[l];
-  // DS_ANCHOR_SHAPE=persistent|launch overrides the rule (crossover measurements)
-  static int shape = -1;
-  if (shape < 0) {
-    const char* e = getenv("DS_ANCHOR_SHAPE");
-    shape = !e ? 0 : (e[0] == 'p' ? 1 : (e[0] == 'l' ? 2 : 0));
-  }
+  // DS_ANCHOR_SHAPE=persistent|launch / ds_set_anchor_shape override the rule (crossover measurements, tests)
+  const int shape = anchor_shape();
   const bool fused = anchor_persistent_fits(d, n) &&
-                     (shape == 1 || (shape == 0 && recomputed * P >= (long long)kFuseRowLayers * L));
+                     (shape == 1 || (shape == 0 && recomputed * P >= (long long)kFuseRowLayers * L)) &&
+                     xs != cs && fused_slot_free(cs, xs);
   std::vector<char> reused_flag(L, 0);
   for (int l : reused) reused_flag[l] = 1;
   AnchorPlan plan;
@@ -722,6 +790,7 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
   if (rc) return rc;
   cudaEventRecord(ev_join, xs);
   cudaStreamWaitEvent(cs, ev_join, 0);
+  if (fused) return fused_slot_arm(cs, xs);
   return DS_OK;
 }
 
@@ -730,6 +799,13 @@ int prefill_core(Ctx& c, const int64_t* tok, int n, const int32_t* groups, int n
 extern "C" {
 
 int ds_abi_version(void) { return DS_ABI_VERSION; }
+unsigned long long ds_fused_fallbacks(void) { return g_fused_denied.load(std::memory_order_relaxed); }
+int ds_set_anchor_shape(int32_t shape) {
+  if (shape < 0 || shape > 2) return -1;
+  const int prev = anchor_shape();
+  g_anchor_shape.store(shape, std::memory_order_relaxed);
+  return prev;
+}
 int ds_anchor_placement(const ds_dims* dims, int32_t n_tokens, const void* workspace, int32_t* sm_out, int32_t cap) {
   g_err.clear();
   if (!dims || !workspace || !sm_out || n_tokens < 1) return fail(DS_ERR_INVALID, "bad placement arguments"), -1;
@@ -802,7 +878,7 @@ int ds_kv_ingest(const ds_kv_cache* src, const ds_kv_cache* dst, const int32_t* 
 }
 
 int ds_token_selective_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t* tokens_dev,
-                               int32_t n_tokens, const ds_kv_cache* sender_kv, float ratio, const ds_kv_cache* out_kv,
+                               int32_t n_tokens, const ds_kv_cache* sender_kv, double ratio, const ds_kv_cache* out_kv,
                                float* logits_out, int32_t* token_out, int32_t* n_selected, void* workspace,
                                size_t workspace_bytes, void* stream, int32_t* miss_layer) {
   g_err.clear();
@@ -810,7 +886,7 @@ int ds_token_selective_prefill(const ds_model* m, const int64_t* tokens_host, co
   const ds_dims& d = m->dims;
   int rc;
   if ((rc = check_dims(d))) return rc;
-  if (!(ratio > 0.f && ratio <= 1.f)) return fail(DS_ERR_INVALID, "ratio must lie in (0, 1], got %g", (double)ratio);
+  if (!(ratio > 0.0 && ratio <= 1.0)) return fail(DS_ERR_INVALID, "ratio must lie in (0, 1], got %g", ratio);
   if ((rc = check_tokens(d, tokens_host, n_tokens))) return rc;
   const int L = d.n_layers, n = n_tokens, P = n - 1;
   // sender checks in the reference's order (model.py:699-702)
@@ -829,7 +905,7 @@ int ds_token_selective_prefill(const ds_model* m, const int64_t* tokens_host, co
   Workspace w = carve(d, n, workspace);
   if (!workspace || workspace_bytes < w.bytes)
     return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes);
-  const int n_sel = (int)ceil((double)ratio * P);
+  const int n_sel = (int)ceil(ratio * P);  // math.ceil(ratio * window) in double (model.py:715)
   if (n_selected) *n_selected = n_sel;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t* tok = stage_tokens(tokens_host, tokens_dev, n, w, s);

@@ -401,11 +401,8 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
     return launch_status(cudaErrorInvalidValue);
   FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, q_pos, head_stride / D, page_stride / D, table, o, ldo,
              (float)(1.4426950408889634 / sqrt((double)D))};
-  static bool set = false;
-  if (!set) {
-    if (int rc_ = launch_status(cudaFuncSetAttribute(fa_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL))) return rc_;
-    set = true;
-  }
+  static PerDevice attr;
+  if (int rc_ = launch_status(ensure_smem_attr(fa_tc_kernel<D>, L::TOTAL, attr))) return rc_;
   dim3 grid(n_heads, (n_q + 2 * FA_BM - 1) / (2 * FA_BM));
   count_launch();
   return launch_status(launch_pdl(fa_tc_kernel<D>, grid, dim3(FA_THREADS), L::TOTAL, stream, tq, tk, tv, a));

@@ -623,12 +623,13 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, long long rows, long long 
 }
 
 int num_sms() {
-  static int n = 0;
+  static PerDevice cache;
+  int& n = cache();
   if (!n) {
-    int dev = 0;
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n = v > 0 ? v : 148;
   }
   return n;
 }
@@ -638,12 +639,8 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
                                  cudaStream_t stream, int max_ctas) {
   using L = GemmSmem<BN, STAGES>;
   auto kern = gemm_tcgen05_kernel<BN, STAGES>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static PerDevice attr;
+  if (cudaError_t e = ensure_smem_attr(kern, L::TOTAL, attr)) return e;
   const int tiles = ((epi.M + GEMM_BM - 1) / GEMM_BM) * ((epi.N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
@@ -676,13 +673,8 @@ unsigned int gemm_done_target(int M, int N) {
 
 static cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, int K, const GemmEpi& epi,
                                    cudaStream_t stream, int max_ctas) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Smem::TOTAL);
-    if (e != cudaSuccess) return e;
-    prefer_max_smem(gemm_tc2_kernel);
-    attr_set = true;
-  }
+  static PerDevice smem_set;
+  if (cudaError_t e = ensure_smem_attr(gemm_tc2_kernel, Gemm2Smem::TOTAL, smem_set)) return e;
   const int tiles = ((epi.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((epi.N + PAIR_BN - 1) / PAIR_BN);
   int pairs = num_sms() / 2;
   if (max_ctas > 0 && pairs > max_ctas / 2) pairs = max_ctas / 2 > 0 ? max_ctas / 2 : 1;

@@ -175,11 +175,8 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   // a persistent tcgen05 GEMM of the concurrent recompute
   const int stages = background ? 2 : INGEST_STAGES_MAX;
   const int smem = stages * stage_bytes;
-  static int attr_smem = 0;
-  if (smem > attr_smem) {
-    if (int rc_ = launch_status(cudaFuncSetAttribute(kv_ingest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return rc_;
-    attr_smem = smem;
-  }
+  static PerDevice attr;
+  if (int rc_ = launch_status(ensure_smem_attr(kv_ingest_kernel, smem, attr))) return rc_;
   const long long total = (long long)n_layers * 2 * n_kv_heads * a.n_pages;
   if (total > 0x7fffffffLL) return DS_ERR_INVALID;
   int per_sm = background ? 1 : (200 * 1024) / (smem + 1024);
@@ -188,8 +185,8 @@ int kv_ingest_launch(const ds_kv_cache& src, const ds_kv_cache& dst, const int32
   long long grid = (long long)num_sms() * per_sm;
   if (grid > total) grid = total;
   count_launch();
-  static const bool c0 = prefer_max_smem(kv_ingest_kernel);
-  (void)c0;
+  static PerDevice carve;
+  prefer_max_smem_once(kv_ingest_kernel, carve);
   kv_ingest_kernel<<<(int)grid, 32, smem, stream>>>(a, (int)total, stage_bytes, stages);
   return launch_status();
 }

@@ -67,6 +67,36 @@ inline bool prefer_max_smem(F* kern) {
          cudaSuccess;
 }
 
+// Function attributes are per device: a once-flag per (kernel, device).
+struct PerDevice {
+  int v[64] = {};
+  int& operator()() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0) d = 0;
+    return v[d & 63];
+  }
+};
+// Raise a kernel's dynamic shared-memory limit to `bytes` (and ask for the
+// maximum carveout) on the current device, once per size increase.
+template <typename F>
+inline cudaError_t ensure_smem_attr(F* kern, int bytes, PerDevice& seen) {
+  int& s = seen();
+  if (bytes <= s) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  prefer_max_smem(kern);
+  s = bytes;
+  return cudaSuccess;
+}
+
+template <typename F>
+inline void prefer_max_smem_once(F* kern, PerDevice& seen) {
+  int& s = seen();
+  if (s & 1) return;
+  prefer_max_smem(kern);
+  s |= 1;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while the previous kernel in the stream drains; it must call pdl_wait()
 // before touching anything the predecessor writes or reads.

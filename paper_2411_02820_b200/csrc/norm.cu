@@ -159,8 +159,9 @@ int norm_seed_launch(const void* x, bool x_bf16, const int64_t* gather, int M, i
   if (M <= 0) return DS_OK;
   if (T < 16 || T > 512 || T % 16 || d % T || d / 16 > 1024 || (32 % (T / 16) && (T / 16) % 32)) return DS_ERR_INVALID;
   count_launch();
-  static const bool c0 = prefer_max_smem(norm_seed_kernel<true>) && prefer_max_smem(norm_seed_kernel<false>);
-  (void)c0;
+  static PerDevice carve_t, carve_f;
+  prefer_max_smem_once(norm_seed_kernel<true>, carve_t);
+  prefer_max_smem_once(norm_seed_kernel<false>, carve_f);
   const dim3 block(d / 16);
   if (x_bf16)
     return launch_status(launch_pdl(norm_seed_kernel<true>, dim3(M), block, 0, stream, x, gather, d, T, gain, out,
@@ -173,8 +174,9 @@ int rmsnorm_launch(const void* x, bool x_bf16, const int64_t* gather, int M, int
                    float* copy_f32, bf16* copy_bf16, int copy_rows, cudaStream_t stream) {
   if (M <= 0) return DS_OK;
   count_launch();
-  static const bool c0 = prefer_max_smem(rmsnorm_kernel<true>) && prefer_max_smem(rmsnorm_kernel<false>);
-  (void)c0;
+  static PerDevice carve_t, carve_f;
+  prefer_max_smem_once(rmsnorm_kernel<true>, carve_t);
+  prefer_max_smem_once(rmsnorm_kernel<false>, carve_f);
   if (x_bf16)
     return launch_status(launch_pdl(rmsnorm_kernel<true>, dim3(M), dim3(NORM_THREADS), 0, stream, x, gather, d, gain,
                                     out, copy_f32, copy_bf16, copy_rows));

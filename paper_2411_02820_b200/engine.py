@@ -16,6 +16,7 @@ memory and streams.  There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 from typing import Iterable, Mapping, Sequence
 
@@ -63,6 +64,7 @@ class LayerKV:
 
     k: torch.Tensor
     v: torch.Tensor
+    context: str | None = None  # context_hash digest of the tokens it was prefilled from (store.py:55-63)
 
     def __post_init__(self) -> None:
         if self.k.shape != self.v.shape or self.k.dim() != 4:
@@ -188,7 +190,9 @@ class MixedPrefill:
 # Workspace
 # ---------------------------------------------------------------------------
 
-_WS: dict = {}
+# model -> {(device, stream): workspace}; weak keys, so a dead model's scratch
+# goes with it and a recycled id() can never alias another model's entry
+_WS: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def workspace_bytes(config: ModelConfig, n_tokens: int) -> int:
@@ -198,19 +202,28 @@ def workspace_bytes(config: ModelConfig, n_tokens: int) -> int:
 
 
 def _workspace(model: ModelWeights, n: int, stream=None) -> torch.Tensor:
-    """Scratch for one call, cached per (device, model, stream): calls on the
-    same stream are ordered, so they may share it; calls on different streams
-    (a producer and a consumer prefilling concurrently) get their own.  The
-    pointer stays stable across calls, which CUDA-graph capture relies on."""
+    """Scratch for one eager call, cached per (model, device, stream): calls on
+    the same stream are ordered, so they may share it; calls on different
+    streams (a producer and a consumer prefilling concurrently) get their own.
+    A larger n replaces the entry; the old buffer returns to the caching
+    allocator of the stream it belongs to, so only later work on that same
+    stream can reuse it.  CUDA graphs never use these: a capture gets a private
+    workspace that lives as long as the graph (:class:`CapturedPartialPrefill`)."""
     need = workspace_bytes(model.config, n)
     s = stream if stream is not None else torch.cuda.current_stream(model.device)
-    key = (model.device, id(model), s.cuda_stream)
-    ws = _WS.get(key)
+    per_model = _WS.setdefault(model, {})
+    key = (str(model.device), s.cuda_stream)
+    ws = per_model.get(key)
     if ws is None or ws.numel() < need:
         with torch.cuda.stream(s):  # owned by the stream that uses it (allocator reuse across streams)
             ws = torch.empty(need, dtype=torch.uint8, device=model.device)
-        _WS[key] = ws
+        per_model[key] = ws
     return ws
+
+
+def _context_digest(tokens) -> str:
+    from .store import context_hash  # store imports this module
+    return context_hash(tokens).digest
 
 
 def _normalize_e(sender_e) -> dict:
@@ -227,7 +240,8 @@ def _normalize_e(sender_e) -> dict:
 
 
 def full_prefill(model: ModelWeights, tokens, e_layers: Iterable[int] | None = None, *, out: LayerKV | None = None,
-                 stream=None, copy_stream=None, tokens_dev: torch.Tensor | None = None) -> PrefillResult:
+                 stream=None, copy_stream=None, tokens_dev: torch.Tensor | None = None,
+                 workspace: torch.Tensor | None = None) -> PrefillResult:
     """Producer export: K/V at every layer over all n positions, E over the
     window (n-1 rows) at ``e_layers`` (default: every layer, profiling mode;
     pass the transition layers for the serving-mode filter, store.py:202-203),
@@ -244,22 +258,25 @@ def full_prefill(model: ModelWeights, tokens, e_layers: Iterable[int] | None = N
         e_bufs = [torch.empty(n - 1, cfg.d_model, dtype=torch.float32, device=model.device) for _ in layers]
         logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=model.device)
         tok = torch.empty(1, dtype=torch.int32, device=model.device)
-    ws = _workspace(model, n, s)
+    ws = workspace if workspace is not None else _workspace(model, n, s)
     la = (C.c_int32 * max(1, len(layers)))(*layers)
     ptrs = (C.c_void_p * max(1, len(layers)))(*[b.data_ptr() for b in e_bufs])
     desc = kv.desc()
-    rc = L.lib().ds_full_prefill(C.byref(model.desc()), ids.ctypes.data,
-                                 tokens_dev.data_ptr() if tokens_dev is not None else None, n, C.byref(desc), la,
-                                 len(layers), ptrs, logits.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel(),
-                                 s.cuda_stream, copy_stream.cuda_stream if copy_stream is not None else None)
+    with torch.cuda.device(model.device):  # the library launches on the current device
+        rc = L.lib().ds_full_prefill(C.byref(model.desc()), ids.ctypes.data,
+                                     tokens_dev.data_ptr() if tokens_dev is not None else None, n, C.byref(desc), la,
+                                     len(layers), ptrs, logits.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel(),
+                                     s.cuda_stream, copy_stream.cuda_stream if copy_stream is not None else None)
     L.check(rc)
+    kv.context = _context_digest(ids)
     return PrefillResult(kv=kv, e_caches=tuple(ECache(l, b) for l, b in zip(layers, e_bufs)), logits=logits,
                          token_dev=tok)
 
 
 def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sender_kv: LayerKV | None,
                     sender_e: Mapping[int, ECache] | Iterable[ECache] | None = None, *, out: PagedKV | None = None,
-                    stream=None, copy_stream=None, tokens_dev: torch.Tensor | None = None) -> MixedPrefill:
+                    stream=None, copy_stream=None, tokens_dev: torch.Tensor | None = None,
+                    workspace: torch.Tensor | None = None) -> MixedPrefill:
     """Consumer partial prefill (model.py:660-679): ingest the sender's K/V at
     reused layers, recompute each group over the window from embeddings (a=0)
     or the sender's E at its transition layer, run the anchor position through
@@ -275,7 +292,7 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
         cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
         logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
         tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
-    ws = _workspace(receiver, n, s)
+    ws = workspace if workspace is not None else _workspace(receiver, n, s)
     groups = [x for g in config.groups for x in g]
     ga = (C.c_int32 * max(1, len(groups)))(*groups)
     for l, e in e_map.items():
@@ -286,11 +303,12 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
     skv = sender_kv.desc() if sender_kv is not None else None
     odesc = cache.desc()
     ml, mk = C.c_int32(-1), C.c_int32(0)
-    rc = L.lib().ds_partial_prefill(
-        C.byref(receiver.desc()), ids.ctypes.data, tokens_dev.data_ptr() if tokens_dev is not None else None, n, ga,
-        len(config.groups), C.byref(skv) if skv is not None else None, ea, len(e_list), C.byref(odesc),
-        logits.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream,
-        copy_stream.cuda_stream if copy_stream is not None else None, C.byref(ml), C.byref(mk))
+    with torch.cuda.device(receiver.device):
+        rc = L.lib().ds_partial_prefill(
+            C.byref(receiver.desc()), ids.ctypes.data, tokens_dev.data_ptr() if tokens_dev is not None else None, n,
+            ga, len(config.groups), C.byref(skv) if skv is not None else None, ea, len(e_list), C.byref(odesc),
+            logits.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream,
+            copy_stream.cuda_stream if copy_stream is not None else None, C.byref(ml), C.byref(mk))
     L.check(rc, ml.value, mk.value)
     return MixedPrefill(kv=cache, logits=logits, token_dev=tok)
 
@@ -301,32 +319,61 @@ class CapturedPartialPrefill:
     recompute config, sender export, output cache and prefix length (CUDA graphs
     instead of a tracing compiler).
 
+    The graph reads ONE export: the sender's K/V and E of one context.  Its
+    context is ``context_hash(context)`` when ``context`` (the tokens the export
+    was prefilled from) is given, else the export's own tag (``LayerKV.context``
+    set by :func:`full_prefill`, ``FetchedKV.context`` by the store,
+    ``RemoteKV.context`` by the IPC transport).  :meth:`run` hashes each
+    request's tokens and raises ``CacheMissError`` -- what the reference's
+    ``fetch_context_caches`` raises for a context it does not hold
+    (store.py:351-395) -- when they are not that context, so a request can never
+    be served another context's KV.  A config that reads no export (every layer
+    recomputed from the embeddings) accepts any tokens.
+
     Construction runs the call once eagerly (all validation and cache-miss
     errors surface there, exactly as :func:`partial_prefill` raises them), then
-    captures it.  :meth:`run` validates the request's tokens on the host
-    (check_tokens, model.py:425-437), copies them into a fixed device buffer
-    (asynchronously from pinned memory) and replays the whole two-stream step:
-    one graph launch instead of ~30 kernel launches.  The returned
-    :class:`MixedPrefill` holds the same device tensors on every call (the
-    graph writes into them); copy what must outlive the next request."""
+    captures it into a graph with a PRIVATE workspace that lives as long as this
+    object (eager calls on the same streams can never resize or free it).
+    :meth:`run` validates the tokens on the host (check_tokens,
+    model.py:425-437), copies them into a fixed device buffer (asynchronously
+    from pinned memory) and replays the whole two-stream step: one graph launch
+    instead of ~30 kernel launches.  The returned :class:`MixedPrefill` holds
+    the same device tensors on every call (the graph writes into them); copy
+    what must outlive the next request."""
 
     def __init__(self, receiver: ModelWeights, n_tokens: int, config: RecomputeConfig, sender_kv: LayerKV | None,
                  sender_e: Mapping[int, ECache] | Iterable[ECache] | None = None, *, out: PagedKV | None = None,
-                 stream=None, copy_stream=None):
+                 stream=None, copy_stream=None, context=None):
         cfg = receiver.config
         self.receiver, self.n = receiver, int(n_tokens)
+        reads_export = sender_kv is not None or any(a > 0 for a, _ in config.groups)
+        if context is not None:
+            tag = _context_digest(check_tokens(context, cfg))
+            own = getattr(sender_kv, "context", None)
+            if own is not None and own != tag:
+                raise ValueError("context= does not match the context the sender export was prefilled from")
+        else:
+            tag = getattr(sender_kv, "context", None)
+        if reads_export and tag is None:
+            raise ValueError("the sender export carries no context tag: pass context=<the tokens it was prefilled from>")
+        self.context = tag if reads_export else None
+        reused = config.reused_layers(cfg.n_layers)
+        self._miss = (reused[0], "kv") if reused else (config.transition_layers[0] if config.transition_layers else 0,
+                                                      "e")
         self.stream = stream if stream is not None else torch.cuda.Stream(device=receiver.device)
         self.copy_stream = copy_stream if copy_stream is not None else torch.cuda.Stream(device=receiver.device)
-        self.tokens_dev = torch.zeros(self.n, dtype=torch.int64, device=receiver.device)
+        with torch.cuda.stream(self.stream):
+            self.tokens_dev = torch.zeros(self.n, dtype=torch.int64, device=receiver.device)
+            self.workspace = torch.empty(workspace_bytes(cfg, self.n), dtype=torch.uint8, device=receiver.device)
         probe = np.zeros(self.n, dtype=np.int64)  # valid ids for the host-side checks during capture
         self.out = out if out is not None else PagedKV.allocate(cfg, self.n, receiver.device)
 
         def call():
             return partial_prefill(receiver, probe, config, sender_kv, sender_e, out=self.out, stream=self.stream,
-                                   copy_stream=self.copy_stream, tokens_dev=self.tokens_dev)
+                                   copy_stream=self.copy_stream, tokens_dev=self.tokens_dev, workspace=self.workspace)
 
         with torch.cuda.stream(self.stream):
-            call()  # eager: raises like partial_prefill; allocates the workspace
+            call()  # eager: raises like partial_prefill
         torch.cuda.synchronize(receiver.device)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, stream=self.stream):
@@ -335,11 +382,15 @@ class CapturedPartialPrefill:
     def run(self, tokens) -> MixedPrefill:
         if isinstance(tokens, torch.Tensor):
             src = tokens
-            check_tokens(tokens.numpy(), self.receiver.config)
+            ids = check_tokens(tokens.numpy(), self.receiver.config)
         else:
-            src = torch.from_numpy(check_tokens(tokens, self.receiver.config))
+            ids = check_tokens(tokens, self.receiver.config)
+            src = torch.from_numpy(ids)
         if src.shape[0] != self.n:
             raise ValueError(f"captured for {self.n} tokens, got {src.shape[0]}")
+        if self.context is not None and _context_digest(ids) != self.context:
+            layer, kind = self._miss
+            raise CacheMissError(layer, kind, "request tokens are not the context of the captured export")
         caller = torch.cuda.current_stream(self.receiver.device)
         self.stream.wait_stream(caller)  # the previous request's readers are done with the outputs
         with torch.cuda.stream(self.stream):
@@ -372,10 +423,11 @@ def token_selective_prefill(receiver: ModelWeights, tokens, sender_kv: LayerKV, 
     ws = _workspace(receiver, n, s)
     skv, odesc = sender_kv.desc(), cache.desc()
     ml, nsel = C.c_int32(-1), C.c_int32(0)
-    rc = L.lib().ds_token_selective_prefill(
-        C.byref(receiver.desc()), ids.ctypes.data, tokens_dev.data_ptr() if tokens_dev is not None else None, n,
-        C.byref(skv), float(ratio), C.byref(odesc), logits.data_ptr(), tok.data_ptr(), C.byref(nsel), ws.data_ptr(),
-        ws.numel(), s.cuda_stream, C.byref(ml))
+    with torch.cuda.device(receiver.device):
+        rc = L.lib().ds_token_selective_prefill(
+            C.byref(receiver.desc()), ids.ctypes.data, tokens_dev.data_ptr() if tokens_dev is not None else None, n,
+            C.byref(skv), float(ratio), C.byref(odesc), logits.data_ptr(), tok.data_ptr(), C.byref(nsel),
+            ws.data_ptr(), ws.numel(), s.cuda_stream, C.byref(ml))
     L.check(rc, ml.value, 0)
     res = MixedPrefill(kv=cache, logits=logits, token_dev=tok)
     res.n_selected = int(nsel.value)

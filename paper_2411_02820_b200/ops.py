@@ -35,8 +35,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, mode: int = L.EPI_STORE_BF16, resid: 
     if out is None:
         dt = torch.float32 if mode in (L.EPI_RESID_F32, L.EPI_STORE_F32) else torch.bfloat16
         out = torch.empty(M, N, device=a.device, dtype=dt)
-    rc = L.lib().ds_gemm(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0),
-                         _ptr(resid), resid.stride(0) if resid is not None else 0, M, N, K, mode, _stream(stream))
+    with torch.cuda.device(a.device):
+        rc = L.lib().ds_gemm(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0),
+                             _ptr(resid), resid.stride(0) if resid is not None else 0, M, N, K, mode, _stream(stream))
     L.check(rc)
     return out
 
@@ -46,8 +47,9 @@ def rmsnorm(x: torch.Tensor, gain: torch.Tensor, gather: torch.Tensor | None = N
     d = x.shape[-1]
     M = gather.numel() if gather is not None else x.numel() // d
     out = torch.empty(M, d, device=x.device, dtype=torch.bfloat16)
-    rc = L.lib().ds_rmsnorm(x.data_ptr(), int(x.dtype == torch.bfloat16), _ptr(gather), M, d, gain.data_ptr(),
-                            out.data_ptr(), _ptr(copy_f32), _ptr(copy_bf16), _stream(stream))
+    with torch.cuda.device(x.device):
+        rc = L.lib().ds_rmsnorm(x.data_ptr(), int(x.dtype == torch.bfloat16), _ptr(gather), M, d, gain.data_ptr(),
+                                out.data_ptr(), _ptr(copy_f32), _ptr(copy_bf16), _stream(stream))
     L.check(rc)
     return out
 
@@ -76,8 +78,9 @@ def attention_prefill(q: torch.Tensor, kv: L.KvCache, layer: int, n_heads: int, 
     n_q = q.shape[0]
     if out is None:
         out = torch.empty(n_q, n_heads * head_dim, device=q.device, dtype=torch.bfloat16)
-    rc = L.lib().ds_attention_prefill(q.data_ptr(), q.stride(0), C.byref(kv), layer, n_q, q_pos0, n_heads,
-                                      n_kv_heads, head_dim, out.data_ptr(), out.stride(0), _stream(stream))
+    with torch.cuda.device(q.device):
+        rc = L.lib().ds_attention_prefill(q.data_ptr(), q.stride(0), C.byref(kv), layer, n_q, q_pos0, n_heads,
+                                          n_kv_heads, head_dim, out.data_ptr(), out.stride(0), _stream(stream))
     L.check(rc)
     return out
 
@@ -86,6 +89,8 @@ def kv_ingest(src: L.KvCache, dst: L.KvCache, reused: list[int], window: int, n_
               stream=None) -> None:
     arr = (C.c_int32 * max(1, len(reused)))(*reused)
     miss = C.c_int32(-1)
-    rc = L.lib().ds_kv_ingest(C.byref(src), C.byref(dst), arr, len(reused), window, n_kv_heads, head_dim,
-                              _stream(stream), C.byref(miss))
+    dev = stream.device if stream is not None else torch.cuda.current_device()
+    with torch.cuda.device(dev):
+        rc = L.lib().ds_kv_ingest(C.byref(src), C.byref(dst), arr, len(reused), window, n_kv_heads, head_dim,
+                                  _stream(stream), C.byref(miss))
     L.check(rc, miss.value, 1)

@@ -77,6 +77,11 @@ class ConsumerPipeline:
 
     def run(self, tokens, config: RecomputeConfig, sender_kv, sender_e=None, *, out: PagedKV | None = None,
             tokens_dev: torch.Tensor | None = None, timing: bool = False, arrival_event=None):
+        with torch.cuda.device(self.device):  # the library launches on the current device
+            return self._run(tokens, config, sender_kv, sender_e, out=out, tokens_dev=tokens_dev, timing=timing,
+                             arrival_event=arrival_event)
+
+    def _run(self, tokens, config, sender_kv, sender_e, *, out, tokens_dev, timing, arrival_event):
         cfg = self.receiver.config
         ids = check_tokens(tokens, cfg)
         config.validate_for(cfg.n_layers)
@@ -94,19 +99,25 @@ class ConsumerPipeline:
                     e = e_map.get(a)
                     if e is None or e.positions < P or e.hidden.shape[1] != cfg.d_model:
                         raise CacheMissError(a, "e")
-        cache = out if out is not None else PagedKV.allocate(cfg, n, self.device)
+        with torch.cuda.stream(self.compute):  # outputs belong to the stream that writes them
+            cache = out if out is not None else PagedKV.allocate(cfg, n, self.device)
+            logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=self.device)
+            tok = torch.empty(1, dtype=torch.int32, device=self.device)
         dst = cache.desc()
-        logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=self.device)
-        tok = torch.empty(1, dtype=torch.int32, device=self.device)
         ws = _workspace(self.receiver, n, self.compute)
-        if tokens_dev is None:
-            tokens_dev = torch.from_numpy(ids).to(self.device, non_blocking=True)
         cur = torch.cuda.current_stream(self.device)
         start = arrival_event or self._event(timing)
         if arrival_event is None:
             start.record(cur)
         self.link.wait_event(start)
         self.compute.wait_event(start)
+        if out is not None:
+            self.compute.wait_stream(cur)  # the caller's pending work on its cache
+        if tokens_dev is None:
+            # on the compute stream, which every reader of the ids (the group seed,
+            # the anchor) runs on: ordered before them whatever event gates the start
+            with torch.cuda.stream(self.compute):
+                tokens_dev = torch.from_numpy(ids).to(self.device, non_blocking=True)
         times = StageTimes()
         req = ScheduledRequest("r", 0.0, self.receiver.ident, config, cfg.n_layers)
 

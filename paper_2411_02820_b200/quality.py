@@ -64,9 +64,10 @@ def decode_greedy(model, cache, last, steps: int, positions: int | None = None) 
     out = torch.empty(steps, dtype=torch.int32, device=model.device)
     ws = _workspace(model, positions + steps)
     desc = cache.desc()
-    rc = L.lib().ds_decode_greedy(C.byref(model.desc()), C.byref(desc), positions, first.data_ptr(), steps,
-                                  out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                  torch.cuda.current_stream(model.device).cuda_stream)
+    with torch.cuda.device(model.device):
+        rc = L.lib().ds_decode_greedy(C.byref(model.desc()), C.byref(desc), positions, first.data_ptr(), steps,
+                                      out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      torch.cuda.current_stream(model.device).cuda_stream)
     L.check(rc)
     return out.cpu().numpy().astype(np.int64)
 

@@ -102,11 +102,28 @@ class PeerBuffer:
         return self.shape[0] * self.shape[1] * 4
 
 
+class _DeviceArray:
+    """__cuda_array_interface__ over a raw device pointer (a mapped peer buffer)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def peer_view(ptr: int, shape: tuple, dtype: torch.dtype) -> torch.Tensor:
+    """A torch view (no copy) of a mapped peer buffer; bf16 travels as f16 bits."""
+    typestr = {torch.float32: "<f4", torch.bfloat16: "<f2"}[dtype]
+    t = torch.as_tensor(_DeviceArray(ptr, shape, typestr), device=torch.device("cuda", torch.cuda.current_device()))
+    return t.view(dtype) if dtype == torch.bfloat16 else t
+
+
 class RemoteKV:
     """The producer's dense [L, KVH, n, D] export, mapped; ``desc()`` for the ingest."""
 
-    def __init__(self, k_ptr: int, v_ptr: int, n_layers: int, n_kv_heads: int, positions: int, head_dim: int):
+    def __init__(self, k_ptr: int, v_ptr: int, n_layers: int, n_kv_heads: int, positions: int, head_dim: int,
+                 context: str | None = None):
         self.k_ptr, self.v_ptr = k_ptr, v_ptr
+        self.context = context
         self.n_layers, self.n_kv_heads, self.positions, self.head_dim = n_layers, n_kv_heads, positions, head_dim
 
     def desc(self) -> L.KvCache:
@@ -122,7 +139,8 @@ class RemoteExport:
         self._bases = []
         k = self._open(*handles.k)
         v = self._open(*handles.v)
-        self.kv = RemoteKV(k, v, handles.n_layers, handles.n_kv_heads, handles.positions, handles.head_dim)
+        self.kv = RemoteKV(k, v, handles.n_layers, handles.n_kv_heads, handles.positions, handles.head_dim,
+                           handles.context)
         self.e_map = {l: ECache(l, PeerBuffer(self._open(h, off), rows, handles.d_model))
                       for l, (h, off, rows) in handles.e.items()}
 
@@ -132,6 +150,22 @@ class RemoteExport:
         L.check(L.lib().ds_ipc_open(buf, offset, C.byref(base), C.byref(ptr)))
         self._bases.append(base.value)
         return ptr.value
+
+    def local_copy(self, stream=None):
+        """Pull the whole export over the link into this GPU's HBM (one copy per
+        tensor): ``(LayerKV, {layer: ECache})`` with the export's context tag.
+        The fan-out bench times the consumer step on it (local data) beside the
+        step on the mapped export (NVLink) -- the §8d hidden fraction."""
+        from .engine import LayerKV
+        h = self.handles
+        shape = (h.n_layers, h.n_kv_heads, h.positions, h.head_dim)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            k = peer_view(self.kv.k_ptr, shape, torch.bfloat16).clone()
+            v = peer_view(self.kv.v_ptr, shape, torch.bfloat16).clone()
+            e = {l: ECache(l, peer_view(ec.hidden.data_ptr(), ec.hidden.shape, torch.float32).clone())
+                 for l, ec in self.e_map.items()}
+        return LayerKV(k, v, context=h.context), e
 
     def close(self) -> None:
         for b in self._bases:

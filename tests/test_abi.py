@@ -45,7 +45,16 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_host_only_entry_points(lib):
     L = lib.lib()
-    assert L.ds_abi_version() == 1
+    assert L.ds_abi_version() == lib.ABI_VERSION == 2
+    # anchor-shape override: returns the previous value, rejects unknown shapes
+    prev = L.ds_set_anchor_shape(2)
+    assert prev in (0, 1, 2)
+    assert L.ds_set_anchor_shape(prev) == 2
+    assert L.ds_set_anchor_shape(7) == -1
+    with lib.anchor_shape("persistent"):
+        assert L.ds_set_anchor_shape(1) == 1
+    assert L.ds_set_anchor_shape(prev) == prev
+    assert L.ds_fused_fallbacks() == 0
     dims = lib.Dims(32, 4096, 32, 8, 128, 14336, 128256, 8192)
     assert L.ds_workspace_size(ctypes.byref(dims), 8192) > 8192 * 4096 * 4
     assert L.ds_workspace_size(None, 8) == 0

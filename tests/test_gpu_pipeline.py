@@ -120,7 +120,8 @@ def test_recompute_group_and_anchor_entry_points(pair):
 
 def test_captured_partial_prefill_matches_eager():
     """CapturedPartialPrefill (one CUDA-graph replay per request) gives the eager
-    call's logits bit for bit, request after request, and re-validates tokens."""
+    call's logits bit for bit, request after request; a graph per exported
+    context serves that context's requests, and tokens are re-validated."""
     import numpy as np
     import paper_2411_02820_b200 as P
     from oracle import crosskv_oracle as O
@@ -129,13 +130,14 @@ def test_captured_partial_prefill_matches_eager():
     B = P.build_model(cfg, P.PerturbationSpec.block(4, [2], 0.5, 1000), device="cuda")
     rc = P.RecomputeConfig([(2, 3)])
     toks = [O.synthetic_tokens(300 + i, 1, 200, cfg.vocab_size)[0] for i in range(2)]
-    prod = P.full_prefill(A, toks[0], e_layers=rc.transition_layers)
-    cap = P.CapturedPartialPrefill(B, 200, rc, prod.kv, prod.e_map())
-    for t in toks:  # the sender export is fixed; the request tokens change
-        got = cap.run(t).logits.clone()
-        ref = P.partial_prefill(B, t, rc, prod.kv, prod.e_map(), copy_stream=torch.cuda.Stream()).logits
-        torch.cuda.synchronize()
-        assert torch.equal(got, ref)
+    for t in toks:  # one export (and one captured graph) per shared context
+        prod = P.full_prefill(A, t, e_layers=rc.transition_layers)
+        cap = P.CapturedPartialPrefill(B, 200, rc, prod.kv, prod.e_map())
+        for _ in range(2):
+            got = cap.run(t).logits.clone()
+            ref = P.partial_prefill(B, t, rc, prod.kv, prod.e_map(), copy_stream=torch.cuda.Stream()).logits
+            torch.cuda.synchronize()
+            assert torch.equal(got, ref)
     with pytest.raises(ValueError):
         cap.run(np.full(200, cfg.vocab_size, dtype=np.int64))
     with pytest.raises(ValueError):

@@ -203,3 +203,42 @@ def test_token_selective_selection_ties_and_misses(toy_base):
     assert e.value.layer == 0
     with pytest.raises(ValueError):
         O.token_selective_prefill(toy_base, toks, k, v, 0.0)
+
+
+def test_make_variant_equals_make_weights():
+    """make_variant (shared base tensors) draws the same noise streams as
+    make_weights with eps (model.py:315-320): bit-identical weights."""
+    dims = O.Dims(4, 256, 4, 1, 64, 1024, 4096, 1024, 7)
+    base = O.make_weights(dims)
+    eps = O.block_eps(4, [1, 3], 0.25)
+    want = O.make_weights(dims, eps, noise_seed=55)
+    got = O.make_variant(base, eps, 55)
+    assert np.array_equal(got["embed"], want["embed"]) and np.array_equal(got["unembed"], want["unembed"])
+    for lw_w, lw_g in zip(want["layers"], got["layers"]):
+        for name in O.LAYER_SLOTS:
+            assert np.array_equal(lw_w[name], lw_g[name]), name
+
+
+def test_einsum_attention_matches_blocked():
+    """attend_einsum (the reference's einsum restatement, timed by bench.py)
+    equals the blocked-BLAS attend to float32 rounding."""
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((70, 8, 64), dtype=np.float32)
+    k = rng.standard_normal((2, 70, 64), dtype=np.float32)
+    v = rng.standard_normal((2, 70, 64), dtype=np.float32)
+    pos = np.arange(70)
+    a = O.attend(q, k, v, pos)
+    b = O.attend_einsum(q, k, v, pos[None, :] <= pos[:, None])
+    assert np.abs(a - b).max() < 1e-5
+
+
+@pytest.mark.reference
+def test_einsum_attention_matches_reference(crosskv_ref):
+    m = crosskv_ref
+    cfg = m.ModelConfig(1, 512, 8, 2, 64, 1024, 4096, 128, 0)
+    rng = np.random.default_rng(1)
+    q = rng.standard_normal((60, 8, 64), dtype=np.float32)
+    k = rng.standard_normal((2, 60, 64), dtype=np.float32)
+    v = rng.standard_normal((2, 60, 64), dtype=np.float32)
+    allowed = np.tril(np.ones((60, 60), dtype=bool))
+    assert np.array_equal(m._masked_attention(q, k, v, allowed, cfg), O.attend_einsum(q, k, v, allowed))
