@@ -7,11 +7,13 @@ entry point raises — there is no CPU or eager-PyTorch fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import CacheMissError, DegenerateInputError
 
-LIB_PATH = Path(__file__).resolve().parent / "libdroidspeak.so"
+# DS_LIB: another build of the same library (same-box A/B measurements of kernel variants)
+LIB_PATH = Path(os.environ.get("DS_LIB") or Path(__file__).resolve().parent / "libdroidspeak.so")
 
 DS_OK, DS_ERR_INVALID, DS_ERR_CACHE_MISS, DS_ERR_DEGENERATE, DS_ERR_CUDA = range(5)
 MISS_KIND = {1: "kv", 2: "e"}

@@ -425,6 +425,25 @@ DS_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+// Same with an L2 cache policy (createpolicy) on the loaded lines.
+DS_DEV void tma_load_2d_pair_hint(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1,
+                                  uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+DS_DEV uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+DS_DEV uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 DS_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -498,6 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t leader_full0 = map_to_rank(&full[0], 0);
+      const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < num_tiles; t += n_pairs) {
@@ -509,8 +529,13 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], 2 * L::STAGE_BYTES);
           const uint32_t fb = leader_full0 + stage * 8;
-          tma_load_2d_pair(sA + stage * L::A_BYTES, &tmA, fb, kb * GEMM_BK, arow);
-          tma_load_2d_pair(sB + stage * L::B_BYTES, &tmB, fb, kb * GEMM_BK, brow);
+          if (epi.l2_hint) {
+            tma_load_2d_pair_hint(sA + stage * L::A_BYTES, &tmA, fb, kb * GEMM_BK, arow, pol_a);
+            tma_load_2d_pair_hint(sB + stage * L::B_BYTES, &tmB, fb, kb * GEMM_BK, brow, pol_b);
+          } else {
+            tma_load_2d_pair(sA + stage * L::A_BYTES, &tmA, fb, kb * GEMM_BK, arow);
+            tma_load_2d_pair(sB + stage * L::B_BYTES, &tmB, fb, kb * GEMM_BK, brow);
+          }
           if (++stage == PAIR_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -650,6 +675,12 @@ static cudaError_t launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, i
 
 int gemm_bn(int N) { return N >= 1024 ? 256 : 128; }
 
+static int env_or(const char* name, int dflt) {
+  const char* v = getenv(name);
+  const int x = v ? atoi(v) : dflt;
+  return x >= 0 ? x : dflt;
+}
+
 // The CTA-pair kernel serves the large recompute shapes (DS_GEMM_PAIR=0 turns it off).
 static bool use_pair(int M, int N) {
   static int env = -1;
@@ -699,13 +730,18 @@ int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int 
   GemmEpi e2 = epi;
   CUtensorMap ta, tb;
   if (!force_bn && use_pair(epi.M, epi.N)) {
-    static int group = -1;
-    if (group < 0) {
-      const char* v = getenv("DS_GEMM_GROUP");  // raster experiments
-      group = v ? atoi(v) : 8;
-      if (group < 1) group = 8;
-    }
-    e2.group = group;  // 8 pair m-blocks = the 16 128-row m-blocks of the single-CTA raster
+    // Raster group (pair m-blocks sweeping all n-blocks), per shape from the ncu
+    // DRAM sweep (tools/raster_sweep.sh, profiles/r02_raster_sweep.txt): 16 for
+    // K <= 4096 (W1 reads 369 vs 557 MB at 8, QKV 197 vs 265 MB), 8 for the
+    // long-K W2.  DS_GEMM_GROUP / DS_GEMM_GROUP_LONGK override (experiments).
+    // Long K (W2, K = d_ff): DS_GEMM_L2HINT=1 loads the weights evict_last and
+    // the activations evict_first (experiment).
+    static const int group_short = env_or("DS_GEMM_GROUP", 16);
+    static const int group_long = env_or("DS_GEMM_GROUP_LONGK", 8);
+    static const int l2hint = env_or("DS_GEMM_L2HINT", 0);
+    const bool long_k = K > 8192;
+    e2.group = max(1, long_k ? group_long : group_short);
+    e2.l2_hint = long_k ? l2hint : 0;
     if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK) ||
         make_tmap_bf16(&tb, B, epi.N, K, ldb, PAIR_HALF, GEMM_BK))
       return launch_status(cudaErrorInvalidValue);

@@ -30,6 +30,7 @@ struct GemmEpi {
   int pos0;             // absolute position of row 0
   const int32_t* pos_rows;  // or, if set, the absolute position of each row (token-selective recompute)
   int group;            // raster: m-blocks per group (set by gemm_launch)
+  int l2_hint;          // pair GEMM: 1 = B (weights) loaded L2 evict_last, A evict_first (long-K shapes)
   const float* rope_cos;  // [max_seq][head_dim/2]
   const float* rope_sin;
   unsigned int* done;   // optional: +1 per (tile, epilogue warp) once its stores are visible
