@@ -5,6 +5,8 @@
 // query at absolute position p sees keys 0..p; max-subtracted softmax; output
 // head-major [rows][H*D].  Online softmax in fp32 (exp2 with the scale folded
 // in), P rounded to bf16 for the P.V product, output rounded to bf16.
+#include <cstdio>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -54,6 +56,28 @@ DS_DEV float2 exp2_fma2(float2 x) {
 #define DS_FA_EMU_MOD 4  // one pair in DS_FA_EMU_MOD on the FMA pipe (0: all on MUFU)
 #endif
 
+#ifndef DS_FA_STAMPS
+#define DS_FA_STAMPS 0
+#endif
+#if DS_FA_STAMPS
+// Debug timeline (DS_NVCC_EXTRA=-DDS_FA_STAMPS=1): CTA (0,0) records clock64
+// at the pipeline hand-offs and prints them.
+__device__ long long fa_stamps[2][64][8];
+#define FA_STAMP(i, j, k) \
+  if (DS_FA_STAMPS && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) fa_stamps[i][j][k] = clock64()
+#else
+#define FA_STAMP(i, j, k)
+#endif
+
+#ifdef DS_FA_DIVERGENT_ISSUE
+#define FA_ISSUER (lane == 0)
+#else
+#define FA_ISSUER elect_one()
+#endif
+#ifndef DS_FA_ABLATE
+#define DS_FA_ABLATE 0
+#endif
+
 constexpr int FA_BM = 128;
 constexpr int FA_BN = 128;
 constexpr int FA_THREADS = 320;
@@ -81,7 +105,7 @@ struct FaTcArgs {
 
 // At most 136 registers per thread: 3 FA warps of an SM sub-partition then
 // leave room for one 88-register warp of the persistent anchor (anchor.cu).
-template <int D>
+template <int D, bool CHUNK>
 __global__ void __maxnreg__(136)
     fa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
@@ -161,6 +185,12 @@ __global__ void __maxnreg__(136)
           rows[p] = (int)(g * a.k_head_rows + (long long)tp * a.k_page_rows);
         }
         mbar_wait(&k_empty[st], ph ^ 1);
+        if (DS_FA_ABLATE >= 2 && j >= 2) {  // timing only: stale K/V tiles, no loads
+          mbar_expect_tx(&k_full[st], 0);
+          mbar_wait(&v_empty[st], ph ^ 1);
+          mbar_expect_tx(&v_full[st], 0);
+          continue;
+        }
         mbar_expect_tx(&k_full[st], CH * L::CHUNK);
         for (int p = 0; p < 2; ++p)
           for (int c = 0; c < CH; ++c) tma_load_2d(sK(st, c) + p * 64 * 128, &tmK, &k_full[st], c * 64, rows[p]);
@@ -173,29 +203,31 @@ __global__ void __maxnreg__(136)
   } else if (warp == 1) {
     constexpr uint32_t IDESC_QK = umma_idesc_bf16(FA_BM, FA_BN);
     constexpr uint32_t IDESC_PV = umma_idesc_bf16_bmn(FA_BM, D);
+    // The whole warp runs the issue code (warp-uniform descriptors stay in
+    // uniform registers) and one elected lane issues each MMA: issuing from a
+    // divergent `lane == 0` branch costs ~180 cycles per tcgen05.mma (R2UR
+    // moves + a waterfall loop per instruction) against 64 cycles of tensor
+    // work for a 128x128x16 MMA (tools/mma_probe.cu).
     auto qk = [&](int i, int st) {
-      if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < CH; ++c)
+      for (int c = 0; c < CH; ++c)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = sdesc_sw128(smem_u32(sQ(i, c)) + k * 32, 16, 1024);
-            const uint64_t bd = sdesc_sw128(smem_u32(sK(st, c)) + k * 32, 16, 1024);
-            umma_bf16(tmem + i * 128, ad, bd, IDESC_QK, (c | k) != 0 ? 1u : 0u);
-          }
-        umma_commit(&s_full[i]);
-      }
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ad = sdesc_sw128(smem_u32(sQ(i, c)) + k * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(smem_u32(sK(st, c)) + k * 32, 16, 1024);
+          if (FA_ISSUER) umma_bf16(tmem + i * 128, ad, bd, IDESC_QK, (c | k) != 0 ? 1u : 0u);
+        }
+      if (FA_ISSUER) umma_commit(&s_full[i]);
       __syncwarp();
     };
     auto pv = [&](int i, int st, int j) {
-      if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < FA_BN / 16; ++s) {
-          const uint64_t bd = sdesc_sw128(smem_u32(sV(st, 0)) + s * 2048, L::CHUNK, 1024);
+      for (int s = 0; s < FA_BN / 16; ++s) {
+        const uint64_t bd = sdesc_sw128(smem_u32(sV(st, 0)) + s * 2048, L::CHUNK, 1024);
+        if (FA_ISSUER)
           umma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + s * 8, bd, IDESC_PV, (j | s) != 0 ? 1u : 0u);
-        }
-        umma_commit(&o_done[i]);
       }
+      if (FA_ISSUER) umma_commit(&o_done[i]);
       __syncwarp();
     };
     mbar_wait(q_full, 0);
@@ -203,7 +235,7 @@ __global__ void __maxnreg__(136)
     tc_fence_after();
     if (n_kv[0] > 0) qk(0, 0);
     if (n_kv[1] > 0) qk(1, 0);
-    if (lane == 0) umma_commit(&k_empty[0]);
+    if (FA_ISSUER) umma_commit(&k_empty[0]);
     __syncwarp();
     for (int j = 0; j < J; ++j) {
       const int st = j & 1, st1 = (j + 1) & 1;
@@ -224,24 +256,27 @@ __global__ void __maxnreg__(136)
       }
       if (j < n_kv[0]) {
         mbar_wait(&p_full[0], j & 1);
+        if (lane == 0) FA_STAMP(0, j, 2);
         tc_fence_after();
         pv(0, st, j);
       }
       if (more) {
         mbar_wait(&k_full[st1], ((j + 1) >> 1) & 1);
+        if (lane == 0) FA_STAMP(0, j, 3);
         tc_fence_after();
         if (j + 1 < n_kv[0]) qk(0, st1);
       }
       if (j < n_kv[1]) {
         mbar_wait(&p_full[1], j & 1);
+        if (lane == 0) FA_STAMP(1, j, 2);
         tc_fence_after();
         pv(1, st, j);
       }
-      if (lane == 0) umma_commit(&v_empty[st]);
+      if (FA_ISSUER) umma_commit(&v_empty[st]);
       __syncwarp();
       if (more) {
         if (j + 1 < n_kv[1]) qk(1, st1);
-        if (lane == 0) umma_commit(&k_empty[st1]);
+        if (FA_ISSUER) umma_commit(&k_empty[st1]);
         __syncwarp();
       }
     }
@@ -258,106 +293,226 @@ __global__ void __maxnreg__(136)
     const float sc = a.scale_log2;
     const float thr = 8.0f / sc;
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kv[i]; ++j) {
-      mbar_wait(&s_full[i], j & 1);
-      tc_fence_after();
-      // The row in two 64-column halves (at most 136 registers per thread, so
-      // an anchor warp of the other stream fits beside the 3 FA warps of an SM
-      // sub-partition): pass 1 takes the masked row max, upper half first so
-      // the lower half stays in registers for pass 2.
-      const int kbase = j * FA_BN;
-      const bool maskit = kbase + FA_BN - 1 > tile_pos0;
-      uint32_t sr[FA_BN / 2];
-      tmem_ld32_nowait(tS + 64, sr);
-      tmem_ld32_nowait(tS + 96, sr + 32);
-      tmem_wait_ld();
-      if (maskit) {
-#pragma unroll
-        for (int c = 0; c < FA_BN / 2; ++c)
-          if (kbase + FA_BN / 2 + c > qpos) sr[c] = __float_as_uint(-INFINITY);
-      }
-      // row max as 8 independent chains (a single 128-long fmax chain is
-      // ~4 cycles per link on the softmax critical path)
-      float mx8[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(sr[q]);
-#pragma unroll
-      for (int c = 8; c < FA_BN / 2; c += 2)
-        mx8[(c >> 1) & 7] = fmax3(mx8[(c >> 1) & 7], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-      tmem_ld32_nowait(tS, sr);
-      tmem_ld32_nowait(tS + 32, sr + 32);
-      tmem_wait_ld();
-      if (maskit) {
-#pragma unroll
-        for (int c = 0; c < FA_BN / 2; ++c)
-          if (kbase + c > qpos) sr[c] = __float_as_uint(-INFINITY);
-      }
-#pragma unroll
-      for (int c = 0; c < FA_BN / 2; c += 2)
-        mx8[(c >> 1) & 7] = fmax3(mx8[(c >> 1) & 7], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
-      const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const bool need = mt > m_used + thr;
-      float corr = 1.f;
-      if (need) {
-        corr = fast_exp2((m_used - mt) * sc);
-        m_used = mt;
-      }
-      l *= corr;
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        mbar_wait(&o_done[i], (j - 1) & 1);
+    if constexpr (CHUNK) {
+      // Softmax in four 32-column chunks against a running max: chunk c+1's
+      // TMEM load is in flight while chunk c is exponentiated, and P chunk c
+      // (16 packed columns) goes over S columns already consumed.  The max
+      // used for the exponentials only moves when a chunk's max exceeds it by
+      // more than 2^8 (p <= 256 always); then the P chunks already written
+      // are rescaled in TMEM (rare: in practice only the first chunk of the
+      // first key block) and O once per key block, as in the lazy rescale.
+      for (int j = 0; j < n_kv[i]; ++j) {
+        mbar_wait(&s_full[i], j & 1);
+        if (lane == 0 && quarter == 0) FA_STAMP(i, j, 0);
         tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t orow[32];
-          tmem_ld32_nowait(tO + c * 32, orow);
-          tmem_wait_ld();
+#if DS_FA_ABLATE
+        // timing only: the MMA pipeline without the softmax (wrong results)
+        if (lane == 0) mbar_arrive(&p_full[i]);
+        l = 1.f;
+        continue;
+#endif
+        const int kbase = j * FA_BN;
+        const bool maskit = kbase + FA_BN - 1 > tile_pos0;
+        uint32_t sa[32], sb[32];
+        tmem_ld32_nowait(tS, sa);
+        tmem_wait_ld();
+        float ocorr = 1.f;
+        float2 sum4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+        const float2 sc2 = make_float2(sc, sc);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * corr);
-          tmem_st32_nowait(tO + c * 32, orow);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t* cur = (c & 1) ? sb : sa;
+          uint32_t* nxt = (c & 1) ? sa : sb;
+          if (c < 3) tmem_ld32_nowait(tS + 32 * (c + 1), nxt);
+          if (maskit) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (kbase + 32 * c + e > qpos) cur[e] = __float_as_uint(-INFINITY);
+          }
+          float mx4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) mx4[q] = fmax3(__uint_as_float(cur[q]), __uint_as_float(cur[q + 4]),
+                                                     __uint_as_float(cur[q + 8]));
+#pragma unroll
+          for (int e = 12; e < 32; e += 8)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              mx4[q] = fmax3(mx4[q], __uint_as_float(cur[e + q]), __uint_as_float(cur[e + 4 + q]));
+          const float cm = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+          const bool need = cm > m_used + thr;
+          if (__any_sync(0xffffffffu, need)) {
+            float f = 1.f;
+            if (need) {
+              f = fast_exp2((m_used - cm) * sc);  // 0 while m_used is -inf
+              m_used = cm;
+            }
+            l *= f;
+            ocorr *= f;
+            if (c > 0) {
+              // rescale the P chunks already in TMEM (bf16 pairs) by f
+              tmem_wait_st();
+#pragma unroll 1
+              for (int cc = 0; cc < c; ++cc) {
+                uint32_t pr[16];
+                tmem_ld16_nowait(tS + 16 * cc, pr);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const float2 v = unpack_bf16x2(pr[e]);
+                  pr[e] = pack_bf16x2(v.x * f, v.y * f);
+                }
+                tmem_st16_nowait(tS + 16 * cc, pr);
+              }
+              const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+              l += (s2.x + s2.y) * f;  // the chunks summed so far, rescaled
+              sum4[0] = sum4[1] = sum4[2] = sum4[3] = make_float2(0.f, 0.f);
+            }
+          }
+          const float msc = m_used * sc;
+          const float2 nmsc2 = make_float2(-msc, -msc);
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 x = ffma2(make_float2(__uint_as_float(cur[2 * e]), __uint_as_float(cur[2 * e + 1])), sc2,
+                                   nmsc2);
+            float2 p;
+            if (DS_FA_EMU_MOD && (e % (DS_FA_EMU_MOD > 0 ? DS_FA_EMU_MOD : 1)) == DS_FA_EMU_MOD - 1)
+              p = exp2_fma2(x);
+            else
+              p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+            sum4[e & 3] = fadd2(sum4[e & 3], p);
+            pk[e] = pack_bf16x2(p.x, p.y);
+          }
+          tmem_st16_nowait(tS + 16 * c, pk);
+          if (c < 3) {
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) asm volatile("" : "+r"(nxt[e]));  // values valid only after the wait
+          }
+        }
+        const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+        l += s2.x + s2.y;
+        if (j > 0 && __any_sync(0xffffffffu, ocorr != 1.f)) {
+          mbar_wait(&o_done[i], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t orow[32];
+            tmem_ld32_nowait(tO + c * 32, orow);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * ocorr);
+            tmem_st32_nowait(tO + c * 32, orow);
+          }
         }
         tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0 && quarter == 0) FA_STAMP(i, j, 1);
+        if (lane == 0) mbar_arrive(&p_full[i]);
       }
-      const float msc = m_used * sc;
-      float2 sum4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};  // independent partial sums
-      uint32_t pk[FA_BN / 8];
-      const float2 sc2 = make_float2(sc, sc), nmsc2 = make_float2(-msc, -msc);
-      auto expo = [&](int c, uint32_t s0, uint32_t s1) {
-        const float2 x = ffma2(make_float2(__uint_as_float(s0), __uint_as_float(s1)), sc2, nmsc2);
-        float2 p;
-        if (DS_FA_EMU_MOD && (c % (DS_FA_EMU_MOD > 0 ? DS_FA_EMU_MOD : 1)) == DS_FA_EMU_MOD - 1)
-          p = exp2_fma2(x);
-        else
-          p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-        sum4[c & 3] = fadd2(sum4[c & 3], p);
-        pk[c & 15] = pack_bf16x2(p.x, p.y);
-      };
-      // pass 2: lower half from registers -> P columns [0, 32) (over consumed S)
-#pragma unroll
-      for (int c = 0; c < FA_BN / 4; ++c) {
-        expo(c, sr[2 * c], sr[2 * c + 1]);
-        if ((c & 15) == 15) tmem_st16_nowait(tS + (c & ~15), pk);  // P columns as they complete
+    } else {
+      for (int j = 0; j < n_kv[i]; ++j) {
+        mbar_wait(&s_full[i], j & 1);
+        tc_fence_after();
+        // The row in two 64-column halves (at most 136 registers per thread, so
+        // an anchor warp of the other stream fits beside the 3 FA warps of an SM
+        // sub-partition): pass 1 takes the masked row max, upper half first so
+        // the lower half stays in registers for pass 2.
+        const int kbase = j * FA_BN;
+        const bool maskit = kbase + FA_BN - 1 > tile_pos0;
+        uint32_t sr[FA_BN / 2];
+        tmem_ld32_nowait(tS + 64, sr);
+        tmem_ld32_nowait(tS + 96, sr + 32);
+        tmem_wait_ld();
+        if (maskit) {
+  #pragma unroll
+          for (int c = 0; c < FA_BN / 2; ++c)
+            if (kbase + FA_BN / 2 + c > qpos) sr[c] = __float_as_uint(-INFINITY);
+        }
+        // row max as 8 independent chains (a single 128-long fmax chain is
+        // ~4 cycles per link on the softmax critical path)
+        float mx8[8];
+  #pragma unroll
+        for (int q = 0; q < 8; ++q) mx8[q] = __uint_as_float(sr[q]);
+  #pragma unroll
+        for (int c = 8; c < FA_BN / 2; c += 2)
+          mx8[(c >> 1) & 7] = fmax3(mx8[(c >> 1) & 7], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        tmem_ld32_nowait(tS, sr);
+        tmem_ld32_nowait(tS + 32, sr + 32);
+        tmem_wait_ld();
+        if (maskit) {
+  #pragma unroll
+          for (int c = 0; c < FA_BN / 2; ++c)
+            if (kbase + c > qpos) sr[c] = __float_as_uint(-INFINITY);
+        }
+  #pragma unroll
+        for (int c = 0; c < FA_BN / 2; c += 2)
+          mx8[(c >> 1) & 7] = fmax3(mx8[(c >> 1) & 7], __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const bool need = mt > m_used + thr;
+        float corr = 1.f;
+        if (need) {
+          corr = fast_exp2((m_used - mt) * sc);
+          m_used = mt;
+        }
+        l *= corr;
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+          mbar_wait(&o_done[i], (j - 1) & 1);
+          tc_fence_after();
+  #pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t orow[32];
+            tmem_ld32_nowait(tO + c * 32, orow);
+            tmem_wait_ld();
+  #pragma unroll
+            for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * corr);
+            tmem_st32_nowait(tO + c * 32, orow);
+          }
+          tmem_wait_st();
+        }
+        const float msc = m_used * sc;
+        float2 sum4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};  // independent partial sums
+        uint32_t pk[FA_BN / 8];
+        const float2 sc2 = make_float2(sc, sc), nmsc2 = make_float2(-msc, -msc);
+        auto expo = [&](int c, uint32_t s0, uint32_t s1) {
+          const float2 x = ffma2(make_float2(__uint_as_float(s0), __uint_as_float(s1)), sc2, nmsc2);
+          float2 p;
+          if (DS_FA_EMU_MOD && (c % (DS_FA_EMU_MOD > 0 ? DS_FA_EMU_MOD : 1)) == DS_FA_EMU_MOD - 1)
+            p = exp2_fma2(x);
+          else
+            p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+          sum4[c & 3] = fadd2(sum4[c & 3], p);
+          pk[c & 15] = pack_bf16x2(p.x, p.y);
+        };
+        // pass 2: lower half from registers -> P columns [0, 32) (over consumed S)
+  #pragma unroll
+        for (int c = 0; c < FA_BN / 4; ++c) {
+          expo(c, sr[2 * c], sr[2 * c + 1]);
+          if ((c & 15) == 15) tmem_st16_nowait(tS + (c & ~15), pk);  // P columns as they complete
+        }
+        // upper half re-read -> P columns [32, 64) (S columns 32..63 are consumed)
+        tmem_ld32_nowait(tS + 64, sr);
+        tmem_ld32_nowait(tS + 96, sr + 32);
+        tmem_wait_ld();
+        if (maskit) {
+  #pragma unroll
+          for (int c = 0; c < FA_BN / 2; ++c)
+            if (kbase + FA_BN / 2 + c > qpos) sr[c] = __float_as_uint(-INFINITY);
+        }
+  #pragma unroll
+        for (int c = 0; c < FA_BN / 4; ++c) {
+          expo(c, sr[2 * c], sr[2 * c + 1]);
+          if ((c & 15) == 15) tmem_st16_nowait(tS + 32 + (c & ~15), pk);
+        }
+        const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+        l += s2.x + s2.y;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
       }
-      // upper half re-read -> P columns [32, 64) (S columns 32..63 are consumed)
-      tmem_ld32_nowait(tS + 64, sr);
-      tmem_ld32_nowait(tS + 96, sr + 32);
-      tmem_wait_ld();
-      if (maskit) {
-#pragma unroll
-        for (int c = 0; c < FA_BN / 2; ++c)
-          if (kbase + FA_BN / 2 + c > qpos) sr[c] = __float_as_uint(-INFINITY);
-      }
-#pragma unroll
-      for (int c = 0; c < FA_BN / 4; ++c) {
-        expo(c, sr[2 * c], sr[2 * c + 1]);
-        if ((c & 15) == 15) tmem_st16_nowait(tS + 32 + (c & ~15), pk);
-      }
-      const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
-      l += s2.x + s2.y;
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[i]);
     }
     if (n_kv[i] > 0) {
       mbar_wait(&o_done[i], (n_kv[i] - 1) & 1);
@@ -387,6 +542,362 @@ __global__ void __maxnreg__(136)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+#if DS_FA_STAMPS
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const long long t0 = fa_stamps[0][0][0];
+    for (int j = 0; j < min(J, 64); ++j)
+      printf("FA j=%2d  S0 %7lld P0 %7lld mmaP0 %7lld K %7lld | S1 %7lld P1 %7lld mmaP1 %7lld\n", j,
+             fa_stamps[0][j][0] - t0, fa_stamps[0][j][1] - t0, fa_stamps[0][j][2] - t0, fa_stamps[0][j][3] - t0,
+             fa_stamps[1][j][0] - t0, fa_stamps[1][j][1] - t0, fa_stamps[1][j][2] - t0);
+  }
+#endif
+}
+
+// ----------------------------------------------------------------------
+// Split-half variant (the default): each 128-key block's scores are produced
+// and consumed in two 64-key halves.  QK of half h of the next block only
+// waits for P.V of half h of this block, so the tensor pipe always holds
+// the other half's work while a softmax warp exponentiates: a tile's softmax
+// may take up to ~2x its MMA time before the tensor pipe idles (with whole
+// tiles it stalls as soon as the softmax outlasts one tile's QK + P.V).
+// Measured reason (tools/fa stamps): one 128-key softmax pass takes ~2000
+// cycles with both tiles' softmax warps sharing an SM sub-partition, against
+// 1024 cycles of MMA per tile.
+//
+// TMEM per Q tile i: S [128i, 128i+128); half h's scores in columns 64h..,
+// its bf16 P in columns 64h..64h+31 (over consumed scores).  O as before.
+// Softmax: 32-column chunks against a running max (p <= 2^8 always); a max
+// that moves by more than 2^8 rescales the P chunk of the current half and O
+// (after the P.V half issued last has completed) -- in practice only the
+// first chunk of the first block.
+// ----------------------------------------------------------------------
+template <int D>
+__global__ void __maxnreg__(136)
+    fa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
+  using L = FaTcSmem<D>;
+  constexpr int CH = L::CH;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 3;
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 7;
+  uint64_t* s_full = bars + 9;   // [tile][half]
+  uint64_t* p_full = bars + 13;  // [tile][half]
+  uint64_t* o_done = bars + 17;  // [tile][half]: P.V of that half complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  auto sQ = [&](int i, int c) { return smem + L::Q + (i * CH + c) * L::CHUNK; };
+  auto sK = [&](int st, int c) { return smem + L::K + (st * CH + c) * L::CHUNK; };
+  auto sV = [&](int st, int c) { return smem + L::V + (st * CH + c) * L::CHUNK; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x;
+  const int q0 = (gridDim.y - 1 - blockIdx.y) * 2 * FA_BM;  // heaviest (latest) blocks first
+  const int g = h / (a.n_heads / a.n_kv_heads);
+  auto rowpos = [&](int r) { return a.q_pos ? __ldg(a.q_pos + r) : a.q_pos0 + r; };
+  int n_kv[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int rows = min(FA_BM, a.n_q - (q0 + i * FA_BM));
+    n_kv[i] = rows > 0 ? rowpos(q0 + i * FA_BM + rows - 1) / FA_BN + 1 : 0;
+  }
+  const int J = max(n_kv[0], n_kv[1]);
+  const int max_key = rowpos(min(q0 + 2 * FA_BM, a.n_q) - 1);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&o_done[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int n_tiles = n_kv[1] > 0 ? 2 : 1;
+      mbar_expect_tx(q_full, n_tiles * CH * L::CHUNK);
+      for (int i = 0; i < n_tiles; ++i)
+        for (int c = 0; c < CH; ++c) tma_load_2d(sQ(i, c), &tmQ, q_full, h * D + c * 64, q0 + i * FA_BM);
+      for (int j = 0; j < J; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        int rows[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          int page = 2 * j + p;
+          if (page * 64 > max_key) page = 2 * j;  // beyond the window: duplicate a valid page (finite, masked)
+          const int tp = a.table ? __ldg(a.table + page) : page;
+          rows[p] = (int)(g * a.k_head_rows + (long long)tp * a.k_page_rows);
+        }
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sK(st, c) + p * 64 * 128, &tmK, &k_full[st], c * 64, rows[p]);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sV(st, c) + p * 64 * 128, &tmV, &v_full[st], c * 64, rows[p]);
+      }
+    }
+  } else if (warp == 1) {
+    // whole warp runs the issue code (uniform descriptors), one elected lane issues
+    constexpr uint32_t IDESC_QK = umma_idesc_bf16(FA_BM, FA_BN / 2);
+    constexpr uint32_t IDESC_PV = umma_idesc_bf16_bmn(FA_BM, D);
+    auto qk = [&](int i, int hf, int st) {  // S_i[:, half hf] = Q_i K_half^T
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ad = sdesc_sw128(smem_u32(sQ(i, c)) + k * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(smem_u32(sK(st, c)) + hf * 8192 + k * 32, 16, 1024);
+          if (elect_one()) umma_bf16(tmem + i * 128 + hf * 64, ad, bd, IDESC_QK, (c | k) != 0 ? 1u : 0u);
+        }
+      if (elect_one()) umma_commit(&s_full[2 * i + hf]);
+      __syncwarp();
+    };
+    auto pv = [&](int i, int hf, int st, int j) {  // O_i += P_half V_half
+#pragma unroll
+      for (int s = 0; s < FA_BN / 32; ++s) {
+        const uint64_t bd = sdesc_sw128(smem_u32(sV(st, 0)) + (hf * 4 + s) * 2048, L::CHUNK, 1024);
+        if (elect_one())
+          umma_bf16_ts(tmem + 256 + i * 128, tmem + i * 128 + hf * 64 + s * 8, bd, IDESC_PV,
+                       (j | hf | s) != 0 ? 1u : 0u);
+      }
+      if (elect_one()) umma_commit(&o_done[2 * i + hf]);
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait(&k_full[0], 0);
+    tc_fence_after();
+    for (int i = 0; i < 2; ++i)
+      if (n_kv[i] > 0) {
+        qk(i, 0, 0);
+        qk(i, 1, 0);
+      }
+    if (elect_one()) umma_commit(&k_empty[0]);
+    __syncwarp();
+    for (int j = 0; j < J; ++j) {
+      const int st = j & 1, st1 = (j + 1) & 1;
+      const bool more = j + 1 < J;
+      mbar_wait(&v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (j * FA_BN + FA_BN - 1 > max_key) {
+        // keys past the window end: zero their V rows so p = 0 never meets a
+        // non-finite cache value (a SW128 row's 128 bytes stay within the row)
+        const int first = max_key + 1 - j * FA_BN;
+        for (int c = 0; c < CH; ++c) {
+          const uint32_t base = smem_u32(sV(st, c));
+          for (int off = first * 128 + lane * 16; off < FA_BN * 128; off += 32 * 16)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + off), "r"(0u) : "memory");
+        }
+        fence_async_shared();
+        __syncwarp();
+      }
+      bool k_ready = false;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (j < n_kv[i]) {
+            mbar_wait(&p_full[2 * i + hf], j & 1);
+            if (lane == 0) FA_STAMP(i, j, 4 + hf);
+            tc_fence_after();
+            pv(i, hf, st, j);
+          }
+          if (hf == 1 && i == 1) {
+            if (elect_one()) umma_commit(&v_empty[st]);
+            __syncwarp();
+          }
+          if (j + 1 < n_kv[i]) {
+            if (!k_ready) {
+              mbar_wait(&k_full[st1], ((j + 1) >> 1) & 1);
+              tc_fence_after();
+              k_ready = true;
+            }
+            qk(i, hf, st1);
+          }
+        }
+      if (more) {
+        if (elect_one()) umma_commit(&k_empty[st1]);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int i = (warp - 2) >> 2;  // Q tile
+    const int quarter = warp & 3;   // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const int first_row = min(q0 + i * FA_BM, a.n_q - 1);
+    const int tile_pos0 = rowpos(first_row);
+    const int qpos = q0 + i * FA_BM + row < a.n_q ? rowpos(q0 + i * FA_BM + row) : max_key;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + i * 128;
+    const uint32_t tO = tmem + lane_base + 256 + i * 128;
+    const float sc = a.scale_log2;
+    const float thr = 8.0f / sc;
+    const float2 sc2 = make_float2(sc, sc);
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv[i]; ++j) {
+      const int kbase = j * FA_BN;
+      const bool maskit = kbase + FA_BN - 1 > tile_pos0;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        mbar_wait(&s_full[2 * i + hf], j & 1);
+        if (lane == 0 && quarter == 0) FA_STAMP(i, j, 2 * hf);
+        tc_fence_after();
+        uint32_t sa[32], sb[32];
+        tmem_ld32_nowait(tS + hf * 64, sa);
+        tmem_wait_ld();
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hf + cc;  // chunk: keys kbase + 32c ..
+          uint32_t* cur = cc ? sb : sa;
+          if (cc == 0) tmem_ld32_nowait(tS + hf * 64 + 32, sb);
+          if (maskit) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (kbase + 32 * c + e > qpos) cur[e] = __float_as_uint(-INFINITY);
+          }
+          float mx4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            mx4[q] = fmax3(__uint_as_float(cur[q]), __uint_as_float(cur[q + 4]), __uint_as_float(cur[q + 8]));
+#pragma unroll
+          for (int e = 12; e < 32; e += 8)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              mx4[q] = fmax3(mx4[q], __uint_as_float(cur[e + q]), __uint_as_float(cur[e + 4 + q]));
+          const float cm = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+          const bool need = cm > m_used + thr;
+          if (__any_sync(0xffffffffu, need)) {
+            float f = 1.f;
+            if (need) {
+              f = fast_exp2((m_used - cm) * sc);  // 0 while m_used is -inf
+              m_used = cm;
+            }
+            l *= f;
+            if (cc == 1) {  // this half's first P chunk is already in TMEM
+              tmem_wait_st();
+              uint32_t pr[16];
+              tmem_ld16_nowait(tS + hf * 64, pr);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const float2 v = unpack_bf16x2(pr[e]);
+                pr[e] = pack_bf16x2(v.x * f, v.y * f);
+              }
+              tmem_st16_nowait(tS + hf * 64, pr);
+            }
+            if (j > 0 || hf > 0) {
+              // O holds P.V of every half released so far: wait for the last
+              // one -- half a of this block, or half b of the previous one.
+              // (One barrier per half: each is at most one phase behind here,
+              // so the parity wait cannot alias.)
+              if (hf) mbar_wait(&o_done[2 * i], j & 1);
+              else mbar_wait(&o_done[2 * i + 1], (j - 1) & 1);
+              tc_fence_after();
+#pragma unroll 1
+              for (int oc = 0; oc < D / 32; ++oc) {
+                uint32_t orow[32];
+                tmem_ld32_nowait(tO + oc * 32, orow);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * f);
+                tmem_st32_nowait(tO + oc * 32, orow);
+              }
+            }
+          }
+          const float msc = m_used * sc;
+          const float2 nmsc2 = make_float2(-msc, -msc);
+          float2 sum4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 x =
+                ffma2(make_float2(__uint_as_float(cur[2 * e]), __uint_as_float(cur[2 * e + 1])), sc2, nmsc2);
+            float2 p;
+            if (DS_FA_EMU_MOD && (e % (DS_FA_EMU_MOD > 0 ? DS_FA_EMU_MOD : 1)) == DS_FA_EMU_MOD - 1)
+              p = exp2_fma2(x);
+            else
+              p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+            sum4[e & 3] = fadd2(sum4[e & 3], p);
+            pk[e] = pack_bf16x2(p.x, p.y);
+          }
+          tmem_st16_nowait(tS + hf * 64 + cc * 16, pk);
+          const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+          l += s2.x + s2.y;
+          if (cc == 0) {
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) asm volatile("" : "+r"(sb[e]));  // valid only after the wait
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0 && quarter == 0) FA_STAMP(i, j, 2 * hf + 1);
+        if (lane == 0) mbar_arrive(&p_full[2 * i + hf]);
+      }
+    }
+    if (n_kv[i] > 0) {
+      mbar_wait(&o_done[2 * i + 1], (n_kv[i] - 1) & 1);  // the last P.V half
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const int qrow = q0 + i * FA_BM + row;
+      bf16* dst = a.o + (long long)qrow * a.ldo + (long long)h * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t orow[32];
+        tmem_ld32_nowait(tO + c * 32, orow);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack_bf16x2(__uint_as_float(orow[2 * e]) * inv, __uint_as_float(orow[2 * e + 1]) * inv);
+        if (qrow < a.n_q) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) st_global_v4(dst + c * 32 + e * 8, pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+#if DS_FA_STAMPS
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const long long t0 = fa_stamps[0][0][0];
+    for (int j = 0; j < min(J, 64); ++j)
+      printf("FA j=%2d | t0: Sa %7lld Pa %7lld Sb %7lld Pb %7lld pvA %7lld pvB %7lld | t1: Sa %7lld Pa %7lld Sb %7lld Pb %7lld pvA %7lld pvB %7lld\n", j,
+             fa_stamps[0][j][0] - t0, fa_stamps[0][j][1] - t0, fa_stamps[0][j][2] - t0, fa_stamps[0][j][3] - t0,
+             fa_stamps[0][j][4] - t0, fa_stamps[0][j][5] - t0,
+             fa_stamps[1][j][0] - t0, fa_stamps[1][j][1] - t0, fa_stamps[1][j][2] - t0, fa_stamps[1][j][3] - t0,
+             fa_stamps[1][j][4] - t0, fa_stamps[1][j][5] - t0);
+  }
+#endif
 }
 
 template <int D>
@@ -401,11 +912,17 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
     return launch_status(cudaErrorInvalidValue);
   FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, q_pos, head_stride / D, page_stride / D, table, o, ldo,
              (float)(1.4426950408889634 / sqrt((double)D))};
-  static PerDevice attr;
-  if (int rc_ = launch_status(ensure_smem_attr(fa_tc_kernel<D>, L::TOTAL, attr))) return rc_;
+  // DS_FA_VARIANT: 0 whole-tile softmax (round 1), 1 whole-tile chunked (default), 2 split halves
+  static const int variant = [] {
+    const char* e = getenv("DS_FA_VARIANT");
+    return e ? atoi(e) : 1;
+  }();
+  auto kern = variant == 0 ? fa_tc_kernel<D, false> : variant == 1 ? fa_tc_kernel<D, true> : fa_split_kernel<D>;
+  static PerDevice attr[3];
+  if (int rc_ = launch_status(ensure_smem_attr(kern, L::TOTAL, attr[variant < 0 || variant > 2 ? 2 : variant]))) return rc_;
   dim3 grid(n_heads, (n_q + 2 * FA_BM - 1) / (2 * FA_BM));
   count_launch();
-  return launch_status(launch_pdl(fa_tc_kernel<D>, grid, dim3(FA_THREADS), L::TOTAL, stream, tq, tk, tv, a));
+  return launch_status(launch_pdl(kern, grid, dim3(FA_THREADS), L::TOTAL, stream, tq, tk, tv, a));
 }
 
 int attention_prefill_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer,
