@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--vocab", type=int, default=128256, help="32000 = Mistral-7B shape (config 3)")
     ap.add_argument("--batch", type=int, default=1,
                     help="N>1: requests per consumer per step (config 4 batched requests; each its own prefix)")
+    ap.add_argument("--batch-leg", default="4,8",
+                    help="N=1: batched-request sizes for the config-4 leg (comma list, empty to skip)")
     ap.add_argument("--same-device", action="store_true",
                     help="debug: run every rank on cuda:0 with gloo (exercises the N>1 code path on one GPU)")
     return ap.parse_args()
@@ -366,6 +368,70 @@ def time_kernel(fn, reps, stream):
     return statistics.median(s.elapsed_time(e) for s, e in zip(starts, ends))
 
 
+def batch_leg(P, _lib, cfg, A, B, rc, n, sizes, single_ttft_ms, single_anchor_ms, dev, stream, side):
+    """BASELINE config 4 on one consumer GPU: a batch of requests (each its own
+    8K prefix and producer export) through partial_prefill_batch -- the recompute
+    request by request, every request's KV ingest on the copy stream, then ONE
+    batched anchor pass that streams each layer's weights once for all rows --
+    and a batched greedy decode over the resulting caches.  Reported against the
+    single-request fused step and the single-row anchor pass."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2411_02820_b200.quality import decode_greedy_batch
+    out = {}
+    dsteps = 32
+    for nb in sizes:
+        ids = [np.random.default_rng(500 + b).integers(0, cfg.vocab_size, size=n, dtype=np.int64) for b in range(nb)]
+        toks = [torch.from_numpy(x).to(dev) for x in ids]
+        prods = [P.full_prefill(A, x, e_layers=rc.transition_layers, tokens_dev=t) for x, t in zip(ids, toks)]
+        caches = [P.PagedKV.allocate(cfg, n + dsteps, dev, zero=False) for _ in range(nb)]
+        kvs, es = [p.kv for p in prods], [p.e_map() for p in prods]
+        ws = torch.empty(P.engine.batch_workspace_bytes(cfg, n + dsteps, nb), dtype=torch.uint8, device=dev)
+        torch.cuda.synchronize()
+
+        def prefill():
+            with torch.cuda.stream(stream):
+                return P.partial_prefill_batch(B, ids, rc, kvs, es, out=caches, stream=stream, copy_stream=side,
+                                               workspace=ws)
+        res = prefill()
+        ttft = time_kernel(prefill, 3, stream)
+        # the batched anchor pass alone over the caches just written
+        anc_ids = torch.tensor([int(x[-1]) for x in ids], dtype=torch.int64, device=dev)
+        pos = (ctypes.c_int32 * nb)(*([n - 1] * nb))
+        descs = (_lib.KvCache * nb)(*[c.desc() for c in caches])
+        lg = torch.empty(nb, cfg.vocab_size, device=dev)
+        tk = torch.empty(nb, dtype=torch.int32, device=dev)
+        bdesc = B.desc()
+        anc = time_kernel(lambda: _lib.check(_lib.lib().ds_anchor_batch(
+            ctypes.byref(bdesc), nb, anc_ids.data_ptr(), pos, descs, lg.data_ptr(), tk.data_ptr(), ws.data_ptr(),
+            ws.numel(), stream.cuda_stream)), 5, stream)
+        # batched greedy decode: dsteps tokens per sequence after the prefills
+        with torch.cuda.stream(stream):
+            decode_greedy_batch(B, caches, res, 2, [n] * nb)  # warm-up
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            decode_greedy_batch(B, caches, res, dsteps + 1, [n] * nb)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        dec = e0.elapsed_time(e1) / dsteps
+        out[str(nb)] = {
+            "ttft_ms": round(ttft, 3), "ms_per_request": round(ttft / nb, 3), "tok_s": nb * n / (ttft / 1e3),
+            "vs_single_requests_back_to_back": round(nb * single_ttft_ms / ttft, 3),
+            "anchor_ms": round(anc, 3), "anchor_ms_per_request": round(anc / nb, 3),
+            "anchor_per_request_vs_single": round(anc / nb / single_anchor_ms, 3),
+            "decode_ms_per_step": round(dec, 3), "decode_tok_s": nb * 1e3 / dec,
+        }
+        del prods, caches, res, ws, kvs, es
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    return {"sizes": out, "n_tokens": n, "decode_steps": dsteps,
+            "note": "each request its own prefix and producer export; batch TTFT = time to every request's "
+                    "first token; anchor and decode rows share one weight stream per layer"}
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
@@ -622,6 +688,9 @@ def run_ours(args, world, rank, local):
             wsa.data_ptr(), wsa.numel(), stream.cuda_stream)), 10, stream)
         kern["anchor_pass"] = {"ms": ms, "gbs": anchor_bytes / ms / 1e6, "bytes": anchor_bytes}
     torch.cuda.synchronize()
+    sizes = [int(x) for x in args.batch_leg.split(",") if x.strip()]
+    batch = batch_leg(P, _lib, cfg, A, B, rc, n, sizes, ttft_ms, kern["anchor_pass"]["ms"], dev, stream, side) \
+        if sizes and world == 1 else None
 
     gemm = kern["gemm_w1_silu"]
     traffic = None
@@ -661,6 +730,7 @@ def run_ours(args, world, rank, local):
                        "gbs": kern["anchor_pass"]["bytes"] / dec_ms / 1e6,
                        "note": "greedy decode after the partial prefill, one anchor pass per token; "
                                "the token stream is copied to the host once, at the end"},
+            "batch": batch,
             "gpu_launches": int(launches),
             "e2e": {"value": world * n / e2e_ttft, "unit": "tok/s", "ttft_p50_ms": e2e_ttft * 1e3,
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 4 * cfg.vocab_size + 4},

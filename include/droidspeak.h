@@ -223,6 +223,47 @@ DS_API int ds_decode_greedy(const ds_model* m, const ds_kv_cache* kv, int32_t po
                             int32_t steps, int32_t* tokens_out, void* workspace, size_t workspace_bytes,
                             void* stream);
 
+/* ---- batched requests (config 4: a consumer's batch of requests; batched decode) ----
+ * The anchor rows of a batch share ONE stream of the weights per layer (a
+ * GEMV over up to DS_MAX_BATCH rows) and one attention launch; each row's
+ * arithmetic is the single-request pass's, so a batch gives its requests'
+ * one-by-one results bit for bit.  Workspace: ds_workspace_size_batch(dims,
+ * longest request (or positions + steps), batch). */
+#define DS_MAX_BATCH 8
+DS_API size_t ds_workspace_size_batch(const ds_dims* dims, int32_t max_tokens, int32_t batch);
+
+/* `batch` partial prefills (model.py:660-679) with one RecomputeConfig, each
+ * request its own tokens (varlen), producer export and output cache:
+ *   tokens_host / tokens_dev  [batch] pointers (tokens_dev may be NULL or hold NULLs)
+ *   sender_kv  [batch] (a request without an export: k = v = NULL), sender_e [batch]
+ *   pointers to n_e[b] E caches; out_kv [batch]; logits_out device f32 [batch][V];
+ *   token_out device int32 [batch].
+ * Validation per request in the reference's order, requests in order; on error
+ * *bad_request names the request (and *miss_layer / *miss_kind the miss).
+ * copy_stream (optional): every request's reused-layer KV ingest beside the
+ * compute stream's recompute of the batch; then one batched anchor pass. */
+DS_API int ds_partial_prefill_batch(const ds_model* m, int32_t batch, const int64_t* const* tokens_host,
+                                    const int64_t* const* tokens_dev, const int32_t* n_tokens, const int32_t* groups,
+                                    int32_t n_groups, const ds_kv_cache* sender_kv, const ds_e_cache* const* sender_e,
+                                    const int32_t* n_e, const ds_kv_cache* out_kv, float* logits_out,
+                                    int32_t* token_out, void* workspace, size_t workspace_bytes,
+                                    void* compute_stream, void* copy_stream, int32_t* bad_request,
+                                    int32_t* miss_layer, int32_t* miss_kind);
+
+/* Batched anchor pass (ds_anchor for `batch` rows): row b = token
+ * anchor_tokens_dev[b] at position positions[b] (host) over kv[b]; logits
+ * [batch][V], token_out [batch]. */
+DS_API int ds_anchor_batch(const ds_model* m, int32_t batch, const int64_t* anchor_tokens_dev, const int32_t* positions,
+                           const ds_kv_cache* kv, float* logits_out, int32_t* token_out, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* Batched greedy decode (ds_decode_greedy for `batch` sequences, each its own
+ * cache and length): tokens_out device int32 [batch][steps]; first_token
+ * device int32 [batch]; positions host int32 [batch]. */
+DS_API int ds_decode_greedy_batch(const ds_model* m, int32_t batch, const ds_kv_cache* kv, const int32_t* positions,
+                                  const int32_t* first_token, int32_t steps, int32_t* tokens_out, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* ---- producer -> consumer over NVLink (P2P pull through CUDA IPC) ----
  * The producer exports a device buffer once; a consumer process maps it and
  * hands the mapped pointer to ds_kv_ingest (ds_kv_cache.k/v or layer_k/v) and

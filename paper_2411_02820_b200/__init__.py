@@ -17,6 +17,7 @@ from .engine import (
     full_prefill,
     make_synthetic_dataset,
     partial_prefill,
+    partial_prefill_batch,
     token_selective_prefill,
     workspace_bytes,
 )
@@ -33,7 +34,7 @@ __all__ = [
     "CapturedPartialPrefill", "CacheMissError", "CapacityError", "DegenerateInputError", "ECache", "LayerKV", "MixedPrefill",
     "ModelConfig", "ModelWeights", "PagedKV", "PerturbationSpec", "PrefillResult", "RecomputeConfig",
     "SchemaError", "build_model", "check_tokens", "full_prefill", "make_synthetic_dataset", "model_ident",
-    "partial_prefill", "random_model", "token_selective_prefill", "reference_weights", "workspace_bytes",
+    "partial_prefill", "partial_prefill_batch", "random_model", "token_selective_prefill", "reference_weights", "workspace_bytes",
     "AdaptDecision", "CostModel", "ScheduledRequest", "SloPolicy", "adapt_config", "estimate_ttft", "plan", "build_frontier", "enumerate_groups", "load_profile",
     "save_profile", "select_by_layer_budget", "select_by_quality_floor", "CacheKey", "CacheStore", "FetchedKV",
     "KVSlice", "context_hash", "fetch_context_caches", "store_prefill",

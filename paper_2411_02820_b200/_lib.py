@@ -85,6 +85,11 @@ def lib() -> C.CDLL:
             "ds_token_selective_prefill": (I32, [C.POINTER(Model), P, P, I32, C.POINTER(KvCache), C.c_double,
                                                  C.POINTER(KvCache), P, P, C.POINTER(I32), P, SZ, P, C.POINTER(I32)]),
             "ds_decode_greedy": (I32, [C.POINTER(Model), C.POINTER(KvCache), I32, P, I32, P, P, SZ, P]),
+            "ds_workspace_size_batch": (SZ, [C.POINTER(Dims), I32, I32]),
+            "ds_partial_prefill_batch": (I32, [C.POINTER(Model), I32, P, P, P, P, I32, P, P, P, P, P, P, P, SZ, P,
+                                               P, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)]),
+            "ds_anchor_batch": (I32, [C.POINTER(Model), I32, P, P, P, P, P, P, SZ, P]),
+            "ds_decode_greedy_batch": (I32, [C.POINTER(Model), I32, P, P, P, I32, P, P, SZ, P]),
             "ds_ipc_export": (I32, [P, P, C.POINTER(C.c_uint64)]),
             "ds_ipc_open": (I32, [P, C.c_uint64, C.POINTER(P), C.POINTER(P)]),
             "ds_ipc_close": (I32, [P]),
@@ -120,7 +125,8 @@ EXPORTED_SYMBOLS = ("ds_abi_version", "ds_last_error", "ds_launch_count", "ds_wo
                     "ds_full_prefill", "ds_gemm", "ds_rmsnorm", "ds_attention_prefill", "ds_recompute_group",
                     "ds_anchor", "ds_token_selective_prefill", "ds_decode_greedy", "ds_ipc_export", "ds_ipc_open", "ds_ipc_close",
                     "ds_trace_begin", "ds_trace_end", "ds_anchor_placement", "ds_anchor_timeline",
-                    "ds_set_anchor_shape", "ds_fused_fallbacks")
+                    "ds_set_anchor_shape", "ds_fused_fallbacks", "ds_workspace_size_batch",
+                    "ds_partial_prefill_batch", "ds_anchor_batch", "ds_decode_greedy_batch")
 
 
 class anchor_shape:

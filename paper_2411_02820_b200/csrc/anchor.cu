@@ -32,6 +32,7 @@
 //                  a stream event.
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -150,9 +151,11 @@ DS_DEV void gemv_prefetch(const GemvArgs& a, int t) {
 // Stage the input vector in shared memory as bf16 (RMSNorm fused when a.gain).
 // `sync`: a barrier over the 128 staging threads (default: the whole CTA).
 DS_DEV void cta_sync() { __syncthreads(); }
-template <void (*Sync)() = cta_sync>
-DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+// tid: the thread's index among the 128 staging threads (a batched GEMV runs
+// one staging group per 128-thread consumer warpgroup).
+template <typename SyncF>
+DS_DEV void gemv_stage_x_t(const GemvArgs& a, bf16* xs, float* ssq, int tid, SyncF sync) {
+  const int warp = tid >> 5, lane = tid & 31;
   const bool active = tid < GEMV_THREADS;
   if (a.x_f32) {
     float inv = 1.f;
@@ -160,12 +163,13 @@ DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
       float ss = 0.f;
       for (int k = tid * 4; active && k < a.K; k += GEMV_THREADS * 4) {
         const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k));
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        // explicit roundings: every kernel that inlines this gets the same bits
+        ss = __fadd_rn(ss, __fmaf_rn(v.w, v.w, __fmaf_rn(v.z, v.z, __fmaf_rn(v.y, v.y, __fmul_rn(v.x, v.x)))));
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       if (lane == 0 && active) ssq[warp] = ss;
-      Sync();
+      sync();
       float t = 0.f;
 #pragma unroll
       for (int w = 0; w < GEMV_WARPS; ++w) t += ssq[w];
@@ -183,7 +187,11 @@ DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
     for (int k = tid * 8; active && k < a.K; k += GEMV_THREADS * 8)
       *reinterpret_cast<uint4*>(xs + k) = ld_cg16(a.x_bf16 + k);
   }
-  Sync();
+  sync();
+}
+template <void (*Sync)() = cta_sync>
+DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
+  gemv_stage_x_t(a, xs, ssq, (int)threadIdx.x, [] { Sync(); });
 }
 
 // The 128 accumulating threads' per-row pair sums -> row results (warp
@@ -195,9 +203,8 @@ DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
 struct EpiPre {
   float a, b;
 };
-DS_DEV EpiPre gemv_epi_pre(const GemvArgs& a, int t) {
+DS_DEV EpiPre gemv_epi_pre(const GemvArgs& a, int t, int tid = threadIdx.x) {
   EpiPre e{0.f, 0.f};
-  const int tid = threadIdx.x;
   if (a.mode == EPI_QKV_ROPE) {
     if (tid < 4) {
       const int r0 = gemv_row(a, t, tid);
@@ -213,8 +220,8 @@ DS_DEV EpiPre gemv_epi_pre(const GemvArgs& a, int t) {
 
 template <typename Sync>
 DS_DEV void gemv_finish(const GemvArgs& a, int t, const float2* s2, float (*red)[GEMV_ROWS], unsigned long long& best,
-                        const EpiPre& pre, Sync sync) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+                        const EpiPre& pre, Sync sync, int tid = threadIdx.x) {
+  const int warp = tid >> 5, lane = tid & 31;
   float s[GEMV_ROWS];
 #pragma unroll
   for (int r = 0; r < GEMV_ROWS; ++r) s[r] = s2[r].x + s2[r].y;
@@ -244,8 +251,10 @@ DS_DEV void gemv_finish(const GemvArgs& a, int t, const float2* s2, float (*red)
       if (is_q || is_k) {
         const float cs = pre.a, sn = pre.b;
         const float x1 = lo, x2 = hi;
-        lo = x1 * cs - x2 * sn;
-        hi = x1 * sn + x2 * cs;
+        // explicit roundings (no FMA contraction, whose choice may differ
+        // between the kernels inlining this): one result for every launch shape
+        lo = __fsub_rn(__fmul_rn(x1, cs), __fmul_rn(x2, sn));
+        hi = __fadd_rn(__fmul_rn(x1, sn), __fmul_rn(x2, cs));
       }
       bf16* dst = is_q ? a.q_out + (long long)head * a.head_dim
                        : (is_k ? a.kv.k + a.kv.off(head - a.n_heads, a.pos)
@@ -571,6 +580,245 @@ int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged) {
   return launch_status(launch_pdl(gemv_kernel, dim3(grid), dim3(GEMV_THREADS), smem, stream, a));
 }
 
+// ---------------------------------------------------------------- batched GEMV
+//
+// nb anchor rows (one per request of a consumer's batch, or one per sequence
+// of a batched decode step) against ONE stream of the weights: the TMA ring
+// of gemv_tma_kernel, read by WG consumer warpgroups of 128 threads, each
+// holding up to NBW rows' accumulators.  Row b's x is staged (RMSNorm'ed) by
+// its warpgroup exactly as the single-row kernel stages it; thread t of the
+// warpgroup accumulates chunks t, t+128, ... in ascending order for each row,
+// and gemv_finish reduces and runs the epilogue per row -- so every row's
+// result is the single-row GEMV's bit for bit, with the weight bytes read once
+// per launch instead of once per row.
+DS_DEV void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+DS_HOST_DEV_INLINE GemvArgs gemv_row_view(const GemvArgs& a, const GemvBatch& bt, int b) {
+  GemvArgs v = a;
+  if (v.x_f32) v.x_f32 += b * bt.x_stride;
+  if (v.x_bf16) v.x_bf16 += b * bt.x_stride;
+  if (v.out_f32) v.out_f32 += b * bt.out_stride;
+  if (v.resid) v.resid += b * bt.out_stride;
+  if (v.out_bf16) v.out_bf16 += b * bt.out_stride;
+  if (v.q_out) v.q_out += b * bt.q_stride;
+  if (v.argmax) v.argmax += b;
+  v.pos = bt.pos[b];
+  v.kv = bt.kv[b];
+  return v;
+}
+
+// Two rows per warpgroup and one warpgroup per row pair: the per-thread
+// instruction count per weight byte stays near the single-row kernel's (each
+// bf16 pair is unpacked once and feeds 2 rows' FFMA2s), and the SM runs
+// WG + 1 warps per sub-partition instead of one, so the FMA / issue work of
+// several rows never throttles the weight stream (4 rows on one warpgroup: 3.5x
+// slower than one row).  Registers: every CTA must fit beside one
+// persistent-anchor warp (2.8 K registers) per SM sub-partition, which holds
+// WG + 1 of this kernel's warps.
+template <int KS, int NBW, int WG>
+__global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80)))
+    gemv_batch_kernel(const __grid_constant__ GemvArgs a, const __grid_constant__ GemvBatch bt, int slots) {
+  constexpr int SLOT = GEMV_ROWS * KS * 2;
+  constexpr int CPT = KS / (GEMV_THREADS * 8);
+  constexpr int NC = WG * GEMV_THREADS;
+  extern __shared__ __align__(128) uint8_t smem_dyn[];
+  uint8_t* ring = smem_dyn;
+  bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * SLOT);  // [nb][K]
+  __shared__ __align__(8) uint64_t full[16], empty[16];
+  __shared__ float red[WG][GEMV_WARPS][GEMV_ROWS];
+  __shared__ float ssq[WG][GEMV_WARPS];
+  const int tid = threadIdx.x;
+  const int tiles = a.N / GEMV_ROWS, ks = a.K / KS;
+  if (tid == NC) {
+    for (int i = 0; i < slots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], WG * GEMV_WARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  if (tid >= NC) {
+    if (tid == NC) {  // producer: the weights never depend on the predecessor
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int s = 0; s < ks; ++s) {
+          mbar_wait(&empty[slot], phase ^ 1);
+          mbar_expect_tx(&full[slot], SLOT);
+#pragma unroll
+          for (int r = 0; r < GEMV_ROWS; ++r)
+            bulk_g2s(ring + slot * SLOT + r * KS * 2, a.W + (long long)gemv_row(a, t, r) * a.ldw + (long long)s * KS,
+                     KS * 2, &full[slot]);
+          if (++slot == slots) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+    }
+    return;
+  }
+  const int wg = tid / GEMV_THREADS, t = tid - wg * GEMV_THREADS;
+  const int b0 = wg * NBW;
+  const int nbw = min(NBW, bt.nb - b0);
+  auto sync = [wg] { bar_named(1 + wg, GEMV_THREADS); };
+  pdl_wait();
+  for (int i = 0; i < nbw; ++i) {
+    const GemvArgs v = gemv_row_view(a, bt, b0 + i);
+    gemv_stage_x_t(v, xs + (long long)(b0 + i) * a.K, ssq[wg], t, sync);
+  }
+  int slot = 0;
+  uint32_t phase = 0;
+  unsigned long long best[NBW];
+#pragma unroll
+  for (int i = 0; i < NBW; ++i) best[i] = 0ull;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    EpiPre pre[NBW];
+#pragma unroll
+    for (int i = 0; i < NBW; ++i) pre[i] = i < nbw ? gemv_epi_pre(gemv_row_view(a, bt, b0 + i), tile, t) : EpiPre{0.f, 0.f};
+    float2 s2[NBW][GEMV_ROWS];
+#pragma unroll
+    for (int i = 0; i < NBW; ++i)
+#pragma unroll
+      for (int r = 0; r < GEMV_ROWS; ++r) s2[i][r] = make_float2(0.f, 0.f);
+    for (int s = 0; s < ks; ++s) {
+      mbar_wait(&full[slot], phase);
+#pragma unroll
+      for (int cc = 0; cc < CPT; ++cc) {
+        const int c = s * (KS / 8) + cc * GEMV_THREADS + t;  // this thread's chunk
+        float2 xf[NBW][4];
+#pragma unroll
+        for (int i = 0; i < NBW; ++i) {
+          const uint4 xv = i < nbw ? *reinterpret_cast<const uint4*>(xs + (long long)(b0 + i) * a.K + c * 8)
+                                   : make_uint4(0u, 0u, 0u, 0u);
+          xf[i][0] = bf16x2_to_float2(xv.x);
+          xf[i][1] = bf16x2_to_float2(xv.y);
+          xf[i][2] = bf16x2_to_float2(xv.z);
+          xf[i][3] = bf16x2_to_float2(xv.w);
+        }
+#pragma unroll
+        for (int r = 0; r < GEMV_ROWS; ++r) {
+          const uint4 w =
+              *reinterpret_cast<const uint4*>(ring + slot * SLOT + r * KS * 2 + (cc * GEMV_THREADS + t) * 16);
+          const float2 w0 = bf16x2_to_float2(w.x), w1 = bf16x2_to_float2(w.y);
+          const float2 w2 = bf16x2_to_float2(w.z), w3 = bf16x2_to_float2(w.w);
+#pragma unroll
+          for (int i = 0; i < NBW; ++i) {
+            if (i < nbw) {
+              s2[i][r] = ffma2(w0, xf[i][0], s2[i][r]);
+              s2[i][r] = ffma2(w1, xf[i][1], s2[i][r]);
+              s2[i][r] = ffma2(w2, xf[i][2], s2[i][r]);
+              s2[i][r] = ffma2(w3, xf[i][3], s2[i][r]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
+      if (++slot == slots) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NBW; ++i)
+      if (i < nbw) gemv_finish(gemv_row_view(a, bt, b0 + i), tile, s2[i], red[wg], best[i], pre[i], sync, t);
+  }
+  if (a.mode == EPI_STORE_F32 && a.argmax && t < GEMV_ROWS) {
+#pragma unroll
+    for (int i = 0; i < NBW; ++i) {
+      unsigned long long bb = best[i];
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0x000000ffu, bb, o);
+        bb = other > bb ? other : bb;
+      }
+      if (t == 0 && i < nbw && bb) atomicMax(a.argmax + b0 + i, bb);
+    }
+  }
+}
+
+template <int KS, int NBW, int WG>
+static int gemv_batch_launch_t(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream) {
+  constexpr int SLOT = GEMV_ROWS * KS * 2;
+  const int xbytes = (bt.nb * a.K * 2 + 127) & ~127;
+  static const int budget = env_int("DS_GEMV_SMEM_KB", 196) * 1024;  // fits beside a persistent anchor CTA
+  int slots = (budget - xbytes) / SLOT;
+  slots = slots > 16 ? 16 : slots;
+  if (slots < 2) return DS_ERR_INVALID;
+  const int smem = slots * SLOT + xbytes;
+  auto kern = gemv_batch_kernel<KS, NBW, WG>;
+  static PerDevice attr;
+  if (int rc_ = launch_status(ensure_smem_attr(kern, smem, attr))) return rc_;
+  const int tiles = a.N / GEMV_ROWS, cap = num_sms();
+  const int grid = tiles < cap ? tiles : cap;
+  count_launch();
+  return launch_status(launch_pdl(kern, dim3(grid), dim3(WG * GEMV_THREADS + 32), smem, stream, a, bt, slots));
+}
+
+template <int KS>
+static int gemv_batch_launch_ks(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream) {
+  switch ((bt.nb + 1) / 2) {
+    case 1: return gemv_batch_launch_t<KS, 2, 1>(a, bt, stream);
+    case 2: return gemv_batch_launch_t<KS, 2, 2>(a, bt, stream);
+    case 3: return gemv_batch_launch_t<KS, 2, 3>(a, bt, stream);
+    default: return gemv_batch_launch_t<KS, 2, 4>(a, bt, stream);
+  }
+}
+
+// Rows per launch: as many as fit in shared memory beside a 2-slot ring (W2 at
+// d_ff = 14336: 4 rows of 28 KB; the 8B shape's other GEMVs: 8).  Shapes the
+// TMA kernel does not take (K not a multiple of 1024, fewer tiles than SMs)
+// run the single-row GEMV per row -- the same bits.
+int gemv_batch_launch(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream) {
+  if (bt.nb < 1 || bt.nb > kMaxBatch) return DS_ERR_INVALID;
+  if ((a.N % GEMV_ROWS) || (a.K & 7) || (a.mode == EPI_SWIGLU_BF16 && a.N % 32)) return DS_ERR_INVALID;
+  if (a.mode == EPI_QKV_ROPE && (a.head_dim % 8 || a.N % a.head_dim)) return DS_ERR_INVALID;
+  const int ks = a.K % 4096 == 0 ? 4096 : (a.K % 2048 == 0 ? 2048 : 1024);
+  static const int budget = env_int("DS_GEMV_SMEM_KB", 196) * 1024;
+  int fit = (budget - 2 * GEMV_ROWS * ks * 2) / (a.K * 2);
+  fit = fit > kMaxBatch ? kMaxBatch : fit;
+  const bool tma = gemv_tma_enabled() && a.K % 1024 == 0 && a.N / GEMV_ROWS >= 148 && fit >= 2 && bt.nb > 1;
+  if (!tma) {
+    for (int b = 0; b < bt.nb; ++b)
+      if (int rc = gemv_launch(gemv_row_view(a, bt, b), stream)) return rc;
+    return DS_OK;
+  }
+  for (int b0 = 0; b0 < bt.nb; b0 += fit) {
+    GemvArgs sa = gemv_row_view(a, bt, b0);  // row b0 becomes row 0 of the launch
+    GemvBatch sb = bt;
+    sb.nb = bt.nb - b0 < fit ? bt.nb - b0 : fit;
+    for (int i = 0; i < sb.nb; ++i) {
+      sb.pos[i] = bt.pos[b0 + i];
+      sb.kv[i] = bt.kv[b0 + i];
+    }
+    int rc = DS_ERR_INVALID;
+    if (ks == 4096) rc = gemv_batch_launch_ks<4096>(sa, sb, stream);
+    else if (ks == 2048) rc = gemv_batch_launch_ks<2048>(sa, sb, stream);
+    else rc = gemv_batch_launch_ks<1024>(sa, sb, stream);
+    if (rc) return rc;
+  }
+  return DS_OK;
+}
+
+__global__ void argmax_finalize_batch_kernel(const unsigned long long* packed, int nb, int32_t* token,
+                                             int token_stride, int64_t* token64) {
+  const int b = threadIdx.x;
+  if (b >= nb) return;
+  const int32_t t = (int32_t)(0xFFFFFFFFu - (uint32_t)(packed[b] & 0xFFFFFFFFull));
+  if (token) token[(long long)b * token_stride] = t;
+  if (token64) token64[b] = t;
+}
+
+int argmax_finalize_batch_launch(const unsigned long long* packed, int nb, int32_t* token, int token_stride,
+                                 int64_t* token64, cudaStream_t stream) {
+  count_launch();
+  static PerDevice carve;
+  prefer_max_smem_once(argmax_finalize_batch_kernel, carve);
+  argmax_finalize_batch_kernel<<<1, 32, 0, stream>>>(packed, nb, token, token_stride, token64);
+  return launch_status();
+}
+
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream) {
   count_launch();
   static PerDevice carve;
@@ -711,7 +959,7 @@ DS_DEV void attn_finish(const AttnArgs& a, int g, int s, float* sc, const float*
       for (int s2 = lane; s2 < a.splits; s2 += 32) {
         const float w = exp2f(__ldcg(ml + 2 * s2) - M);
         wts[r * a.splits + s2] = w;
-        dn += w * __ldcg(ml + 2 * s2 + 1);
+        dn = __fmaf_rn(w, __ldcg(ml + 2 * s2 + 1), dn);
       }
 #pragma unroll
       for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
@@ -961,7 +1209,7 @@ DS_DEV void attn_finish_wide(const AttnArgs& a, int g, int s, float* sc, const f
       for (int s2 = lane; s2 < a.splits; s2 += 32) {
         const float w = exp2f((staged ? ml[2 * s2] : __ldcg(ml + 2 * s2)) - M);
         wts[r * a.splits + s2] = w;
-        dn += w * (staged ? ml[2 * s2 + 1] : __ldcg(ml + 2 * s2 + 1));
+        dn = __fmaf_rn(w, staged ? ml[2 * s2 + 1] : __ldcg(ml + 2 * s2 + 1), dn);
       }
 #pragma unroll
       for (int off = 16; off; off >>= 1) dn += __shfl_xor_sync(0xffffffffu, dn, off);
@@ -1000,8 +1248,9 @@ __device__ unsigned int g_att_launch;
   } while (0)
 #endif
 
+// One (kv head, split) item of row `a` (the kernel body; `item` replaces item).
 template <int D, int R>
-__global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnArgs a, int slots, int prefetch) {
+DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) {
 #if DS_ATT_STAMPS
   unsigned long long st_ns[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -1022,7 +1271,7 @@ __global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnAr
   __shared__ float stat[2 * R];
   __shared__ unsigned int is_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = blockIdx.x / a.splits, s = blockIdx.x - g * a.splits;
+  const int g = item / a.splits, s = item - g * a.splits;
   const int k0 = s * a.split_keys;
   const int nk = min(a.split_keys, a.n_keys - k0);
   const int sk = a.split_keys;
@@ -1036,7 +1285,7 @@ __global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnAr
     fence_mbar_init();
   }
   // optionally pull the whole item toward L2 first (the ring then reads L2)
-  if (prefetch & 1) attn_prefetch(a, blockIdx.x, D);
+  if (prefetch & 1) attn_prefetch(a, item, D);
   // timing experiments (results are wrong): data movement only, or no scores / no P.V math
   const bool no_scores = prefetch & 6, no_pv = prefetch & 10;
   __syncthreads();
@@ -1233,9 +1482,30 @@ __global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(AttnAr
     if (launch == 100 && (s == 0 || s == a.splits - 1 || is_last))
       printf("ATT %d %d %d last=%d %llu %llu %llu %llu %llu %llu %llu\n", launch, g, s, (int)is_last, st_ns[0], st_ns[1],
              st_ns[2], st_ns[3], st_ns[4], st_ns[5], st_ns[6]);
-    if (blockIdx.x == 0) atomicAdd(&g_att_launch, 1u);
+    if (item == 0) atomicAdd(&g_att_launch, 1u);
   }
 #endif
+}
+
+template <int D, int R>
+__global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_decode_tma_kernel(const __grid_constant__ AttnArgs a, int slots,
+                                                                          int prefetch) {
+  attn_tma_item<D, R>(a, blockIdx.x, slots, prefetch);
+}
+
+// Batched rows: CTA x serves item x - start[b] of row b (start[] = running
+// item counts).  Each row keeps its own splits, scratch and merge counters.
+struct AttnBatch {
+  AttnArgs r[kMaxBatch];
+  int start[kMaxBatch + 1];
+  int nb;
+};
+template <int D, int R>
+__global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_batch_tma_kernel(const __grid_constant__ AttnBatch ab, int slots,
+                                                                         int prefetch) {
+  int b = 0;
+  while (b + 1 < ab.nb && (int)blockIdx.x >= ab.start[b + 1]) ++b;
+  attn_tma_item<D, R>(ab.r[b], (int)blockIdx.x - ab.start[b], slots, prefetch);
 }
 
 template <int D, int R>
@@ -1285,6 +1555,52 @@ int decode_attention_launch(AttnArgs a, int head_dim, cudaStream_t stream) {
   DS_ATT_CASE(128, 1) DS_ATT_CASE(128, 2) DS_ATT_CASE(128, 4) DS_ATT_CASE(128, 8)
   DS_ATT_CASE(64, 1) DS_ATT_CASE(64, 2) DS_ATT_CASE(64, 4) DS_ATT_CASE(64, 8)
 #undef DS_ATT_CASE
+  return launch_status(e);
+}
+
+template <int D, int R>
+static cudaError_t attn_batch_launch_t(const AttnBatch& ab, int smem, cudaStream_t stream) {
+  static const int slots_env = env_int("DS_ATT_SLOTS", 12);
+  static const int prefetch = env_int("DS_ATT_PREFETCH", 0);
+  const int slots = slots_env < 2 ? 2 : (slots_env > ATT_SLOTS_MAX ? ATT_SLOTS_MAX : slots_env);
+  auto kern = attn_batch_tma_kernel<D, R>;
+  static PerDevice attr;
+  const int total = slots * ATT_PIECE * D * 2 + smem;
+  if (cudaError_t e = ensure_smem_attr(kern, total, attr)) return e;
+  return launch_pdl(kern, dim3(ab.start[ab.nb]), dim3(ATT_TTHREADS), total, stream, ab, slots, prefetch);
+}
+
+int decode_attention_batch_launch(const AttnArgs* rows, int nb, int head_dim, cudaStream_t stream) {
+  if (nb < 1 || nb > kMaxBatch) return DS_ERR_INVALID;
+  const int R = rows[0].n_heads / rows[0].n_kv_heads;
+  if ((R != 1 && R != 2 && R != 4 && R != 8) || (head_dim != 64 && head_dim != 128)) return DS_ERR_INVALID;
+  if (nb == 1 || !attn_tma_enabled()) {
+    for (int b = 0; b < nb; ++b)
+      if (int rc = decode_attention_launch(rows[b], head_dim, stream)) return rc;
+    return DS_OK;
+  }
+  static thread_local AttnBatch ab;
+  memset(&ab, 0, sizeof(ab));
+  ab.nb = nb;
+  int smem = 0;
+  for (int b = 0; b < nb; ++b) {
+    AttnArgs a = rows[b];
+    if (a.n_keys < 1 || a.n_heads != rows[0].n_heads || a.n_kv_heads != rows[0].n_kv_heads) return DS_ERR_INVALID;
+    a.split_keys = attn_split_keys(a.n_keys, a.n_kv_heads, R);
+    a.splits = (a.n_keys + a.split_keys - 1) / a.split_keys;
+    a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+    const int sm = attn_smem_bytes(R, a.split_keys, a.splits);
+    smem = sm > smem ? sm : smem;
+    ab.r[b] = a;
+    ab.start[b + 1] = ab.start[b] + a.n_kv_heads * a.splits;
+  }
+  count_launch();
+  cudaError_t e = cudaErrorInvalidValue;
+#define DS_ATTB_CASE(DD, RR) \
+  if (head_dim == DD && R == RR) e = attn_batch_launch_t<DD, RR>(ab, smem, stream);
+  DS_ATTB_CASE(128, 1) DS_ATTB_CASE(128, 2) DS_ATTB_CASE(128, 4) DS_ATTB_CASE(128, 8)
+  DS_ATTB_CASE(64, 1) DS_ATTB_CASE(64, 2) DS_ATTB_CASE(64, 4) DS_ATTB_CASE(64, 8)
+#undef DS_ATTB_CASE
   return launch_status(e);
 }
 

@@ -596,6 +596,184 @@ int anchor_pass(Ctx& c, const int64_t* token_id, int P, float* logits, int32_t* 
   return rc;
 }
 
+// ---------------------------------------------------------------- batched anchor rows
+//
+// Config 4's batch of requests on one consumer, and batched greedy decode:
+// nb anchor rows (each its own cache, position and token) through every
+// layer against ONE stream of the weights per layer (gemv_batch_launch), the
+// attention of every row in one launch (decode_attention_batch_launch), and
+// one lm-head pass.  Row b's arithmetic is the single-row per-launch pass's
+// bit for bit (same kernels' per-row order), so a batch equals its requests
+// run one by one.
+struct BatchWs {
+  int64_t* tokens;  // [nb][n_max] staged request ids
+  int64_t* ids;     // [nb] anchor token ids (the seed gather)
+  float* h;         // [nb][d] residual stream of each row
+  bf16* a;          // [nb][d] seed scratch
+  bf16* q;          // [nb][H*D]
+  bf16* o;          // [nb][H*D]
+  bf16* u;          // [nb][d_ff]
+  float* part_o;    // [nb][splits][H*D]
+  float* part_ml;   // [nb][splits][H][2]
+  unsigned int* count;         // [nb][KVH] split-merge counters
+  unsigned long long* argmax;  // [nb]
+  int64_t* tok64;   // [nb] greedy tokens feeding the next decode step
+  float* logits;    // [nb][V] decode-step logits
+  long long splits;  // per-row split capacity
+  size_t bytes;
+};
+
+BatchWs carve_batch(const ds_dims& m, int n_max, int nb, void* base) {
+  BatchWs w{};
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> uint8_t* {
+    uint8_t* r = p ? p + off : nullptr;
+    off += align_up(bytes);
+    return r;
+  };
+  const size_t hd = (size_t)m.n_heads * m.head_dim;
+  w.splits = attn_max_splits(n_max, m.n_kv_heads, m.n_heads / (m.n_kv_heads > 0 ? m.n_kv_heads : 1));
+  w.tokens = reinterpret_cast<int64_t*>(take(8ull * nb * n_max));
+  w.ids = reinterpret_cast<int64_t*>(take(8ull * nb));
+  w.h = reinterpret_cast<float*>(take(4ull * nb * m.d_model));
+  w.a = reinterpret_cast<bf16*>(take(2ull * nb * m.d_model));
+  w.q = reinterpret_cast<bf16*>(take(2ull * nb * hd));
+  w.o = reinterpret_cast<bf16*>(take(2ull * nb * hd));
+  w.u = reinterpret_cast<bf16*>(take(2ull * nb * m.d_ff));
+  w.part_o = reinterpret_cast<float*>(take(4ull * nb * w.splits * hd));
+  w.part_ml = reinterpret_cast<float*>(take(8ull * nb * w.splits * m.n_heads));
+  w.count = reinterpret_cast<unsigned int*>(take(4ull * nb * m.n_kv_heads));
+  w.argmax = reinterpret_cast<unsigned long long*>(take(8ull * nb));
+  w.tok64 = reinterpret_cast<int64_t*>(take(8ull * nb));
+  w.logits = reinterpret_cast<float*>(take(4ull * nb * m.vocab_size));
+  w.bytes = off;
+  return w;
+}
+
+// The batch section follows the single-request workspace of n_max rows.
+size_t batch_ws_bytes(const ds_dims& d, int n_max, int nb) {
+  return carve(d, n_max, nullptr).bytes + carve_batch(d, n_max, nb, nullptr).bytes;
+}
+
+int anchor_layer_batch(const ds_model* m, BatchWs& bw, const ds_kv_cache* kv, const int* pos, int nb, int l,
+                       cudaStream_t s) {
+  const ds_dims& d = m->dims;
+  const ds_layer_weights& W = m->layers[l];
+  const int hd = d.n_heads * d.head_dim, kvd = d.n_kv_heads * d.head_dim;
+  GemvBatch bt{};
+  bt.nb = nb;
+  for (int b = 0; b < nb; ++b) {
+    bt.pos[b] = pos[b];
+    bt.kv[b] = layer_addr(kv[b], l, d.head_dim);
+  }
+  GemvArgs g{};
+  g.W = static_cast<const bf16*>(W.wqkv);
+  g.ldw = d.d_model;
+  g.N = hd + 2 * kvd;
+  g.K = d.d_model;
+  g.x_f32 = bw.h;
+  g.gain = W.g_attn;
+  g.mode = EPI_QKV_ROPE;
+  g.n_heads = d.n_heads;
+  g.n_kv_heads = d.n_kv_heads;
+  g.head_dim = d.head_dim;
+  g.q_out = bw.q;
+  g.rope_cos = m->rope_cos;
+  g.rope_sin = m->rope_sin;
+  bt.x_stride = d.d_model;
+  bt.q_stride = hd;
+  DS_TRY(gemv_batch_launch(g, bt, s), "batched anchor qkv");
+  AttnArgs rows[kMaxBatch];
+  for (int b = 0; b < nb; ++b) {
+    AttnArgs& at = rows[b];
+    at = AttnArgs{};
+    at.q = bw.q + (long long)b * hd;
+    at.lo = at.hi = bt.kv[b];
+    at.n_lo = pos[b];
+    at.n_keys = pos[b] + 1;
+    at.n_heads = d.n_heads;
+    at.n_kv_heads = d.n_kv_heads;
+    at.part_o = bw.part_o + (long long)b * bw.splits * hd;
+    at.part_ml = bw.part_ml + (long long)b * bw.splits * d.n_heads * 2;
+    at.counters = bw.count + (long long)b * d.n_kv_heads;
+    at.out = bw.o + (long long)b * hd;
+  }
+  DS_TRY(decode_attention_batch_launch(rows, nb, d.head_dim, s), "batched anchor attention");
+  GemvArgs o{};
+  o.W = static_cast<const bf16*>(W.wo);
+  o.ldw = hd;
+  o.N = d.d_model;
+  o.K = hd;
+  o.x_bf16 = bw.o;
+  o.mode = EPI_RESID_F32;
+  o.out_f32 = bw.h;
+  o.resid = bw.h;
+  bt.x_stride = hd;
+  bt.out_stride = d.d_model;
+  DS_TRY(gemv_batch_launch(o, bt, s), "batched anchor o-proj");
+  GemvArgs f{};
+  f.W = static_cast<const bf16*>(W.w1);
+  f.ldw = d.d_model;
+  f.N = d.mlp_kind == DS_MLP_SWIGLU ? 2 * d.d_ff : d.d_ff;
+  f.K = d.d_model;
+  f.x_f32 = bw.h;
+  f.gain = W.g_mlp;
+  f.mode = d.mlp_kind == DS_MLP_SWIGLU ? EPI_SWIGLU_BF16 : EPI_SILU_BF16;
+  f.out_bf16 = bw.u;
+  bt.x_stride = d.d_model;
+  bt.out_stride = d.d_ff;
+  DS_TRY(gemv_batch_launch(f, bt, s), "batched anchor w1");
+  GemvArgs s2{};
+  s2.W = static_cast<const bf16*>(W.w2);
+  s2.ldw = d.d_ff;
+  s2.N = d.d_model;
+  s2.K = d.d_ff;
+  s2.x_bf16 = bw.u;
+  s2.mode = EPI_RESID_F32;
+  s2.out_f32 = bw.h;
+  s2.resid = bw.h;
+  bt.x_stride = d.d_ff;
+  bt.out_stride = d.d_model;
+  DS_TRY(gemv_batch_launch(s2, bt, s), "batched anchor w2");
+  return DS_OK;
+}
+
+// ids: device [nb] token of each row; pos: host [nb] position of each row.
+// logits [nb][V]; token[b * token_stride] (optional) and tok64[b] (optional)
+// receive the greedy tokens.
+int anchor_pass_batch(const ds_model* m, BatchWs& bw, const ds_kv_cache* kv, const int* pos, int nb,
+                      const int64_t* ids, float* logits, int32_t* token, int token_stride, int64_t* tok64,
+                      cudaStream_t s) {
+  const ds_dims& d = m->dims;
+  if (cudaMemsetAsync(bw.count, 0, 4ull * nb * d.n_kv_heads, s) != cudaSuccess) return cuda_fail("memset");
+  DS_TRY(rmsnorm_launch(m->embed, true, ids, nb, d.d_model, m->layers[0].g_attn, bw.a, bw.h, nullptr, nb, s),
+         "batched anchor seed");
+  for (int l = 0; l < d.n_layers; ++l) {
+    if (int rc = anchor_layer_batch(m, bw, kv, pos, nb, l, s)) return rc;
+    trace(s, DS_TRACE_ANCHOR + l);
+  }
+  if (cudaMemsetAsync(bw.argmax, 0, 8ull * nb, s) != cudaSuccess) return cuda_fail("memset");
+  GemvArgs g{};
+  g.W = static_cast<const bf16*>(m->unembed);
+  g.ldw = d.d_model;
+  g.N = d.vocab_size;
+  g.K = d.d_model;
+  g.x_f32 = bw.h;
+  g.gain = m->g_final;
+  g.mode = EPI_STORE_F32;
+  g.out_f32 = logits;
+  g.argmax = bw.argmax;
+  GemvBatch bt{};
+  bt.nb = nb;
+  bt.x_stride = d.d_model;
+  bt.out_stride = d.vocab_size;
+  DS_TRY(gemv_batch_launch(g, bt, s), "batched lm head");
+  if (token || tok64) DS_TRY(argmax_finalize_batch_launch(bw.argmax, nb, token, token_stride, tok64, s), "argmax");
+  trace(s, DS_TRACE_LOGITS);
+  return DS_OK;
+}
+
 const int64_t* stage_tokens(const int64_t* host, const int64_t* dev, int n, Workspace& w, cudaStream_t s) {
   if (dev) return dev;
   if (cudaMemcpyAsync(w.tokens, host, 8ull * n, cudaMemcpyHostToDevice, s) != cudaSuccess) return nullptr;
@@ -1223,6 +1401,196 @@ int ds_full_prefill(const ds_model* m, const int64_t* tokens_host, const int64_t
   std::vector<char> covered(L, 1);
   return prefill_core(c, tok, n, all, 1, seed, nullptr, reused, covered, logits_out, token_out,
                       copy_stream ? (cudaStream_t)copy_stream : s);
+}
+
+size_t ds_workspace_size_batch(const ds_dims* dims, int32_t max_tokens, int32_t batch) {
+  if (!dims || max_tokens < 1 || batch < 1 || batch > kMaxBatch) return 0;
+  return batch_ws_bytes(*dims, max_tokens, batch);
+}
+
+int ds_partial_prefill_batch(const ds_model* m, int32_t batch, const int64_t* const* tokens_host,
+                             const int64_t* const* tokens_dev, const int32_t* n_tokens, const int32_t* groups,
+                             int32_t n_groups, const ds_kv_cache* sender_kv, const ds_e_cache* const* sender_e,
+                             const int32_t* n_e, const ds_kv_cache* out_kv, float* logits_out, int32_t* token_out,
+                             void* workspace, size_t workspace_bytes, void* compute_stream, void* copy_stream,
+                             int32_t* bad_request, int32_t* miss_layer, int32_t* miss_kind) {
+  g_err.clear();
+  if (miss_kind) *miss_kind = DS_MISS_NONE;
+  if (bad_request) *bad_request = -1;
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if (batch < 1 || batch > kMaxBatch) return fail(DS_ERR_INVALID, "batch %d outside [1,%d]", batch, kMaxBatch);
+  if (!tokens_host || !n_tokens || !out_kv || !logits_out) return fail(DS_ERR_INVALID, "batch arrays are NULL");
+  const int L = d.n_layers, nb = batch;
+  // each request in the reference's order (check_tokens, validate_for, KV
+  // misses ascending, E per group); requests in order
+  std::vector<char> covered(L, 0);
+  std::vector<int32_t> reused;
+  std::vector<std::vector<const ds_e_cache*>> seed(nb, std::vector<const ds_e_cache*>(n_groups > 0 ? n_groups : 0));
+  int n_max = 0;
+  for (int b = 0; b < nb; ++b) {
+    auto bad = [&](int code) {
+      if (bad_request) *bad_request = b;
+      return code;
+    };
+    if ((rc = check_tokens(d, tokens_host[b], n_tokens[b]))) return bad(rc);
+    const int n = n_tokens[b], P = n - 1;
+    n_max = n > n_max ? n : n_max;
+    if (b == 0) {
+      if (n_groups < 0 || (n_groups && !groups)) return bad(fail(DS_ERR_INVALID, "bad groups"));
+      for (int i = 0; i < n_groups; ++i) {
+        const int a = groups[2 * i], e = groups[2 * i + 1];
+        if (a < 0 || a > e) return bad(fail(DS_ERR_INVALID, "range [%d,%d] invalid", a, e));
+        if (i && a <= groups[2 * i - 1] + 1) return bad(fail(DS_ERR_INVALID, "groups not in normal form"));
+        if (e > L - 1) return bad(fail(DS_ERR_INVALID, "config exceeds layer range [0,%d]", L - 1));
+        for (int l = a; l <= e; ++l) covered[l] = 1;
+      }
+      for (int l = 0; l < L; ++l)
+        if (!covered[l]) reused.push_back(l);
+    }
+    if ((rc = check_cache(&out_kv[b], d, n, "output"))) return bad(rc);
+    for (int l : reused) {
+      const ds_kv_cache* skv = sender_kv ? &sender_kv[b] : nullptr;
+      if (!skv || !kv_layer_present(*skv, l) || skv->positions < P) {
+        if (miss_layer) *miss_layer = l;
+        if (miss_kind) *miss_kind = DS_MISS_KV;
+        return bad(fail(DS_ERR_CACHE_MISS, "request %d: missing kv cache for layer %d", b, l));
+      }
+    }
+    for (int i = 0; i < n_groups; ++i) {
+      const int a = groups[2 * i];
+      if (a == 0) continue;
+      const int ne = n_e ? n_e[b] : 0;
+      for (int j = 0; j < ne; ++j)
+        if (sender_e && sender_e[b] && sender_e[b][j].layer == a) seed[b][i] = &sender_e[b][j];
+      const ds_e_cache* e = seed[b][i];
+      if (!e || !e->hidden || e->positions < P || e->width != d.d_model) {
+        if (miss_layer) *miss_layer = a;
+        if (miss_kind) *miss_kind = DS_MISS_E;
+        return bad(fail(DS_ERR_CACHE_MISS, "request %d: missing e cache for layer %d", b, a));
+      }
+    }
+  }
+  Workspace w = carve(d, n_max, workspace);
+  BatchWs bw = carve_batch(d, n_max, nb, workspace ? static_cast<uint8_t*>(workspace) + w.bytes : nullptr);
+  if (!workspace || workspace_bytes < w.bytes + bw.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes + bw.bytes);
+  cudaStream_t cs = (cudaStream_t)compute_stream;
+  cudaStream_t xs = copy_stream ? (cudaStream_t)copy_stream : cs;
+  std::vector<const int64_t*> tok(nb);
+  for (int b = 0; b < nb; ++b) {
+    if (tokens_dev && tokens_dev[b]) {
+      tok[b] = tokens_dev[b];
+    } else {
+      int64_t* dst = bw.tokens + (long long)b * n_max;
+      if (cudaMemcpyAsync(dst, tokens_host[b], 8ull * n_tokens[b], cudaMemcpyHostToDevice, cs) != cudaSuccess)
+        return cuda_fail("token upload");
+      tok[b] = dst;
+    }
+  }
+  trace(cs, 0);
+  // copy stream: every request's reused layers into its cache (HBM-bound),
+  // beside the compute stream's tensor-bound recompute of the batch
+  thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!ev_fork && (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                   cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess))
+    return cuda_fail("event");
+  if (!reused.empty()) {
+    if (xs != cs) {
+      if (cudaEventRecord(ev_fork, cs) != cudaSuccess || cudaStreamWaitEvent(xs, ev_fork, 0) != cudaSuccess)
+        return cuda_fail("fork");
+    }
+    for (int b = 0; b < nb; ++b)
+      DS_TRY(kv_ingest_launch(sender_kv[b], out_kv[b], reused.data(), (int)reused.size(), d.n_kv_heads, d.head_dim,
+                              n_tokens[b] - 1, xs),
+             "kv ingest");
+    trace(xs, DS_TRACE_INGEST);
+  }
+  for (int b = 0; b < nb; ++b) {
+    Ctx c{m, d, w, &out_kv[b], cs};
+    for (int i = 0; i < n_groups; ++i) {
+      rc = recompute_group(c, tok[b], n_tokens[b] - 1, groups[2 * i], groups[2 * i + 1],
+                           seed[b][i] ? seed[b][i]->hidden : nullptr);
+      if (rc) return rc;
+    }
+  }
+  std::vector<int> pos(nb);
+  for (int b = 0; b < nb; ++b) {
+    pos[b] = n_tokens[b] - 1;
+    if (cudaMemcpyAsync(bw.ids + b, tok[b] + pos[b], 8, cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+      return cuda_fail("anchor ids");
+  }
+  if (!reused.empty() && xs != cs) {
+    if (cudaEventRecord(ev_join, xs) != cudaSuccess || cudaStreamWaitEvent(cs, ev_join, 0) != cudaSuccess)
+      return cuda_fail("join");
+  }
+  return anchor_pass_batch(m, bw, out_kv, pos.data(), nb, bw.ids, logits_out, token_out, 1, nullptr, cs);
+}
+
+int ds_anchor_batch(const ds_model* m, int32_t batch, const int64_t* anchor_tokens_dev, const int32_t* positions,
+                    const ds_kv_cache* kv, float* logits_out, int32_t* token_out, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if (batch < 1 || batch > kMaxBatch) return fail(DS_ERR_INVALID, "batch %d outside [1,%d]", batch, kMaxBatch);
+  if (!anchor_tokens_dev || !positions || !kv || !logits_out)
+    return fail(DS_ERR_INVALID, "anchor tokens, positions, caches and logits_out are required");
+  int n_max = 0;
+  std::vector<int> pos(batch);
+  for (int b = 0; b < batch; ++b) {
+    if (positions[b] < 1) return fail(DS_ERR_DEGENERATE, "row %d: need at least 2 tokens", b);
+    if (positions[b] + 1 > d.max_seq) return fail(DS_ERR_INVALID, "row %d: position %d beyond max_seq", b, positions[b]);
+    if ((rc = check_cache(&kv[b], d, positions[b] + 1, "cache"))) return rc;
+    pos[b] = positions[b];
+    n_max = positions[b] + 1 > n_max ? positions[b] + 1 : n_max;
+  }
+  Workspace w = carve(d, n_max, workspace);
+  BatchWs bw = carve_batch(d, n_max, batch, workspace ? static_cast<uint8_t*>(workspace) + w.bytes : nullptr);
+  if (!workspace || workspace_bytes < w.bytes + bw.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes + bw.bytes);
+  return anchor_pass_batch(m, bw, kv, pos.data(), batch, anchor_tokens_dev, logits_out, token_out, 1, nullptr,
+                           (cudaStream_t)stream);
+}
+
+int ds_decode_greedy_batch(const ds_model* m, int32_t batch, const ds_kv_cache* kv, const int32_t* positions,
+                           const int32_t* first_token, int32_t steps, int32_t* tokens_out, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!m || !m->layers) return fail(DS_ERR_INVALID, "model is NULL");
+  const ds_dims& d = m->dims;
+  int rc;
+  if ((rc = check_dims(d))) return rc;
+  if (batch < 1 || batch > kMaxBatch) return fail(DS_ERR_INVALID, "batch %d outside [1,%d]", batch, kMaxBatch);
+  if (steps < 1) return fail(DS_ERR_INVALID, "steps must be at least 1");
+  if (!kv || !positions || !first_token || !tokens_out) return fail(DS_ERR_INVALID, "batch arrays are NULL");
+  int n_max = 0;
+  for (int b = 0; b < batch; ++b) {
+    if (positions[b] < 1) return fail(DS_ERR_INVALID, "row %d: cache must hold at least one position", b);
+    if ((long long)positions[b] + steps > d.max_seq)
+      return fail(DS_ERR_INVALID, "row %d: decoding %d steps from %d positions exceeds max_seq %d", b, steps,
+                  positions[b], d.max_seq);
+    if ((rc = check_cache(&kv[b], d, positions[b] + steps - 1, "cache"))) return rc;
+    n_max = positions[b] + steps > n_max ? positions[b] + steps : n_max;
+  }
+  Workspace w = carve(d, n_max, workspace);
+  BatchWs bw = carve_batch(d, n_max, batch, workspace ? static_cast<uint8_t*>(workspace) + w.bytes : nullptr);
+  if (!workspace || workspace_bytes < w.bytes + bw.bytes)
+    return fail(DS_ERR_INVALID, "workspace of %zu bytes < required %zu", workspace_bytes, w.bytes + bw.bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int b = 0; b < batch; ++b)
+    DS_TRY(token_copy_launch(first_token + b, tokens_out + (long long)b * steps, bw.tok64 + b, s), "token copy");
+  std::vector<int> pos(batch);
+  for (int st = 1; st < steps; ++st) {
+    for (int b = 0; b < batch; ++b) pos[b] = positions[b] + st - 1;
+    rc = anchor_pass_batch(m, bw, kv, pos.data(), batch, bw.tok64, bw.logits, tokens_out + st, steps, bw.tok64, s);
+    if (rc) return rc;
+  }
+  return DS_OK;
 }
 
 }  // extern "C"

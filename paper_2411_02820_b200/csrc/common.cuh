@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #define DS_DEV __device__ __forceinline__
+#define DS_HOST_DEV_INLINE __host__ __device__ __forceinline__
 
 namespace ds {
 

@@ -185,6 +185,24 @@ struct GemvArgs {
 
 int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged = true);
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream);
+
+// Batched GEMV: nb rows (requests) against one weight stream.  Row b's view is
+// GemvArgs `a` with x / out / resid / out_bf16 advanced by b * stride, q_out by
+// b * q_stride, argmax by b, and the QKV epilogue's position and cache from
+// pos[b] / kv[b].  Every row's result is the single-row GEMV's bit for bit.
+constexpr int kMaxBatch = 8;
+struct GemvBatch {
+  int nb;
+  long long x_stride;    // elements between rows of x_f32 / x_bf16
+  long long out_stride;  // elements between rows of out_f32 / resid / out_bf16
+  long long q_stride;    // elements between rows of q_out
+  int pos[kMaxBatch];
+  KvAddr kv[kMaxBatch];
+};
+int gemv_batch_launch(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream);
+// token[b * token_stride] = token64[b] = argmax of row b's packed maxima
+int argmax_finalize_batch_launch(const unsigned long long* packed, int nb, int32_t* token, int token_stride,
+                                 int64_t* token64, cudaStream_t stream);
 int token_copy_launch(const int32_t* src, int32_t* dst32, int64_t* dst64, cudaStream_t stream);
 
 // Split-KV attention of one query row (the anchor / a decode step) over a
@@ -206,6 +224,10 @@ struct AttnArgs {
 int attn_split_keys(int n_keys, int n_kv_heads, int R);
 int attn_max_splits(int n_keys, int n_kv_heads, int R);  // workspace bound for any n <= n_keys
 int decode_attention_launch(AttnArgs a, int head_dim, cudaStream_t stream);
+// nb independent rows (each its own cache, keys and scratch) in one launch;
+// each row gets the splits decode_attention_launch would give it alone, so the
+// results are the single-row launches' bit for bit.
+int decode_attention_batch_launch(const AttnArgs* rows, int nb, int head_dim, cudaStream_t stream);
 
 // The whole anchor pass as one persistent kernel (one CTA per SM), see anchor.cu.
 constexpr int kAnchorClaimSlots = 256;  // > any SM id

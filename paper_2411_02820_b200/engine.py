@@ -118,7 +118,13 @@ class PagedKV:
 
     @classmethod
     def allocate(cls, config: ModelConfig, positions: int, device="cuda", spare_pages: int = 0,
-                 shuffle_seed: int | None = None) -> "PagedKV":
+                 shuffle_seed: int | None = None, zero: bool = True) -> "PagedKV":
+        """``zero=False`` skips the fill (1.07 GB at the 8B shape, 8K positions)
+        for a cache a prefill writes completely: every position < ``positions``
+        is written before anything reads it, and the kernels never let a value
+        past the written positions reach a result (the FA prefill masks those
+        keys' scores and zeroes their V rows in shared memory; the anchor and
+        decode attention read keys < n only)."""
         need = (positions + PAGE - 1) // PAGE
         pages = need + spare_pages
         shape = (config.n_layers, pages, config.n_kv_heads, PAGE, config.head_dim)
@@ -127,8 +133,9 @@ class PagedKV:
         else:
             g = torch.Generator().manual_seed(shuffle_seed)
             table = torch.randperm(pages, generator=g)[:need].to(torch.int32).to(device)
-        return cls(torch.zeros(shape, dtype=torch.bfloat16, device=device),
-                   torch.zeros(shape, dtype=torch.bfloat16, device=device), table, positions)
+        make = torch.zeros if zero else torch.empty
+        return cls(make(shape, dtype=torch.bfloat16, device=device), make(shape, dtype=torch.bfloat16, device=device),
+                   table, positions)
 
     def dense(self) -> LayerKV:
         """Gather into the reference [L, KVH, n, D] layout (tests / export)."""
@@ -289,7 +296,8 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
     e_map = _normalize_e(sender_e)
     s = stream if stream is not None else torch.cuda.current_stream(receiver.device)
     with torch.cuda.stream(s):  # outputs belong to the stream that writes them (allocator reuse)
-        cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device)
+        # every position of a fresh cache is written by this call: no zero fill
+        cache = out if out is not None else PagedKV.allocate(cfg, n, receiver.device, zero=False)
         logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=receiver.device)
         tok = torch.empty(1, dtype=torch.int32, device=receiver.device)
     ws = workspace if workspace is not None else _workspace(receiver, n, s)
@@ -311,6 +319,74 @@ def partial_prefill(receiver: ModelWeights, tokens, config: RecomputeConfig, sen
             copy_stream.cuda_stream if copy_stream is not None else None, C.byref(ml), C.byref(mk))
     L.check(rc, ml.value, mk.value)
     return MixedPrefill(kv=cache, logits=logits, token_dev=tok)
+
+
+MAX_BATCH = 8  # include/droidspeak.h DS_MAX_BATCH
+
+
+def batch_workspace_bytes(config: ModelConfig, max_tokens: int, batch: int) -> int:
+    dims = L.Dims(config.n_layers, config.d_model, config.n_heads, config.n_kv_heads, config.head_dim,
+                  config.d_ff, config.vocab_size, config.max_seq, L.MLP_KINDS[config.mlp_kind])
+    return int(L.lib().ds_workspace_size_batch(C.byref(dims), max_tokens, batch))
+
+
+def partial_prefill_batch(receiver: ModelWeights, tokens: Sequence, config: RecomputeConfig,
+                          sender_kv: Sequence[LayerKV | None], sender_e: Sequence | None = None, *,
+                          out: Sequence[PagedKV] | None = None, stream=None, copy_stream=None,
+                          workspace: torch.Tensor | None = None) -> list[MixedPrefill]:
+    """A consumer's batch of requests (BASELINE config 4): ``len(tokens)`` <= 8
+    partial prefills with one recompute config, each request its own prefix
+    (lengths may differ), producer export and output cache.  Each request is
+    validated in the reference's order (check_tokens, validate_for, KV misses
+    ascending, E per group; model.py:660-679), requests in order.  The
+    recompute runs request after request on ``stream`` while ``copy_stream``
+    ingests every request's reused layers; then ONE batched anchor pass streams
+    each layer's weights once for all rows.  Results equal the requests'
+    one-by-one :func:`partial_prefill` results bit for bit."""
+    cfg = receiver.config
+    nb = len(tokens)
+    if not 1 <= nb <= MAX_BATCH:
+        raise ValueError(f"batch of {nb} requests outside [1, {MAX_BATCH}]")
+    if len(sender_kv) != nb or (sender_e is not None and len(sender_e) != nb) or (out is not None and len(out) != nb):
+        raise ValueError("tokens, sender_kv, sender_e and out must have one entry per request")
+    ids = []
+    for t in tokens:
+        ids.append(check_tokens(t, cfg))
+        config.validate_for(cfg.n_layers)
+    ns = [x.shape[0] for x in ids]
+    e_maps = [_normalize_e(e) for e in (sender_e if sender_e is not None else [None] * nb)]
+    for em in e_maps:
+        for l, e in em.items():
+            if e.hidden.dtype != torch.float32 or not e.hidden.is_cuda or not e.hidden.is_contiguous():
+                raise ValueError(f"E cache of layer {l} must be a contiguous f32 device tensor")
+    s = stream if stream is not None else torch.cuda.current_stream(receiver.device)
+    with torch.cuda.stream(s):
+        caches = list(out) if out is not None else [PagedKV.allocate(cfg, n, receiver.device, zero=False) for n in ns]
+        logits = torch.empty(nb, cfg.vocab_size, dtype=torch.float32, device=receiver.device)
+        tok = torch.empty(nb, dtype=torch.int32, device=receiver.device)
+    if workspace is None:
+        need = batch_workspace_bytes(cfg, max(ns), nb)
+        with torch.cuda.stream(s):
+            workspace = torch.empty(need, dtype=torch.uint8, device=receiver.device)
+    groups = [x for g in config.groups for x in g]
+    ga = (C.c_int32 * max(1, len(groups)))(*groups)
+    th = (C.c_void_p * nb)(*[x.ctypes.data for x in ids])
+    nt = (C.c_int32 * nb)(*ns)
+    empty = L.KvCache()
+    skv = (L.KvCache * nb)(*[kv.desc() if kv is not None else empty for kv in sender_kv])
+    e_arrays = [(L.ECacheDesc * max(1, len(em)))(*[L.ECacheDesc(l, e.positions, e.hidden.shape[1], e.hidden.data_ptr())
+                                                   for l, e in sorted(em.items())]) for em in e_maps]
+    ep = (C.c_void_p * nb)(*[C.cast(a, C.c_void_p) for a in e_arrays])
+    ne = (C.c_int32 * nb)(*[len(em) for em in e_maps])
+    odesc = (L.KvCache * nb)(*[c.desc() for c in caches])
+    bad, ml, mk = C.c_int32(-1), C.c_int32(-1), C.c_int32(0)
+    with torch.cuda.device(receiver.device):
+        rc = L.lib().ds_partial_prefill_batch(
+            C.byref(receiver.desc()), nb, th, None, nt, ga, len(config.groups), skv, ep, ne, odesc,
+            logits.data_ptr(), tok.data_ptr(), workspace.data_ptr(), workspace.numel(), s.cuda_stream,
+            copy_stream.cuda_stream if copy_stream is not None else None, C.byref(bad), C.byref(ml), C.byref(mk))
+    L.check(rc, ml.value, mk.value)
+    return [MixedPrefill(kv=caches[b], logits=logits[b], token_dev=tok[b:b + 1]) for b in range(nb)]
 
 
 class CapturedPartialPrefill:

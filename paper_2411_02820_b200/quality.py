@@ -72,6 +72,39 @@ def decode_greedy(model, cache, last, steps: int, positions: int | None = None) 
     return out.cpu().numpy().astype(np.int64)
 
 
+def decode_greedy_batch(model, caches, lasts, steps: int, positions) -> np.ndarray:
+    """Greedy decode of up to 8 sequences at once (each its own cache and
+    length): one batched anchor pass per step streams the weights once for
+    every sequence.  Row b equals ``decode_greedy(model, caches[b], lasts[b],
+    steps, positions[b])`` token for token.  Returns int64 [batch, steps]."""
+    cfg = model.config
+    nb = len(caches)
+    if not 1 <= nb <= 8 or len(lasts) != nb or len(positions) != nb:
+        raise ValueError("caches, lasts and positions must have 1..8 matching entries")
+    if steps < 1:
+        raise ValueError("steps must be at least 1")
+    for c, p in zip(caches, positions):
+        if p < 1:
+            raise ValueError("cache must hold at least one position")
+        if p + steps > cfg.max_seq:
+            raise ValueError(f"decoding {steps} steps from {p} positions exceeds max_seq {cfg.max_seq}")
+        if p + steps - 1 > c.positions:
+            raise ValueError(f"cache capacity {c.positions} < {p + steps - 1} positions needed; allocate with reserve")
+    dev = model.device
+    first = torch.cat([getattr(x, "token_dev", x).reshape(1).to(torch.int32) for x in lasts])
+    out = torch.empty(nb, steps, dtype=torch.int32, device=dev)
+    need = int(L.lib().ds_workspace_size_batch(C.byref(model.desc().dims), max(p + steps for p in positions), nb))
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    descs = (L.KvCache * nb)(*[c.desc() for c in caches])
+    pos = (C.c_int32 * nb)(*[int(p) for p in positions])
+    with torch.cuda.device(dev):
+        rc = L.lib().ds_decode_greedy_batch(C.byref(model.desc()), nb, descs, pos, first.data_ptr(), steps,
+                                            out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                            torch.cuda.current_stream(dev).cuda_stream)
+    L.check(rc)
+    return out.cpu().numpy().astype(np.int64)
+
+
 def greedy_agreement(reference, candidate) -> Agreement:
     ref, cand = np.asarray(reference), np.asarray(candidate)
     if ref.shape != cand.shape:
