@@ -153,18 +153,39 @@ DS_DEV void gemv_prefetch(const GemvArgs& a, int t) {
 DS_DEV void cta_sync() { __syncthreads(); }
 // tid: the thread's index among the 128 staging threads (a batched GEMV runs
 // one staging group per 128-thread consumer warpgroup).
-template <typename SyncF>
+// The loads are issued in blocks of XB per thread before any is used (the
+// loop one-load-per-iteration form waited one L2 round trip per 512 columns:
+// ~15% of a batched GEMV's samples); for K <= XB * 512 the f32 row stays in
+// registers between the sum of squares and the normalisation.  Accumulation
+// order is unchanged (ascending k per thread).
+// XB: loads in flight per thread (8 in the TMA-staged kernels; 2 in the
+// register-capped persistent kernel, where more would spill).
+template <int GEMV_XB = 8, typename SyncF>
 DS_DEV void gemv_stage_x_t(const GemvArgs& a, bf16* xs, float* ssq, int tid, SyncF sync) {
   const int warp = tid >> 5, lane = tid & 31;
   const bool active = tid < GEMV_THREADS;
+  constexpr int STEP = GEMV_THREADS * 4;
   if (a.x_f32) {
+    float4 v[GEMV_XB];
+    const bool one_block = a.K <= GEMV_XB * STEP;
+    auto load_block = [&](int k0) {
+#pragma unroll
+      for (int u = 0; u < GEMV_XB; ++u) {
+        const int k = k0 + u * STEP;
+        v[u] = (active && k < a.K) ? __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
     float inv = 1.f;
     if (a.gain) {
       float ss = 0.f;
-      for (int k = tid * 4; active && k < a.K; k += GEMV_THREADS * 4) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k));
-        // explicit roundings: every kernel that inlines this gets the same bits
-        ss = __fadd_rn(ss, __fmaf_rn(v.w, v.w, __fmaf_rn(v.z, v.z, __fmaf_rn(v.y, v.y, __fmul_rn(v.x, v.x)))));
+      for (int k0 = tid * 4; k0 < a.K; k0 += GEMV_XB * STEP) {
+        load_block(k0);
+#pragma unroll
+        for (int u = 0; u < GEMV_XB; ++u)
+          if (active && k0 + u * STEP < a.K)
+            // explicit roundings: every kernel that inlines this gets the same bits
+            ss = __fadd_rn(ss, __fmaf_rn(v[u].w, v[u].w,
+                                         __fmaf_rn(v[u].z, v[u].z, __fmaf_rn(v[u].y, v[u].y, __fmul_rn(v[u].x, v[u].x)))));
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -175,23 +196,45 @@ DS_DEV void gemv_stage_x_t(const GemvArgs& a, bf16* xs, float* ssq, int tid, Syn
       for (int w = 0; w < GEMV_WARPS; ++w) t += ssq[w];
       inv = 1.0f / sqrtf(t / (float)a.K + 1e-6f);
     }
-    for (int k = tid * 4; active && k < a.K; k += GEMV_THREADS * 4) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(a.x_f32 + k));
-      const float4 g = a.gain ? __ldg(reinterpret_cast<const float4*>(a.gain + k)) : make_float4(1.f, 1.f, 1.f, 1.f);
-      uint2 p;
-      p.x = pack_bf16x2(v.x * inv * g.x, v.y * inv * g.y);
-      p.y = pack_bf16x2(v.z * inv * g.z, v.w * inv * g.w);
-      *reinterpret_cast<uint2*>(xs + k) = p;
+    for (int k0 = tid * 4; k0 < a.K; k0 += GEMV_XB * STEP) {
+      if (!(one_block && a.gain)) load_block(k0);
+      float4 g[GEMV_XB];
+#pragma unroll
+      for (int u = 0; u < GEMV_XB; ++u) {
+        const int k = k0 + u * STEP;
+        g[u] = (a.gain && active && k < a.K) ? __ldg(reinterpret_cast<const float4*>(a.gain + k))
+                                             : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
+#pragma unroll
+      for (int u = 0; u < GEMV_XB; ++u) {
+        const int k = k0 + u * STEP;
+        if (active && k < a.K) {
+          uint2 p;
+          p.x = pack_bf16x2(v[u].x * inv * g[u].x, v[u].y * inv * g[u].y);
+          p.y = pack_bf16x2(v[u].z * inv * g[u].z, v[u].w * inv * g[u].w);
+          *reinterpret_cast<uint2*>(xs + k) = p;
+        }
+      }
     }
   } else {
-    for (int k = tid * 8; active && k < a.K; k += GEMV_THREADS * 8)
-      *reinterpret_cast<uint4*>(xs + k) = ld_cg16(a.x_bf16 + k);
+    constexpr int STEP8 = GEMV_THREADS * 8;
+    for (int k0 = tid * 8; k0 < a.K; k0 += GEMV_XB * STEP8) {
+      uint4 v[GEMV_XB];
+#pragma unroll
+      for (int u = 0; u < GEMV_XB; ++u) {
+        const int k = k0 + u * STEP8;
+        v[u] = (active && k < a.K) ? ld_cg16(a.x_bf16 + k) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < GEMV_XB; ++u)
+        if (active && k0 + u * STEP8 < a.K) *reinterpret_cast<uint4*>(xs + k0 + u * STEP8) = v[u];
+    }
   }
   sync();
 }
-template <void (*Sync)() = cta_sync>
+template <void (*Sync)() = cta_sync, int XB = 2>
 DS_DEV void gemv_stage_x(const GemvArgs& a, bf16* xs, float* ssq) {
-  gemv_stage_x_t(a, xs, ssq, (int)threadIdx.x, [] { Sync(); });
+  gemv_stage_x_t<XB>(a, xs, ssq, (int)threadIdx.x, [] { Sync(); });
 }
 
 // The 128 accumulating threads' per-row pair sums -> row results (warp
@@ -436,7 +479,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, in
     return;
   }
   pdl_wait();
-  gemv_stage_x<named_sync_consumers>(a, xs, ssq);
+  gemv_stage_x<named_sync_consumers, 8>(a, xs, ssq);
   int slot = 0;
   uint32_t phase = 0;
   unsigned long long best = 0ull;
@@ -756,8 +799,23 @@ static int gemv_batch_launch_t(const GemvArgs& a, const GemvBatch& bt, cudaStrea
   return launch_status(launch_pdl(kern, dim3(grid), dim3(WG * GEMV_THREADS + 32), smem, stream, a, bt, slots));
 }
 
+#ifndef DS_GEMVB_NBW
+#define DS_GEMVB_NBW 2  // rows per consumer warpgroup (experiments: 1, 2, 4)
+#endif
 template <int KS>
 static int gemv_batch_launch_ks(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream) {
+  if (DS_GEMVB_NBW == 1 && bt.nb <= 4) {
+    switch (bt.nb) {
+      case 1: return gemv_batch_launch_t<KS, 1, 1>(a, bt, stream);
+      case 2: return gemv_batch_launch_t<KS, 1, 2>(a, bt, stream);
+      case 3: return gemv_batch_launch_t<KS, 1, 3>(a, bt, stream);
+      default: return gemv_batch_launch_t<KS, 1, 4>(a, bt, stream);
+    }
+  }
+  if (DS_GEMVB_NBW == 4) {
+    if (bt.nb <= 4) return gemv_batch_launch_t<KS, 4, 1>(a, bt, stream);
+    return gemv_batch_launch_t<KS, 4, 2>(a, bt, stream);
+  }
   switch ((bt.nb + 1) / 2) {
     case 1: return gemv_batch_launch_t<KS, 2, 1>(a, bt, stream);
     case 2: return gemv_batch_launch_t<KS, 2, 2>(a, bt, stream);
@@ -774,7 +832,8 @@ int gemv_batch_launch(const GemvArgs& a, const GemvBatch& bt, cudaStream_t strea
   if (bt.nb < 1 || bt.nb > kMaxBatch) return DS_ERR_INVALID;
   if ((a.N % GEMV_ROWS) || (a.K & 7) || (a.mode == EPI_SWIGLU_BF16 && a.N % 32)) return DS_ERR_INVALID;
   if (a.mode == EPI_QKV_ROPE && (a.head_dim % 8 || a.N % a.head_dim)) return DS_ERR_INVALID;
-  const int ks = a.K % 4096 == 0 ? 4096 : (a.K % 2048 == 0 ? 2048 : 1024);
+  static const int ks_max = env_int("DS_GEMVB_KS", 4096);  // slice width (experiments)
+  const int ks = (ks_max >= 4096 && a.K % 4096 == 0) ? 4096 : ((ks_max >= 2048 && a.K % 2048 == 0) ? 2048 : 1024);
   static const int budget = env_int("DS_GEMV_SMEM_KB", 196) * 1024;
   int fit = (budget - 2 * GEMV_ROWS * ks * 2) / (a.K * 2);
   fit = fit > kMaxBatch ? kMaxBatch : fit;

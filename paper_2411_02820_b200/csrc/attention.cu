@@ -55,6 +55,11 @@ DS_DEV float2 exp2_fma2(float2 x) {
 #ifndef DS_FA_EMU_MOD
 #define DS_FA_EMU_MOD 4  // one pair in DS_FA_EMU_MOD on the FMA pipe (0: all on MUFU)
 #endif
+#ifndef DS_FA_DUAL_EMU
+// the dual-softmax kernel: one pair in 8 (in-step A/B at the power cap, 8B shape:
+// 1 in 8 16.29 ms, 1 in 4 16.54, 1 in 2 slower; profiles/r02_fa_dual.txt)
+#define DS_FA_DUAL_EMU 8
+#endif
 
 #ifndef DS_FA_STAMPS
 #define DS_FA_STAMPS 0
@@ -900,6 +905,377 @@ __global__ void __maxnreg__(136)
 #endif
 }
 
+// ----------------------------------------------------------------------
+// Dual-softmax variant: two softmax warps per (Q tile, TMEM lane quarter),
+// each owning 64 of a block's 128 key columns (18 warps).  Measured reason
+// (profiles/r02_fa_stamps_current.txt, r02_pipe_probe.txt): one softmax warp
+// per SM sub-partition and tile runs the 128-column pass latency-bound (~2250
+// cycles per 128x128 block against 1024 cycles of the other tile's MMAs; one
+// warp reaches half the MUFU rate), so the tensor pipe idled ~45% of every
+// period.  Two warps on the same rows halve each warp's chain and keep the MUFU
+// busy.  Per block: pass 1 takes each half's masked row max; the two halves
+// agree on the lazily-moved max (it only moves when a row max exceeds it by
+// more than 2^8) with one barrier-reduction vote per block (bar.red.or over the
+// pair's 64 threads) and exchange their maxima through shared memory only when
+// a row needs the move; pass 2 re-reads S in 16-column pieces, exponentiates and
+// writes bf16 P.  Half h writes P of keys 64h.. over its own consumed S columns
+// 64h.. (the P.V MMA reads its A operand from there), so the halves never touch
+// each other's TMEM columns.  Row sums stay per half and are added (l0 + l1)
+// for the epilogue; O rescales are done by half 0.  At most 80 registers per
+// thread: with 18 warps, 5 share an SM sub-partition with one anchor warp.
+// ----------------------------------------------------------------------
+constexpr int FA_DUAL_THREADS = 18 * 32;
+
+template <int D>
+struct FaDualSmem {
+  using B = FaTcSmem<D>;
+  static constexpr uint32_t XCH = B::BAR + 256;  // float [2 tiles][2 halves][128 rows]
+  static constexpr uint32_t TOTAL = XCH + 2048 + 1024;
+};
+
+DS_DEV bool bar_red_or(int id, int n, bool p) {
+  uint32_t r;
+  asm volatile(
+      "{\n .reg .pred q, o;\n setp.ne.u32 q, %1, 0;\n barrier.cta.red.or.pred o, %2, %3, q;\n selp.u32 %0, 1, 0, o;\n}\n"
+      : "=r"(r)
+      : "r"((uint32_t)p), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+DS_DEV void bar_pair_sync(int id, int n) { asm volatile("barrier.cta.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int D>
+__global__ void __maxnreg__(80)
+    fa_dual_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
+  using L = FaTcSmem<D>;
+  using LD = FaDualSmem<D>;
+  constexpr int CH = L::CH;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 3;
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 7;
+  uint64_t* s_full = bars + 9;
+  uint64_t* p_full = bars + 11;
+  uint64_t* o_done = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  float* xch = reinterpret_cast<float*>(smem + LD::XCH);
+  auto sQ = [&](int i, int c) { return smem + L::Q + (i * CH + c) * L::CHUNK; };
+  auto sK = [&](int st, int c) { return smem + L::K + (st * CH + c) * L::CHUNK; };
+  auto sV = [&](int st, int c) { return smem + L::V + (st * CH + c) * L::CHUNK; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x;
+  const int q0 = (gridDim.y - 1 - blockIdx.y) * 2 * FA_BM;  // heaviest (latest) blocks first
+  const int g = h / (a.n_heads / a.n_kv_heads);
+  auto rowpos = [&](int r) { return a.q_pos ? __ldg(a.q_pos + r) : a.q_pos0 + r; };
+  int n_kv[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int rows = min(FA_BM, a.n_q - (q0 + i * FA_BM));
+    n_kv[i] = rows > 0 ? rowpos(q0 + i * FA_BM + rows - 1) / FA_BN + 1 : 0;
+  }
+  const int J = max(n_kv[0], n_kv[1]);
+  const int max_key = rowpos(min(q0 + 2 * FA_BM, a.n_q) - 1);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int n_tiles = n_kv[1] > 0 ? 2 : 1;
+      mbar_expect_tx(q_full, n_tiles * CH * L::CHUNK);
+      for (int i = 0; i < n_tiles; ++i)
+        for (int c = 0; c < CH; ++c) tma_load_2d(sQ(i, c), &tmQ, q_full, h * D + c * 64, q0 + i * FA_BM);
+      for (int j = 0; j < J; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        int rows[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          int page = 2 * j + p;
+          if (page * 64 > max_key) page = 2 * j;  // beyond the window: duplicate a valid page (finite, masked)
+          const int tp = a.table ? __ldg(a.table + page) : page;
+          rows[p] = (int)(g * a.k_head_rows + (long long)tp * a.k_page_rows);
+        }
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sK(st, c) + p * 64 * 128, &tmK, &k_full[st], c * 64, rows[p]);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sV(st, c) + p * 64 * 128, &tmV, &v_full[st], c * 64, rows[p]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t IDESC_QK = umma_idesc_bf16(FA_BM, FA_BN);
+    constexpr uint32_t IDESC_PV = umma_idesc_bf16_bmn(FA_BM, D);
+    auto qk = [&](int i, int st) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t ad = sdesc_sw128(smem_u32(sQ(i, c)) + k * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(smem_u32(sK(st, c)) + k * 32, 16, 1024);
+          if (elect_one()) umma_bf16(tmem + i * 128, ad, bd, IDESC_QK, (c | k) != 0 ? 1u : 0u);
+        }
+      if (elect_one()) umma_commit(&s_full[i]);
+      __syncwarp();
+    };
+    auto pv = [&](int i, int st, int j) {
+#pragma unroll
+      for (int s = 0; s < FA_BN / 16; ++s) {
+        const uint64_t bd = sdesc_sw128(smem_u32(sV(st, 0)) + s * 2048, L::CHUNK, 1024);
+        // P of keys 16s.. : half 0 (s < 4) at columns 8s, half 1 at 64 + 8(s - 4)
+        const uint32_t pa = tmem + i * 128 + (s < 4 ? s * 8 : 64 + (s - 4) * 8);
+        if (elect_one()) umma_bf16_ts(tmem + 256 + i * 128, pa, bd, IDESC_PV, (j | s) != 0 ? 1u : 0u);
+      }
+      if (elect_one()) umma_commit(&o_done[i]);
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait(&k_full[0], 0);
+    tc_fence_after();
+    if (n_kv[0] > 0) qk(0, 0);
+    if (n_kv[1] > 0) qk(1, 0);
+    if (elect_one()) umma_commit(&k_empty[0]);
+    __syncwarp();
+    for (int j = 0; j < J; ++j) {
+      const int st = j & 1, st1 = (j + 1) & 1;
+      const bool more = j + 1 < J;
+      mbar_wait(&v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (j * FA_BN + FA_BN - 1 > max_key) {
+        // keys past the window end: zero their V rows so p = 0 never meets a
+        // non-finite cache value (a SW128 row's 128 bytes stay within the row)
+        const int first = max_key + 1 - j * FA_BN;
+        for (int c = 0; c < CH; ++c) {
+          const uint32_t base = smem_u32(sV(st, c));
+          for (int off = first * 128 + lane * 16; off < FA_BN * 128; off += 32 * 16)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + off), "r"(0u) : "memory");
+        }
+        fence_async_shared();
+        __syncwarp();
+      }
+      if (j < n_kv[0]) {
+        mbar_wait(&p_full[0], j & 1);
+        if (lane == 0) FA_STAMP(0, j, 2);
+        tc_fence_after();
+        pv(0, st, j);
+      }
+      if (more) {
+        mbar_wait(&k_full[st1], ((j + 1) >> 1) & 1);
+        if (lane == 0) FA_STAMP(0, j, 3);
+        tc_fence_after();
+        if (j + 1 < n_kv[0]) qk(0, st1);
+      }
+      if (j < n_kv[1]) {
+        mbar_wait(&p_full[1], j & 1);
+        if (lane == 0) FA_STAMP(1, j, 2);
+        tc_fence_after();
+        pv(1, st, j);
+      }
+      if (elect_one()) umma_commit(&v_empty[st]);
+      __syncwarp();
+      if (more) {
+        if (j + 1 < n_kv[1]) qk(1, st1);
+        if (elect_one()) umma_commit(&k_empty[st1]);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int i = ((warp - 2) >> 2) & 1;  // Q tile
+    const int hf = (warp - 2) >> 3;       // column half: keys [64 hf, 64 hf + 64) of each block
+    const int quarter = warp & 3;         // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const int pair = 1 + i * 4 + quarter;  // named barrier of the two warps sharing these rows
+    const int first_row = min(q0 + i * FA_BM, a.n_q - 1);
+    const int tile_pos0 = rowpos(first_row);
+    const int qpos = q0 + i * FA_BM + row < a.n_q ? rowpos(q0 + i * FA_BM + row) : max_key;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + i * 128 + hf * 64;  // this half's S (and its P) columns
+    const uint32_t tO = tmem + lane_base + 256 + i * 128;
+    float* xmine = xch + (i * 2 + hf) * 128;
+    float* xother = xch + (i * 2 + (hf ^ 1)) * 128;
+    const float sc = a.scale_log2;
+    const float thr = 8.0f / sc;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv[i]; ++j) {
+      mbar_wait(&s_full[i], j & 1);
+      if (lane == 0 && quarter == 0 && hf == 0) FA_STAMP(i, j, 0);
+      tc_fence_after();
+#if DS_FA_ABLATE
+      if (lane == 0) mbar_arrive(&p_full[i]);
+      l = 1.f;
+      continue;
+#endif
+      const int kbase = j * FA_BN + hf * 64;
+      const bool maskit = j * FA_BN + FA_BN - 1 > tile_pos0;
+      // pass 1: this half's masked row max (two 32-column loads)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        tmem_ld32_nowait(tS + 32 * c, r);
+        tmem_wait_ld();
+        if (maskit) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (kbase + 32 * c + e > qpos) r[e] = __float_as_uint(-INFINITY);
+        }
+        float m4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          m4[q] = fmax3(__uint_as_float(r[q]), __uint_as_float(r[q + 4]), __uint_as_float(r[q + 8]));
+#pragma unroll
+        for (int e = 12; e < 32; e += 8)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) m4[q] = fmax3(m4[q], __uint_as_float(r[e + q]), __uint_as_float(r[e + 4 + q]));
+        mx = fmax3(mx, fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      }
+      // the pair agrees on the (lazily moved) max: one vote; maxima exchanged only when needed
+      float ocorr = 1.f;
+      if (bar_red_or(pair, 64, mx > m_used + thr)) {
+        xmine[row] = mx;
+        bar_pair_sync(pair, 64);
+        const float mo = xother[row];
+        const float mn = fmaxf(mx, mo);
+        if (mn > m_used + thr) {
+          ocorr = fast_exp2((m_used - mn) * sc);  // 0 while m_used is -inf
+          m_used = mn;
+          l *= ocorr;
+        }
+        bar_pair_sync(pair, 64);  // both read before either writes again
+      }
+      if (lane == 0 && quarter == 0 && hf == 0) FA_STAMP(i, j, 4);
+      // pass 2: exponentiate in 16-column pieces (next piece's load in flight), P over consumed S
+      const float msc = m_used * sc;
+      const float2 sc2 = make_float2(sc, sc), nmsc2 = make_float2(-msc, -msc);
+      float2 sum4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+      uint32_t sa[16], sb[16];
+      tmem_ld16_nowait(tS, sa);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t* cur = (c & 1) ? sb : sa;
+        uint32_t* nxt = (c & 1) ? sa : sb;
+        if (c < 3) tmem_ld16_nowait(tS + 16 * (c + 1), nxt);
+        if (maskit) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (kbase + 16 * c + e > qpos) cur[e] = __float_as_uint(-INFINITY);
+        }
+        uint32_t pk[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float2 x =
+              ffma2(make_float2(__uint_as_float(cur[2 * e]), __uint_as_float(cur[2 * e + 1])), sc2, nmsc2);
+          float2 p;
+          if (DS_FA_DUAL_EMU && ((c * 8 + e) % (DS_FA_DUAL_EMU > 0 ? DS_FA_DUAL_EMU : 1)) == DS_FA_DUAL_EMU - 1)
+            p = exp2_fma2(x);
+          else
+            p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+          sum4[e & 3] = fadd2(sum4[e & 3], p);
+          pk[e] = pack_bf16x2(p.x, p.y);
+        }
+        tmem_st8_nowait(tS + 8 * c, pk);  // P keys 16c..16c+15 of this half over S columns 8c.. (consumed)
+        if (c < 3) {
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(nxt[e]));  // values valid only after the wait
+        }
+      }
+      const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+      l += s2.x + s2.y;
+      if (hf == 0 && j > 0 && __any_sync(0xffffffffu, ocorr != 1.f)) {
+        mbar_wait(&o_done[i], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orow[32];
+          tmem_ld32_nowait(tO + c * 32, orow);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * ocorr);
+          tmem_st32_nowait(tO + c * 32, orow);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0 && quarter == 0 && hf == 0) FA_STAMP(i, j, 1);
+      if (lane == 0) mbar_arrive(&p_full[i]);
+    }
+    if (n_kv[i] > 0) {
+      // l = l(half 0) + l(half 1), the same sum in both warps
+      xmine[row] = l;
+      bar_pair_sync(pair, 64);
+      const float lt = hf == 0 ? l + xother[row] : xother[row] + l;
+      mbar_wait(&o_done[i], (n_kv[i] - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / lt;
+      const int qrow = q0 + i * FA_BM + row;
+      bf16* dst = a.o + (long long)qrow * a.ldo + (long long)h * D;
+#pragma unroll 1
+      for (int c = hf * (D / 64); c < (hf + 1) * (D / 64); ++c) {
+        uint32_t orow[32];
+        tmem_ld32_nowait(tO + c * 32, orow);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pk[e] = pack_bf16x2(__uint_as_float(orow[2 * e]) * inv, __uint_as_float(orow[2 * e + 1]) * inv);
+        if (qrow < a.n_q) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) st_global_v4(dst + c * 32 + e * 8, pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+#if DS_FA_STAMPS
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const long long t0 = fa_stamps[0][0][0];
+    for (int j = 0; j < min(J, 64); ++j)
+      printf("FA j=%2d  S0 %7lld max0 %7lld P0 %7lld mmaP0 %7lld K %7lld | S1 %7lld max1 %7lld P1 %7lld mmaP1 %7lld\n", j,
+             fa_stamps[0][j][0] - t0, fa_stamps[0][j][4] - t0, fa_stamps[0][j][1] - t0, fa_stamps[0][j][2] - t0,
+             fa_stamps[0][j][3] - t0, fa_stamps[1][j][0] - t0, fa_stamps[1][j][4] - t0, fa_stamps[1][j][1] - t0,
+             fa_stamps[1][j][2] - t0);
+  }
+#endif
+}
+
 template <int D>
 static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer, long long head_stride,
                         long long page_stride, long long layer_rows, const int32_t* table, int n_q, int q_pos0,
@@ -912,15 +1288,23 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
     return launch_status(cudaErrorInvalidValue);
   FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, q_pos, head_stride / D, page_stride / D, table, o, ldo,
              (float)(1.4426950408889634 / sqrt((double)D))};
-  // DS_FA_VARIANT: 0 whole-tile softmax (round 1), 1 whole-tile chunked (default), 2 split halves
+  // DS_FA_VARIANT: 0 whole-tile softmax (round 1), 1 whole-tile chunked, 2 split halves,
+  // 3 dual softmax warps per row (default)
   static const int variant = [] {
     const char* e = getenv("DS_FA_VARIANT");
-    return e ? atoi(e) : 1;
+    const int v = e ? atoi(e) : 3;
+    return v < 0 || v > 3 ? 3 : v;
   }();
-  auto kern = variant == 0 ? fa_tc_kernel<D, false> : variant == 1 ? fa_tc_kernel<D, true> : fa_split_kernel<D>;
-  static PerDevice attr[3];
-  if (int rc_ = launch_status(ensure_smem_attr(kern, L::TOTAL, attr[variant < 0 || variant > 2 ? 2 : variant]))) return rc_;
   dim3 grid(n_heads, (n_q + 2 * FA_BM - 1) / (2 * FA_BM));
+  static PerDevice attr[4];
+  if (variant == 3) {
+    using LD = FaDualSmem<D>;
+    if (int rc_ = launch_status(ensure_smem_attr(fa_dual_kernel<D>, LD::TOTAL, attr[3]))) return rc_;
+    count_launch();
+    return launch_status(launch_pdl(fa_dual_kernel<D>, grid, dim3(FA_DUAL_THREADS), LD::TOTAL, stream, tq, tk, tv, a));
+  }
+  auto kern = variant == 0 ? fa_tc_kernel<D, false> : variant == 1 ? fa_tc_kernel<D, true> : fa_split_kernel<D>;
+  if (int rc_ = launch_status(ensure_smem_attr(kern, L::TOTAL, attr[variant]))) return rc_;
   count_launch();
   return launch_status(launch_pdl(kern, grid, dim3(FA_THREADS), L::TOTAL, stream, tq, tk, tv, a));
 }

@@ -25,6 +25,7 @@ ap.add_argument("--n", type=int, default=8192)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--swiglu", action="store_true")
+ap.add_argument("--batch", type=int, default=0, help="rows of a batched pass (ds_anchor_batch), 0 = ds_anchor")
 args = ap.parse_args()
 cfg = P.ModelConfig(32, 4096, 32, 8, 128, 14336, 128256, max(args.n, 8192), 0,
                     mlp_kind="swiglu" if args.swiglu else "ungated")
@@ -47,6 +48,25 @@ def run():
                           ws.data_ptr(), ws.numel(), s.cuda_stream))
 
 
+if args.batch:
+    nb = args.batch
+    caches = [cache] + [P.PagedKV.allocate(cfg, n, zero=False) for _ in range(nb - 1)]
+    for c in caches[1:]:
+        c.k.normal_()
+        c.v.normal_()
+    descs = (L.KvCache * nb)(*[c.desc() for c in caches])
+    pos = (C.c_int32 * nb)(*([n - 1] * nb))
+    ids = tok[-nb:].clone()
+    lgb = torch.empty(nb, cfg.vocab_size, device="cuda")
+    tb = torch.empty(nb, dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(s):
+        wsb = torch.empty(P.engine.batch_workspace_bytes(cfg, n, nb), dtype=torch.uint8, device="cuda")
+
+    def run():  # noqa: F811
+        L.check(lib.ds_anchor_batch(C.byref(bdesc), nb, ids.data_ptr(), pos, descs, lgb.data_ptr(), tb.data_ptr(),
+                                    wsb.data_ptr(), wsb.numel(), s.cuda_stream))
+
+
 with torch.cuda.stream(s):
     for _ in range(5):
         run()
@@ -63,7 +83,8 @@ if args.profile:
 lw = B.layers[0]
 w_bytes = sum(t.numel() * t.element_size() for t in (lw["wqkv"], lw["wo"], lw["w1"], lw["w2"]))
 kv_bytes = 2 * cfg.n_kv_heads * cfg.head_dim * n * 2
-total = cfg.n_layers * (w_bytes + kv_bytes) + cfg.vocab_size * cfg.d_model * 2
+nrows = max(1, args.batch)
+total = cfg.n_layers * (w_bytes + nrows * kv_bytes) + cfg.vocab_size * cfg.d_model * 2
 ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.reps)]
 with torch.cuda.stream(s):
     for a, b in ev:
@@ -81,6 +102,6 @@ cap = 256
 tm, tg = (C.c_float * cap)(), (C.c_int32 * cap)()
 m = lib.ds_trace_end(tm, tg, cap)
 marks = [(int(tg[i]), float(tm[i])) for i in range(max(m, 0))]
-out = {"n": n, "ms_median": med, "ms_min": ms[0], "gbs": total / med / 1e6, "bytes": total,
+out = {"n": n, "rows": nrows, "ms_median": med, "ms_min": ms[0], "gbs": total / med / 1e6, "bytes": total,
        "per_layer_bytes": w_bytes + kv_bytes, "trace": marks}
 print(json.dumps(out))
