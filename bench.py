@@ -819,11 +819,21 @@ def run_fanout(args, world, rank, local):
             remote = remotes[0]
             caches = [cache] + [P.PagedKV.allocate(cfg, n, dev) for _ in range(nb - 1)]
 
-            def step():
-                for b in range(nb):  # the consumer's batch of requests, back to back in one graph
-                    r_ = P.partial_prefill(B, batch_ids[b], rc, remotes[b].kv, remotes[b].e_map, out=caches[b],
-                                           stream=stream, copy_stream=side, tokens_dev=batch_tok[b])
-                return r_
+            if nb == 1:
+                def step():
+                    return P.partial_prefill(B, ids, rc, remote.kv, remote.e_map, out=cache, stream=stream,
+                                             copy_stream=side, tokens_dev=tok_dev)
+            else:
+                # config 4: the consumer's batch of requests (each its own context and export) in one
+                # batched call: recompute per request, every request's KV pulled beside it, one
+                # batched anchor pass (one weight stream per layer for all rows)
+                with torch.cuda.stream(stream):
+                    ws_b = torch.empty(P.engine.batch_workspace_bytes(cfg, n, nb), dtype=torch.uint8, device=dev)
+
+                def step():
+                    return P.partial_prefill_batch(B, batch_ids, rc, [r_.kv for r_ in remotes],
+                                                   [r_.e_map for r_ in remotes], out=caches, stream=stream,
+                                                   copy_stream=side, tokens_dev=batch_tok, workspace=ws_b)[0]
         else:
             pipe = ConsumerPipeline(B, transport=NcclTransport(0, cfg, n, dev))
             step = lambda: pipe.run(ids, rc, None, None, out=cache, tokens_dev=tok_dev)  # noqa

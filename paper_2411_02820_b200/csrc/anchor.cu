@@ -658,6 +658,85 @@ DS_HOST_DEV_INLINE GemvArgs gemv_row_view(const GemvArgs& a, const GemvBatch& bt
 // slower than one row).  Registers: every CTA must fit beside one
 // persistent-anchor warp (2.8 K registers) per SM sub-partition, which holds
 // WG + 1 of this kernel's warps.
+// Rows per epilogue thread group: QKV / SwiGLU pair two accumulators per output.
+DS_DEV int gemv_epi_per(int mode) { return (mode == EPI_QKV_ROPE || mode == EPI_SWIGLU_BF16) ? 4 : GEMV_ROWS; }
+
+// gemv_finish for the nbw rows of a warpgroup with two barriers in all (one
+// gemv_finish per row takes three): the same shuffles, the same warp order of
+// the cross-warp sum and the same epilogue arithmetic per row, so the same
+// bits.  Epilogue thread tid < per * nbw handles row tid / per, slot tid % per
+// (its `pre` loaded for that slot); argmax maxima stay with that thread.
+template <int NBW, typename Sync>
+DS_DEV void gemv_finish_rows(const GemvArgs& a, const GemvBatch& bt, int b0, int nbw, int t,
+                             const float2 (*s2)[GEMV_ROWS], float (*red)[NBW * GEMV_ROWS], unsigned long long& best,
+                             const EpiPre& pre, Sync sync, int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int i = 0; i < NBW; ++i) {
+    if (i < nbw) {
+      float sr[GEMV_ROWS];
+#pragma unroll
+      for (int r = 0; r < GEMV_ROWS; ++r) sr[r] = s2[i][r].x + s2[i][r].y;
+#pragma unroll
+      for (int r = 0; r < GEMV_ROWS; ++r) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sr[r] += __shfl_xor_sync(0xffffffffu, sr[r], o);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < GEMV_ROWS; ++r) red[warp][i * GEMV_ROWS + r] = sr[r];
+      }
+    }
+  }
+  sync();
+  if (tid < GEMV_ROWS * nbw) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < GEMV_WARPS; ++w) v += red[w][tid];
+    red[0][tid] = v;  // only thread tid touches column tid
+  }
+  sync();
+  const int per = gemv_epi_per(a.mode);
+  if (tid < per * nbw) {
+    const int i = tid / per, r = tid - i * per;
+    const GemvArgs v = gemv_row_view(a, bt, b0 + i);
+    const float* rv = red[0] + i * GEMV_ROWS;
+    if (a.mode == EPI_QKV_ROPE) {
+      const int r0 = gemv_row(v, t, r);
+      const int head = r0 / v.head_dim, j = r0 - head * v.head_dim, half = v.head_dim >> 1;
+      float lo = rv[r], hi = rv[r + 4];
+      const bool is_q = head < v.n_heads, is_k = !is_q && head < v.n_heads + v.n_kv_heads;
+      if (is_q || is_k) {
+        const float cs = pre.a, sn = pre.b;
+        const float x1 = lo, x2 = hi;
+        lo = __fsub_rn(__fmul_rn(x1, cs), __fmul_rn(x2, sn));
+        hi = __fadd_rn(__fmul_rn(x1, sn), __fmul_rn(x2, cs));
+      }
+      bf16* dst = is_q ? v.q_out + (long long)head * v.head_dim
+                       : (is_k ? v.kv.k + v.kv.off(head - v.n_heads, v.pos)
+                               : v.kv.v + v.kv.off(head - v.n_heads - v.n_kv_heads, v.pos));
+      dst[j] = __float2bfloat16_rn(lo);
+      dst[j + half] = __float2bfloat16_rn(hi);
+    } else if (a.mode == EPI_SWIGLU_BF16) {
+      const int o = (t >> 2) * 16 + (t & 3) * 4 + r;
+      v.out_bf16[o] = __float2bfloat16_rn(silu(rv[r]) * rv[r + 4]);
+    } else {
+      const int row = t * GEMV_ROWS + r;
+      const float x = rv[r];
+      if (a.mode == EPI_RESID_F32) {
+        v.out_f32[row] = pre.a + x;
+      } else if (a.mode == EPI_SILU_BF16) {
+        v.out_bf16[row] = __float2bfloat16_rn(silu(x));
+      } else {
+        v.out_f32[row] = x;
+        const unsigned long long pk = pack_argmax(x, row);
+        best = pk > best ? pk : best;
+      }
+    }
+  }
+  sync();  // red[] reused by the next tile
+}
+
 template <int KS, int NBW, int WG>
 __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80)))
     gemv_batch_kernel(const __grid_constant__ GemvArgs a, const __grid_constant__ GemvBatch bt, int slots) {
@@ -668,7 +747,7 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
   uint8_t* ring = smem_dyn;
   bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * SLOT);  // [nb][K]
   __shared__ __align__(8) uint64_t full[16], empty[16];
-  __shared__ float red[WG][GEMV_WARPS][GEMV_ROWS];
+  __shared__ float red[WG][GEMV_WARPS][NBW * GEMV_ROWS];
   __shared__ float ssq[WG][GEMV_WARPS];
   const int tid = threadIdx.x;
   const int tiles = a.N / GEMV_ROWS, ks = a.K / KS;
@@ -712,13 +791,12 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
   }
   int slot = 0;
   uint32_t phase = 0;
-  unsigned long long best[NBW];
-#pragma unroll
-  for (int i = 0; i < NBW; ++i) best[i] = 0ull;
+  unsigned long long best = 0ull;
+  const int per = gemv_epi_per(a.mode);
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    EpiPre pre[NBW];
-#pragma unroll
-    for (int i = 0; i < NBW; ++i) pre[i] = i < nbw ? gemv_epi_pre(gemv_row_view(a, bt, b0 + i), tile, t) : EpiPre{0.f, 0.f};
+    // the epilogue inputs of the (row, slot) this thread finishes, loaded at tile start
+    const EpiPre pre = t < per * nbw ? gemv_epi_pre(gemv_row_view(a, bt, b0 + t / per), tile, t % per)
+                                     : EpiPre{0.f, 0.f};
     float2 s2[NBW][GEMV_ROWS];
 #pragma unroll
     for (int i = 0; i < NBW; ++i)
@@ -763,21 +841,16 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
         phase ^= 1;
       }
     }
-#pragma unroll
-    for (int i = 0; i < NBW; ++i)
-      if (i < nbw) gemv_finish(gemv_row_view(a, bt, b0 + i), tile, s2[i], red[wg], best[i], pre[i], sync, t);
+    gemv_finish_rows<NBW>(a, bt, b0, nbw, tile, s2, red[wg], best, pre, sync, t);
   }
-  if (a.mode == EPI_STORE_F32 && a.argmax && t < GEMV_ROWS) {
+  if (a.mode == EPI_STORE_F32 && a.argmax && t < 32) {
+    // row i's maxima sit with threads 8i..8i+7 (warp 0 of the warpgroup)
 #pragma unroll
-    for (int i = 0; i < NBW; ++i) {
-      unsigned long long bb = best[i];
-#pragma unroll
-      for (int o = 4; o; o >>= 1) {
-        const unsigned long long other = __shfl_xor_sync(0x000000ffu, bb, o);
-        bb = other > bb ? other : bb;
-      }
-      if (t == 0 && i < nbw && bb) atomicMax(a.argmax + b0 + i, bb);
+    for (int o = 4; o; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other > best ? other : best;
     }
+    if ((t & 7) == 0 && t < GEMV_ROWS * nbw && best) atomicMax(a.argmax + b0 + t / GEMV_ROWS, best);
   }
 }
 

@@ -333,6 +333,7 @@ def batch_workspace_bytes(config: ModelConfig, max_tokens: int, batch: int) -> i
 def partial_prefill_batch(receiver: ModelWeights, tokens: Sequence, config: RecomputeConfig,
                           sender_kv: Sequence[LayerKV | None], sender_e: Sequence | None = None, *,
                           out: Sequence[PagedKV] | None = None, stream=None, copy_stream=None,
+                          tokens_dev: Sequence[torch.Tensor] | None = None,
                           workspace: torch.Tensor | None = None) -> list[MixedPrefill]:
     """A consumer's batch of requests (BASELINE config 4): ``len(tokens)`` <= 8
     partial prefills with one recompute config, each request its own prefix
@@ -342,13 +343,15 @@ def partial_prefill_batch(receiver: ModelWeights, tokens: Sequence, config: Reco
     recompute runs request after request on ``stream`` while ``copy_stream``
     ingests every request's reused layers; then ONE batched anchor pass streams
     each layer's weights once for all rows.  Results equal the requests'
-    one-by-one :func:`partial_prefill` results bit for bit."""
+    one-by-one :func:`partial_prefill` results bit for bit.  ``tokens_dev``:
+    optional device copies of the requests' ids (int64, as in
+    :func:`partial_prefill`; required under CUDA-graph capture)."""
     cfg = receiver.config
     nb = len(tokens)
     if not 1 <= nb <= MAX_BATCH:
         raise ValueError(f"batch of {nb} requests outside [1, {MAX_BATCH}]")
-    if len(sender_kv) != nb or (sender_e is not None and len(sender_e) != nb) or (out is not None and len(out) != nb):
-        raise ValueError("tokens, sender_kv, sender_e and out must have one entry per request")
+    if len(sender_kv) != nb or any(x is not None and len(x) != nb for x in (sender_e, out, tokens_dev)):
+        raise ValueError("tokens, sender_kv, sender_e, out and tokens_dev must have one entry per request")
     ids = []
     for t in tokens:
         ids.append(check_tokens(t, cfg))
@@ -371,6 +374,7 @@ def partial_prefill_batch(receiver: ModelWeights, tokens: Sequence, config: Reco
     groups = [x for g in config.groups for x in g]
     ga = (C.c_int32 * max(1, len(groups)))(*groups)
     th = (C.c_void_p * nb)(*[x.ctypes.data for x in ids])
+    td = (C.c_void_p * nb)(*[t.data_ptr() for t in tokens_dev]) if tokens_dev is not None else None
     nt = (C.c_int32 * nb)(*ns)
     empty = L.KvCache()
     skv = (L.KvCache * nb)(*[kv.desc() if kv is not None else empty for kv in sender_kv])
@@ -382,7 +386,7 @@ def partial_prefill_batch(receiver: ModelWeights, tokens: Sequence, config: Reco
     bad, ml, mk = C.c_int32(-1), C.c_int32(-1), C.c_int32(0)
     with torch.cuda.device(receiver.device):
         rc = L.lib().ds_partial_prefill_batch(
-            C.byref(receiver.desc()), nb, th, None, nt, ga, len(config.groups), skv, ep, ne, odesc,
+            C.byref(receiver.desc()), nb, th, td, nt, ga, len(config.groups), skv, ep, ne, odesc,
             logits.data_ptr(), tok.data_ptr(), workspace.data_ptr(), workspace.numel(), s.cuda_stream,
             copy_stream.cuda_stream if copy_stream is not None else None, C.byref(bad), C.byref(ml), C.byref(mk))
     L.check(rc, ml.value, mk.value)
