@@ -324,7 +324,7 @@ bool sender_is_remote(const void* p) {
 // another stream); the QKV GEMV before it does not depend on it.
 // DS_ABLATE_ANCHOR=<mask>: timing ablation of the per-launch anchor kernels
 // (1 qkv, 2 attention, 4 o-proj, 8 w1, 16 w2 skipped).  The results are wrong
-// under it; tools/ab_anchor.sh uses it to price each kernel inside the chain.
+// under it; tools/anchor_alone.py under it prices each kernel inside the chain.
 static int ablate_anchor() {
   static int v = -1;
   if (v < 0) {

@@ -10,7 +10,7 @@ timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
     --log-file $OUT/launches_partial.csv python tools/profile_step.py --what partial > $OUT/ncu_launch.log 2>&1
 NCU="ncu --profile-from-start off --set full --clock-control none --import-source on"
 timeout 900 $NCU -k regex:gemm_tc2 -c 4 -o $OUT/prof_gemm python tools/profile_step.py --what partial > $OUT/ncu_gemm.log 2>&1
-timeout 600 $NCU -k regex:fa_tc -c 1 -o $OUT/prof_fa python tools/profile_step.py --what partial > $OUT/ncu_fa.log 2>&1
+timeout 600 $NCU -k regex:"fa_(tc|dual)" -c 1 -o $OUT/prof_fa python tools/profile_step.py --what partial > $OUT/ncu_fa.log 2>&1
 timeout 600 $NCU -k regex:anchor_persistent -c 1 -o $OUT/prof_anchor python tools/profile_step.py --what partial > $OUT/ncu_anchor.log 2>&1
 ls -la $OUT
 # the stand-alone anchor kernels (single stream): TMA-staged GEMV and split-KV attention
