@@ -1015,18 +1015,34 @@ DS_DEV void attn_prefetch(const AttnArgs& a, int item, int D) {
 // Softmax of each head over the item's nk scores (log2 domain, in place):
 // stat = (max, sum) per head.
 template <int R>
+// Four of a lane's elements per step (independent loads and exponentials in
+// flight); the max is order-free and l still adds the lane's elements in
+// ascending order, so the result is the one-element loop's bit for bit.
 DS_DEV void attn_softmax(int nk, int sk, float* sc, float* stat) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = warp; r < R; r += ATT_THREADS / 32) {
-    float m = -INFINITY;
-    for (int i = lane; i < nk; i += 32) m = fmaxf(m, sc[r * sk + i]);
+    float* row = sc + r * sk;
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int i = lane; i < nk; i += 128) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + 32 * u < nk) m4[u] = fmaxf(m4[u], row[i + 32 * u]);
+    }
+    float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     float l = 0.f;
-    for (int i = lane; i < nk; i += 32) {
-      const float e = exp2f(sc[r * sk + i] - m);
-      sc[r * sk + i] = e;
-      l += e;
+    for (int i = lane; i < nk; i += 128) {
+      float e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) e[u] = i + 32 * u < nk ? exp2f(row[i + 32 * u] - m) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + 32 * u < nk) {
+          row[i + 32 * u] = e[u];
+          l += e[u];
+        }
+      }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);

@@ -55,6 +55,9 @@ DS_DEV float2 exp2_fma2(float2 x) {
 #ifndef DS_FA_EMU_MOD
 #define DS_FA_EMU_MOD 4  // one pair in DS_FA_EMU_MOD on the FMA pipe (0: all on MUFU)
 #endif
+#ifndef DS_FA_PASS1_BOTH
+#define DS_FA_PASS1_BOTH 0  // dual FA: issue both pass-1 TMEM loads before the first wait (experiment)
+#endif
 #ifndef DS_FA_DUAL_EMU
 // the dual-softmax kernel: one pair in 8 (in-step A/B at the power cap, 8B shape:
 // 1 in 8 16.29 ms, 1 in 4 16.54, 1 in 2 slower; profiles/r02_fa_dual.txt)
@@ -106,6 +109,8 @@ struct FaTcArgs {
   bf16* o;
   long long ldo;
   float scale_log2;
+  const bf16* q;  // [n_q][ldq] (the one-tile kernel stages Q rows into TMEM itself)
+  long long ldq;
 };
 
 // At most 136 registers per thread: 3 FA warps of an SM sub-partition then
@@ -1137,13 +1142,23 @@ __global__ void __maxnreg__(80)
 #endif
       const int kbase = j * FA_BN + hf * 64;
       const bool maskit = j * FA_BN + FA_BN - 1 > tile_pos0;
-      // pass 1: this half's masked row max (two 32-column loads)
+      // pass 1: this half's masked row max (both 32-column loads in flight)
       float mx = -INFINITY;
+#if DS_FA_PASS1_BOTH
+      uint32_t rr[2][32];
+      tmem_ld32_nowait(tS, rr[0]);
+      tmem_ld32_nowait(tS + 32, rr[1]);
+      tmem_wait_ld();
+#endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
+#if DS_FA_PASS1_BOTH
+        uint32_t* r = rr[c];
+#else
         uint32_t r[32];
         tmem_ld32_nowait(tS + 32 * c, r);
         tmem_wait_ld();
+#endif
         if (maskit) {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
@@ -1276,6 +1291,333 @@ __global__ void __maxnreg__(80)
 #endif
 }
 
+// ----------------------------------------------------------------------
+// One-tile variant (DS_FA_VARIANT=4): CTA = one head x ONE 128-row Q tile, Q
+// held in TMEM (the QK MMA reads it as the A operand, like P for P.V: only K
+// comes from shared memory), S double-buffered in TMEM (S0 | S1 | O | Q = 448
+// columns), so QK of block j+1 runs while the softmax of block j does: the
+// softmax no longer waits for its own tile's P.V + QK.  Softmax: the dual
+// scheme of fa_dual_kernel (two warps per lane quarter, 64 key columns each).
+// 3-stage K/V ring (192 KB).  Costs: K/V tiles are loaded once per Q tile
+// instead of once per two (2x the L2->SM traffic).
+// ----------------------------------------------------------------------
+constexpr int FA_ONE_THREADS = 10 * 32;
+constexpr int FA_ONE_STAGES = 3;
+
+template <int D>
+struct FaOneSmem {
+  static constexpr int CH = D / 64;
+  static constexpr uint32_t CHUNK = FA_BN * 64 * 2;  // [128 keys][64] bf16, SW128
+  static constexpr uint32_t K = 0;
+  static constexpr uint32_t V = K + FA_ONE_STAGES * CH * CHUNK;
+  static constexpr uint32_t BAR = V + FA_ONE_STAGES * CH * CHUNK;
+  static constexpr uint32_t XCH = BAR + 256;  // float [2 halves][128 rows]
+  static constexpr uint32_t TOTAL = XCH + 1024 + 1024;
+};
+
+template <int D>
+__global__ void __maxnreg__(136)
+    fa_one_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
+  using L = FaOneSmem<D>;
+  constexpr int CH = L::CH;
+  constexpr int NS = FA_ONE_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* k_full = bars;            // [NS]
+  uint64_t* k_empty = bars + NS;      // [NS]
+  uint64_t* v_full = bars + 2 * NS;   // [NS]
+  uint64_t* v_empty = bars + 3 * NS;  // [NS]
+  uint64_t* q_ready = bars + 4 * NS;
+  uint64_t* s_full = q_ready + 1;     // [2] per S buffer
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* o_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  float* xch = reinterpret_cast<float*>(smem + L::XCH);
+  auto sK = [&](int st, int c) { return smem + L::K + (st * CH + c) * L::CHUNK; };
+  auto sV = [&](int st, int c) { return smem + L::V + (st * CH + c) * L::CHUNK; };
+  constexpr uint32_t TS_O = 256, TS_Q = 384;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x;
+  const int q0 = (gridDim.y - 1 - blockIdx.y) * FA_BM;  // heaviest (latest) tiles first
+  const int g = h / (a.n_heads / a.n_kv_heads);
+  auto rowpos = [&](int r) { return a.q_pos ? __ldg(a.q_pos + r) : a.q_pos0 + r; };
+  const int rows = min(FA_BM, a.n_q - q0);
+  const int max_key = rowpos(q0 + rows - 1);
+  const int J = max_key / FA_BN + 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    mbar_init(q_ready, 8);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+    }
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 0; j < J; ++j) {
+        const int st = j % NS;
+        const uint32_t ph = (j / NS) & 1;
+        int krow[2];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          int page = 2 * j + p;
+          if (page * 64 > max_key) page = 2 * j;  // beyond the window: duplicate a valid page (finite, masked)
+          const int tp = a.table ? __ldg(a.table + page) : page;
+          krow[p] = (int)(g * a.k_head_rows + (long long)tp * a.k_page_rows);
+        }
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sK(st, c) + p * 64 * 128, &tmK, &k_full[st], c * 64, krow[p]);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], CH * L::CHUNK);
+        for (int p = 0; p < 2; ++p)
+          for (int c = 0; c < CH; ++c) tma_load_2d(sV(st, c) + p * 64 * 128, &tmV, &v_full[st], c * 64, krow[p]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t IDESC_QK = umma_idesc_bf16(FA_BM, FA_BN);
+    constexpr uint32_t IDESC_PV = umma_idesc_bf16_bmn(FA_BM, D);
+    auto qk = [&](int j) {  // S[j & 1] = Q K_j^T, Q from TMEM (A), K from shared memory (B)
+      const int st = j % NS;
+      mbar_wait(&k_full[st], (j / NS) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int s = 0; s < D / 16; ++s) {
+        const uint64_t bd = sdesc_sw128(smem_u32(sK(st, s / 4)) + (s % 4) * 32, 16, 1024);
+        if (elect_one()) umma_bf16_ts(tmem + (j & 1) * 128, tmem + TS_Q + s * 8, bd, IDESC_QK, s != 0 ? 1u : 0u);
+      }
+      if (elect_one()) {
+        umma_commit(&s_full[j & 1]);
+        umma_commit(&k_empty[st]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_ready, 0);
+    tc_fence_after();
+    qk(0);
+    if (J > 1) qk(1);
+    for (int j = 0; j < J; ++j) {
+      const int st = j % NS;
+      mbar_wait(&v_full[st], (j / NS) & 1);
+      tc_fence_after();
+      if (j * FA_BN + FA_BN - 1 > max_key) {
+        // keys past the window end: zero their V rows so p = 0 never meets a non-finite cache value
+        const int first = max_key + 1 - j * FA_BN;
+        for (int c = 0; c < CH; ++c) {
+          const uint32_t base = smem_u32(sV(st, c));
+          for (int off = first * 128 + lane * 16; off < FA_BN * 128; off += 32 * 16)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(base + off), "r"(0u) : "memory");
+        }
+        fence_async_shared();
+        __syncwarp();
+      }
+      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      if (lane == 0) FA_STAMP(0, j, 2);
+      tc_fence_after();
+#pragma unroll
+      for (int s = 0; s < FA_BN / 16; ++s) {
+        const uint64_t bd = sdesc_sw128(smem_u32(sV(st, 0)) + s * 2048, L::CHUNK, 1024);
+        const uint32_t pa = tmem + (j & 1) * 128 + (s < 4 ? s * 8 : 64 + (s - 4) * 8);
+        if (elect_one()) umma_bf16_ts(tmem + TS_O, pa, bd, IDESC_PV, (j | s) != 0 ? 1u : 0u);
+      }
+      if (elect_one()) {
+        umma_commit(o_done);
+        umma_commit(&v_empty[st]);
+      }
+      __syncwarp();
+      if (j + 2 < J) qk(j + 2);  // into S[j & 1], after P.V(j) read P there (in-order tensor pipe)
+    }
+  } else {
+    const int hf = (warp - 2) >> 2;  // column half: keys [64 hf, 64 hf + 64) of each block
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int pair = 1 + quarter;
+    const int tile_pos0 = rowpos(q0);
+    const int qpos = row < rows ? rowpos(q0 + row) : max_key;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tO = tmem + lane_base + TS_O;
+    float* xmine = xch + hf * 128;
+    float* xother = xch + (hf ^ 1) * 128;
+    {  // Q row slice -> TMEM (A operand of QK: packed bf16 pairs, 8 columns per 16 dims)
+      constexpr int QC = D / 4;  // packed columns per half
+      uint32_t qr[QC];
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + (long long)(q0 + row) * a.ldq + (long long)h * D + hf * (D / 2));
+#pragma unroll
+      for (int c = 0; c < QC / 4; ++c) {
+        const uint4 v = row < rows ? __ldg(src + c) : make_uint4(0u, 0u, 0u, 0u);
+        qr[4 * c] = v.x;
+        qr[4 * c + 1] = v.y;
+        qr[4 * c + 2] = v.z;
+        qr[4 * c + 3] = v.w;
+      }
+      if constexpr (QC == 32) tmem_st32_nowait(tmem + lane_base + TS_Q + hf * QC, qr);
+      else tmem_st16_nowait(tmem + lane_base + TS_Q + hf * QC, qr);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_ready);
+    }
+    const float sc = a.scale_log2;
+    const float thr = 8.0f / sc;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < J; ++j) {
+      const uint32_t tS = tmem + lane_base + (j & 1) * 128 + hf * 64;
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      if (lane == 0 && quarter == 0 && hf == 0) FA_STAMP(0, j, 0);
+      tc_fence_after();
+      const int kbase = j * FA_BN + hf * 64;
+      const bool maskit = j * FA_BN + FA_BN - 1 > tile_pos0;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        tmem_ld32_nowait(tS + 32 * c, r);
+        tmem_wait_ld();
+        if (maskit) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (kbase + 32 * c + e > qpos) r[e] = __float_as_uint(-INFINITY);
+        }
+        float m4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          m4[q] = fmax3(__uint_as_float(r[q]), __uint_as_float(r[q + 4]), __uint_as_float(r[q + 8]));
+#pragma unroll
+        for (int e = 12; e < 32; e += 8)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) m4[q] = fmax3(m4[q], __uint_as_float(r[e + q]), __uint_as_float(r[e + 4 + q]));
+        mx = fmax3(mx, fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      }
+      float ocorr = 1.f;
+      if (bar_red_or(pair, 64, mx > m_used + thr)) {
+        xmine[row] = mx;
+        bar_pair_sync(pair, 64);
+        const float mo = xother[row];
+        const float mn = fmaxf(mx, mo);
+        if (mn > m_used + thr) {
+          ocorr = fast_exp2((m_used - mn) * sc);  // 0 while m_used is -inf
+          m_used = mn;
+          l *= ocorr;
+        }
+        bar_pair_sync(pair, 64);
+      }
+      const float msc = m_used * sc;
+      const float2 sc2 = make_float2(sc, sc), nmsc2 = make_float2(-msc, -msc);
+      float2 sum4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+      uint32_t sa[16], sb[16];
+      tmem_ld16_nowait(tS, sa);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t* cur = (c & 1) ? sb : sa;
+        uint32_t* nxt = (c & 1) ? sa : sb;
+        if (c < 3) tmem_ld16_nowait(tS + 16 * (c + 1), nxt);
+        if (maskit) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (kbase + 16 * c + e > qpos) cur[e] = __float_as_uint(-INFINITY);
+        }
+        uint32_t pk[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float2 x =
+              ffma2(make_float2(__uint_as_float(cur[2 * e]), __uint_as_float(cur[2 * e + 1])), sc2, nmsc2);
+          float2 p;
+          if (DS_FA_DUAL_EMU && ((c * 8 + e) % (DS_FA_DUAL_EMU > 0 ? DS_FA_DUAL_EMU : 1)) == DS_FA_DUAL_EMU - 1)
+            p = exp2_fma2(x);
+          else
+            p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+          sum4[e & 3] = fadd2(sum4[e & 3], p);
+          pk[e] = pack_bf16x2(p.x, p.y);
+        }
+        tmem_st8_nowait(tS + 8 * c, pk);
+        if (c < 3) {
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(nxt[e]));
+        }
+      }
+      const float2 s2 = fadd2(fadd2(sum4[0], sum4[1]), fadd2(sum4[2], sum4[3]));
+      l += s2.x + s2.y;
+      if (hf == 0 && j > 0 && __any_sync(0xffffffffu, ocorr != 1.f)) {
+        mbar_wait(o_done, (j - 1) & 1);  // P.V(j-1) complete
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orow[32];
+          tmem_ld32_nowait(tO + c * 32, orow);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * ocorr);
+          tmem_st32_nowait(tO + c * 32, orow);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0 && quarter == 0 && hf == 0) FA_STAMP(0, j, 1);
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    xmine[row] = l;
+    bar_pair_sync(pair, 64);
+    const float lt = hf == 0 ? l + xother[row] : xother[row] + l;
+    mbar_wait(o_done, (J - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / lt;
+    const int qrow = q0 + row;
+    bf16* dst = a.o + (long long)qrow * a.ldo + (long long)h * D;
+#pragma unroll 1
+    for (int c = hf * (D / 64); c < (hf + 1) * (D / 64); ++c) {
+      uint32_t orow[32];
+      tmem_ld32_nowait(tO + c * 32, orow);
+      tmem_wait_ld();
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        pk[e] = pack_bf16x2(__uint_as_float(orow[2 * e]) * inv, __uint_as_float(orow[2 * e + 1]) * inv);
+      if (row < rows) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) st_global_v4(dst + c * 32 + e * 8, pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+#if DS_FA_STAMPS
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    const long long t0 = fa_stamps[0][0][0];
+    for (int j = 0; j < min(J, 64); ++j)
+      printf("FA1 j=%2d  S %7lld P %7lld mmaP %7lld\n", j, fa_stamps[0][j][0] - t0, fa_stamps[0][j][1] - t0,
+             fa_stamps[0][j][2] - t0);
+  }
+#endif
+}
+
 template <int D>
 static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const bf16* v_layer, long long head_stride,
                         long long page_stride, long long layer_rows, const int32_t* table, int n_q, int q_pos0,
@@ -1287,16 +1629,23 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
       make_tmap_bf16(&tk, k_layer, layer_rows, D, D, 64, 64) || make_tmap_bf16(&tv, v_layer, layer_rows, D, D, 64, 64))
     return launch_status(cudaErrorInvalidValue);
   FaTcArgs a{n_q, q_pos0, n_heads, n_kv_heads, q_pos, head_stride / D, page_stride / D, table, o, ldo,
-             (float)(1.4426950408889634 / sqrt((double)D))};
+             (float)(1.4426950408889634 / sqrt((double)D)), q, ldq};
   // DS_FA_VARIANT: 0 whole-tile softmax (round 1), 1 whole-tile chunked, 2 split halves,
   // 3 dual softmax warps per row (default)
   static const int variant = [] {
     const char* e = getenv("DS_FA_VARIANT");
     const int v = e ? atoi(e) : 3;
-    return v < 0 || v > 3 ? 3 : v;
+    return v < 0 || v > 4 ? 3 : v;
   }();
+  static PerDevice attr[5];
+  if (variant == 4) {
+    using LO = FaOneSmem<D>;
+    if (int rc_ = launch_status(ensure_smem_attr(fa_one_kernel<D>, LO::TOTAL, attr[4]))) return rc_;
+    count_launch();
+    return launch_status(launch_pdl(fa_one_kernel<D>, dim3(n_heads, (n_q + FA_BM - 1) / FA_BM), dim3(FA_ONE_THREADS),
+                                    LO::TOTAL, stream, tk, tv, a));
+  }
   dim3 grid(n_heads, (n_q + 2 * FA_BM - 1) / (2 * FA_BM));
-  static PerDevice attr[4];
   if (variant == 3) {
     using LD = FaDualSmem<D>;
     if (int rc_ = launch_status(ensure_smem_attr(fa_dual_kernel<D>, LD::TOTAL, attr[3]))) return rc_;
