@@ -41,6 +41,15 @@ struct GemmSmem {
 DS_DEV void tile_coords(int t, int num_m, int num_n, int group, int& mb, int& nb) {
   // Grouped raster: `group` m-blocks sweep all n-blocks before moving on, so the
   // ~148 concurrently resident tiles share A rows and B columns in L2.
+  // group < 0: -group n-blocks sweep all m-blocks (a group's weight strips stay
+  // in L2 while the activations stream; long-K experiment).
+  if (group < 0) {
+    const int G = -group, per = G * num_m;
+    const int gi = t / per, first_n = gi * G, gsize = min(num_n - first_n, G), r = t - gi * per;
+    nb = first_n + r % gsize;
+    mb = r / gsize;
+    return;
+  }
   int per_group = group * num_n;
   int g = t / per_group;
   int first_m = g * group;
@@ -517,7 +526,10 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t leader_full0 = map_to_rank(&full[0], 0);
-      const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
+      // l2_hint 1: weights (B) evict_last, activations (A) evict_first; 2: the reverse (the
+      // group raster reuses a group's A strips across its waves, B strips once per wave)
+      const uint64_t pol_a = epi.l2_hint == 2 ? l2_policy_evict_last() : l2_policy_evict_first();
+      const uint64_t pol_b = epi.l2_hint == 2 ? l2_policy_evict_first() : l2_policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < num_tiles; t += n_pairs) {
@@ -740,7 +752,7 @@ int gemm_launch(const void* A, long long lda, const void* B, long long ldb, int 
     static const int group_long = env_or("DS_GEMM_GROUP_LONGK", 8);
     static const int l2hint = env_or("DS_GEMM_L2HINT", 0);
     const bool long_k = K > 8192;
-    e2.group = max(1, long_k ? group_long : group_short);
+    e2.group = long_k ? (group_long == 0 ? 1 : group_long) : max(1, group_short);
     e2.l2_hint = long_k ? l2hint : 0;
     if (make_tmap_bf16(&ta, A, epi.M, K, lda, GEMM_BM, GEMM_BK) ||
         make_tmap_bf16(&tb, B, epi.N, K, ldb, PAIR_HALF, GEMM_BK))
