@@ -1315,9 +1315,36 @@ struct FaOneSmem {
   static constexpr uint32_t TOTAL = XCH + 1024 + 1024;
 };
 
-template <int D>
-__global__ void __maxnreg__(136)
-    fa_one_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
+// MC: the CTA pair of a 2-CTA cluster (two query heads of one KV head, the same
+// Q rows) shares every K/V tile: each CTA loads one of the tile's two pages and
+// multicasts it into both CTAs' shared memory (half the L2->SM traffic), and
+// each CTA's MMA releases a stage in both CTAs (multicast commit), so a stage
+// is refilled only when both have consumed it.
+DS_DEV void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+DS_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+DS_DEV uint32_t fa_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DS_DEV void fa_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int D, bool MC>
+DS_DEV void fa_one_body(const CUtensorMap& tmK, const CUtensorMap& tmV, const FaTcArgs& a) {
   using L = FaOneSmem<D>;
   constexpr int CH = L::CH;
   constexpr int NS = FA_ONE_STAGES;
@@ -1352,9 +1379,9 @@ __global__ void __maxnreg__(136)
     tma_prefetch(&tmV);
     for (int i = 0; i < NS; ++i) {
       mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
+      mbar_init(&k_empty[i], MC ? 2 : 1);  // MC: both CTAs' MMAs release the stage
       mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
+      mbar_init(&v_empty[i], MC ? 2 : 1);
     }
     mbar_init(q_ready, 8);
     for (int i = 0; i < 2; ++i) {
@@ -1367,8 +1394,10 @@ __global__ void __maxnreg__(136)
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (MC) fa_cluster_sync();  // both CTAs' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int rank = MC ? (int)fa_cluster_rank() : 0;
   pdl_trigger();
   pdl_wait();
 
@@ -1387,12 +1416,22 @@ __global__ void __maxnreg__(136)
         }
         mbar_wait(&k_empty[st], ph ^ 1);
         mbar_expect_tx(&k_full[st], CH * L::CHUNK);
-        for (int p = 0; p < 2; ++p)
-          for (int c = 0; c < CH; ++c) tma_load_2d(sK(st, c) + p * 64 * 128, &tmK, &k_full[st], c * 64, krow[p]);
+        if (MC) {  // this CTA's page of the tile, into both CTAs
+          for (int c = 0; c < CH; ++c)
+            tma_load_2d_mc(sK(st, c) + rank * 64 * 128, &tmK, &k_full[st], c * 64, krow[rank], 3);
+        } else {
+          for (int p = 0; p < 2; ++p)
+            for (int c = 0; c < CH; ++c) tma_load_2d(sK(st, c) + p * 64 * 128, &tmK, &k_full[st], c * 64, krow[p]);
+        }
         mbar_wait(&v_empty[st], ph ^ 1);
         mbar_expect_tx(&v_full[st], CH * L::CHUNK);
-        for (int p = 0; p < 2; ++p)
-          for (int c = 0; c < CH; ++c) tma_load_2d(sV(st, c) + p * 64 * 128, &tmV, &v_full[st], c * 64, krow[p]);
+        if (MC) {
+          for (int c = 0; c < CH; ++c)
+            tma_load_2d_mc(sV(st, c) + rank * 64 * 128, &tmV, &v_full[st], c * 64, krow[rank], 3);
+        } else {
+          for (int p = 0; p < 2; ++p)
+            for (int c = 0; c < CH; ++c) tma_load_2d(sV(st, c) + p * 64 * 128, &tmV, &v_full[st], c * 64, krow[p]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -1409,7 +1448,8 @@ __global__ void __maxnreg__(136)
       }
       if (elect_one()) {
         umma_commit(&s_full[j & 1]);
-        umma_commit(&k_empty[st]);
+        if (MC) umma_commit_mc(&k_empty[st], 3);
+        else umma_commit(&k_empty[st]);
       }
       __syncwarp();
     };
@@ -1443,7 +1483,8 @@ __global__ void __maxnreg__(136)
       }
       if (elect_one()) {
         umma_commit(o_done);
-        umma_commit(&v_empty[st]);
+        if (MC) umma_commit_mc(&v_empty[st], 3);
+        else umma_commit(&v_empty[st]);
       }
       __syncwarp();
       if (j + 2 < J) qk(j + 2);  // into S[j & 1], after P.V(j) read P there (in-order tensor pipe)
@@ -1604,6 +1645,7 @@ __global__ void __maxnreg__(136)
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) fa_cluster_sync();  // the peer's multicasts and commits into this CTA are done
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -1616,6 +1658,17 @@ __global__ void __maxnreg__(136)
              fa_stamps[0][j][2] - t0);
   }
 #endif
+}
+
+template <int D>
+__global__ void __maxnreg__(136)
+    fa_one_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
+  fa_one_body<D, false>(tmK, tmV, a);
+}
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(136)
+    fa_mc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, FaTcArgs a) {
+  fa_one_body<D, true>(tmK, tmV, a);
 }
 
 template <int D>
@@ -1635,10 +1688,18 @@ static int fa_tc_launch(const bf16* q, long long ldq, const bf16* k_layer, const
   static const int variant = [] {
     const char* e = getenv("DS_FA_VARIANT");
     const int v = e ? atoi(e) : 3;
-    return v < 0 || v > 4 ? 3 : v;
+    return v < 0 || v > 5 ? 3 : v;
   }();
-  static PerDevice attr[5];
-  if (variant == 4) {
+  static PerDevice attr[6];
+  if (variant == 5 && n_heads % 2 == 0 && (n_heads / n_kv_heads) % 2 == 0) {
+    // head pairs (2p, 2p+1) share a KV head: 2-CTA clusters multicasting K/V
+    using LO = FaOneSmem<D>;
+    if (int rc_ = launch_status(ensure_smem_attr(fa_mc_kernel<D>, LO::TOTAL, attr[5]))) return rc_;
+    count_launch();
+    return launch_status(launch_pdl(fa_mc_kernel<D>, dim3(n_heads, (n_q + FA_BM - 1) / FA_BM), dim3(FA_ONE_THREADS),
+                                    LO::TOTAL, stream, tk, tv, a));
+  }
+  if (variant == 4 || variant == 5) {
     using LO = FaOneSmem<D>;
     if (int rc_ = launch_status(ensure_smem_attr(fa_one_kernel<D>, LO::TOTAL, attr[4]))) return rc_;
     count_launch();
