@@ -1012,12 +1012,45 @@ DS_DEV void attn_prefetch(const AttnArgs& a, int item, int D) {
   }
 }
 
+// Sum each of a lane's V values over the LPK lanes of its key group (the lane
+// bits below LPK), the same association tree as the xor butterfly (each node
+// is partial(lane) + partial(lane ^ o) of the same two partials; + commutes),
+// so bitwise equal to it -- with fewer shuffles: while a lane holds more than
+// one value, a level keeps half of them and receives the partner's partials
+// of that half instead of exchanging all of them (8 shuffles instead of 32 for
+// 8 values over 16 lanes).  On return v[0 .. max(1, V / LPK)) hold the sums of
+// values base.. (the returned index); lanes that end with the same index hold
+// the same sum.
+template <int V, int LPK>
+DS_DEV int rs_sum(float (&v)[V], int lane) {
+  int base = 0;
+#pragma unroll
+  for (int lvl = 0; (LPK >> (lvl + 1)) > 0; ++lvl) {
+    const int o = LPK >> (lvl + 1);
+    const int cnt = V >> lvl;  // values still held (compile time after unrolling)
+    if (cnt >= 2) {
+      const int h = cnt / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const float keep = up ? v[i + h] : v[i];
+        const float send = up ? v[i] : v[i + h];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      if (up) base += h;
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+  return base;
+}
+
 // Softmax of each head over the item's nk scores (log2 domain, in place):
 // stat = (max, sum) per head.
-template <int R>
 // Four of a lane's elements per step (independent loads and exponentials in
 // flight); the max is order-free and l still adds the lane's elements in
 // ascending order, so the result is the one-element loop's bit for bit.
+template <int R>
 DS_DEV void attn_softmax(int nk, int sk, float* sc, float* stat) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int r = warp; r < R; r += ATT_THREADS / 32) {
@@ -1191,25 +1224,18 @@ DS_DEV void attn_item(const AttnArgs& a, int item, float* sc, float* stat, unsig
             *reinterpret_cast<uint4*>(a.hi.k + a.hi.off(g, pos) + c * 8) = kv[j];
         }
       }
-      float p[U][R];
+      float p[U * R];  // value (j, r) at j * R + r
 #pragma unroll
       for (int j = 0; j < U; ++j)
 #pragma unroll
-        for (int r = 0; r < R; ++r) p[j][r] = dot8(kv[j], qv[r]);
+        for (int r = 0; r < R; ++r) p[j * R + r] = dot8(kv[j], qv[r]);
+      const int vb = rs_sum<U * R, LPK>(p, lane);
+      constexpr int VC = (U * R) / LPK > 0 ? (U * R) / LPK : 1;
 #pragma unroll
-      for (int o = LPK / 2; o; o >>= 1)
-#pragma unroll
-        for (int j = 0; j < U; ++j)
-#pragma unroll
-          for (int r = 0; r < R; ++r) p[j][r] += __shfl_xor_sync(0xffffffffu, p[j][r], o);
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
+      for (int i = 0; i < VC; ++i) {
+        const int idx = vb + i, j = idx / R, r = idx - j * R;
         const int key = base + j * KPW + kk;
-        float v = p[j][0];
-#pragma unroll
-        for (int r = 1; r < R; ++r)
-          if (c == r) v = p[j][r];
-        if (key < nk && c < R) sc[c * sk + key] = v * a.scale_log2;
+        if (key < nk) sc[r * sk + key] = p[i] * a.scale_log2;
       }
     }
   }
@@ -1540,23 +1566,18 @@ DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) 
           pr[j][i] = acc;
         }
       }
+      float pv[UK * R];  // value (j, r) at j * R + r
 #pragma unroll
-      for (int o = LPK / 2; o; o >>= 1)
+      for (int j = 0; j < UK; ++j)
 #pragma unroll
-        for (int j = 0; j < UK; ++j)
+        for (int r = 0; r < R; ++r) pv[j * R + r] = (r & 1) ? pr[j][r >> 1].y : pr[j][r >> 1].x;
+      const int vb = rs_sum<UK * R, LPK>(pv, lane);
+      constexpr int VC = (UK * R) / LPK > 0 ? (UK * R) / LPK : 1;
 #pragma unroll
-          for (int i = 0; i < RP; ++i) {
-            pr[j][i].x += __shfl_xor_sync(0xffffffffu, pr[j][i].x, o);
-            if (R >= 2) pr[j][i].y += __shfl_xor_sync(0xffffffffu, pr[j][i].y, o);
-          }
-#pragma unroll
-      for (int j = 0; j < UK; ++j) {
+      for (int i = 0; i < VC; ++i) {
+        const int idx = vb + i, j = idx / R, r = idx - j * R;
         const int key = warp * (ATT_PIECE / ATT_TW) + j * KPW + kk;
-        float v = pr[j][0].x;
-#pragma unroll
-        for (int r = 1; r < R; ++r)
-          if (c == r) v = (r & 1) ? pr[j][r >> 1].y : pr[j][r >> 1].x;
-        if (key < cnt && c < R) sc[c * sk + pk0 + key] = v * a.scale_log2;
+        if (key < cnt) sc[r * sk + pk0 + key] = pv[i] * a.scale_log2;
       }
       ingest(false, k0 + pk0, cnt, src);
       release();
