@@ -124,6 +124,39 @@ DS_DEV unsigned long long pack_argmax(float v, int idx) {
   return ((unsigned long long)key << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)idx);
 }
 
+// Sum each of a lane's V values over the LPK lanes of its key group (the lane
+// bits below LPK), the same association tree as the xor butterfly (each node
+// is partial(lane) + partial(lane ^ o) of the same two partials; + commutes),
+// so bitwise equal to it -- with fewer shuffles: while a lane holds more than
+// one value, a level keeps half of them and receives the partner's partials
+// of that half instead of exchanging all of them (8 shuffles instead of 32 for
+// 8 values over 16 lanes).  On return v[0 .. max(1, V / LPK)) hold the sums of
+// values base.. (the returned index); lanes that end with the same index hold
+// the same sum.
+template <int V, int LPK>
+DS_DEV int rs_sum(float (&v)[V], int lane) {
+  int base = 0;
+#pragma unroll
+  for (int lvl = 0; (LPK >> (lvl + 1)) > 0; ++lvl) {
+    const int o = LPK >> (lvl + 1);
+    const int cnt = V >> lvl;  // values still held (compile time after unrolling)
+    if (cnt >= 2) {
+      const int h = cnt / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const float keep = up ? v[i + h] : v[i];
+        const float send = up ? v[i] : v[i + h];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+      if (up) base += h;
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
+    }
+  }
+  return base;
+}
+
 // ---------------------------------------------------------------- GEMV
 
 // Global row of slot r (0..7) of tile t.  QKV tiles hold 4 RoPE pairs
@@ -268,15 +301,9 @@ DS_DEV void gemv_finish(const GemvArgs& a, int t, const float2* s2, float (*red)
   float s[GEMV_ROWS];
 #pragma unroll
   for (int r = 0; r < GEMV_ROWS; ++r) s[r] = s2[r].x + s2[r].y;
-#pragma unroll
-  for (int r = 0; r < GEMV_ROWS; ++r) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], o);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int r = 0; r < GEMV_ROWS; ++r) red[warp][r] = s[r];
-  }
+  // the 8 rows' warp sums: the xor butterfly's tree by reduce-scatter (rs_sum), 9 shuffles instead of 40
+  const int vb = rs_sum<GEMV_ROWS, 32>(s, lane);
+  if ((lane & 3) == 0) red[warp][vb] = s[0];
   sync();
   if (tid < GEMV_ROWS) {
     float v = 0.f;
@@ -671,21 +698,21 @@ DS_DEV void gemv_finish_rows(const GemvArgs& a, const GemvBatch& bt, int b0, int
                              const float2 (*s2)[GEMV_ROWS], float (*red)[NBW * GEMV_ROWS], unsigned long long& best,
                              const EpiPre& pre, Sync sync, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
+  {
+    // all rows' warp sums at once: the butterfly's tree by reduce-scatter (rs_sum)
+    constexpr int NV = NBW * GEMV_ROWS;
+    float sr[NV];
 #pragma unroll
-  for (int i = 0; i < NBW; ++i) {
-    if (i < nbw) {
-      float sr[GEMV_ROWS];
+    for (int i = 0; i < NBW; ++i)
 #pragma unroll
-      for (int r = 0; r < GEMV_ROWS; ++r) sr[r] = s2[i][r].x + s2[i][r].y;
+      for (int r = 0; r < GEMV_ROWS; ++r) sr[i * GEMV_ROWS + r] = i < nbw ? s2[i][r].x + s2[i][r].y : 0.f;
+    const int vb = rs_sum<NV, 32>(sr, lane);
+    constexpr int VC = NV / 32 > 0 ? NV / 32 : 1;
+    constexpr int DUP = NV >= 32 ? 1 : 32 / NV;  // lanes holding the same sum
+    if (lane % DUP == 0) {
 #pragma unroll
-      for (int r = 0; r < GEMV_ROWS; ++r) {
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sr[r] += __shfl_xor_sync(0xffffffffu, sr[r], o);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int r = 0; r < GEMV_ROWS; ++r) red[warp][i * GEMV_ROWS + r] = sr[r];
-      }
+      for (int q = 0; q < VC; ++q)
+        if (vb + q < GEMV_ROWS * nbw) red[warp][vb + q] = sr[q];
     }
   }
   sync();
@@ -1010,39 +1037,6 @@ DS_DEV void attn_prefetch(const AttnArgs& a, int item, int D) {
     if (key < a.n_lo && a.lo_remote) continue;  // peer memory: plain loads only
     prefetch_l2(attn_row(a, p & 1, g, key), (uint32_t)cnt * D * 2);
   }
-}
-
-// Sum each of a lane's V values over the LPK lanes of its key group (the lane
-// bits below LPK), the same association tree as the xor butterfly (each node
-// is partial(lane) + partial(lane ^ o) of the same two partials; + commutes),
-// so bitwise equal to it -- with fewer shuffles: while a lane holds more than
-// one value, a level keeps half of them and receives the partner's partials
-// of that half instead of exchanging all of them (8 shuffles instead of 32 for
-// 8 values over 16 lanes).  On return v[0 .. max(1, V / LPK)) hold the sums of
-// values base.. (the returned index); lanes that end with the same index hold
-// the same sum.
-template <int V, int LPK>
-DS_DEV int rs_sum(float (&v)[V], int lane) {
-  int base = 0;
-#pragma unroll
-  for (int lvl = 0; (LPK >> (lvl + 1)) > 0; ++lvl) {
-    const int o = LPK >> (lvl + 1);
-    const int cnt = V >> lvl;  // values still held (compile time after unrolling)
-    if (cnt >= 2) {
-      const int h = cnt / 2;
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < h; ++i) {
-        const float keep = up ? v[i + h] : v[i];
-        const float send = up ? v[i] : v[i + h];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-      if (up) base += h;
-    } else {
-      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], o);
-    }
-  }
-  return base;
 }
 
 // Softmax of each head over the item's nk scores (log2 domain, in place):
