@@ -1003,8 +1003,19 @@ int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int
 //           reduce the streams with shuffles; partial (m, l, o) per split
 //   merge   the last CTA of the kv head combines the splits (fixed order)
 
+// Items per row (kv head x key split) the split size aims for; DS_ATT_ITEMS
+// overrides it for measurements (every path reads the same value, so the
+// persistent and per-launch kernels keep the same split of every row).
+static int att_target_items() {
+  static const int v = [] {
+    const char* e = getenv("DS_ATT_ITEMS");
+    const int x = e ? atoi(e) : ATT_TARGET_ITEMS;
+    return x > 0 ? x : ATT_TARGET_ITEMS;
+  }();
+  return v;
+}
 int attn_split_keys(int n_keys, int n_kv_heads, int R) {
-  const int splits = (ATT_TARGET_ITEMS + n_kv_heads - 1) / n_kv_heads;
+  const int splits = (att_target_items() + n_kv_heads - 1) / n_kv_heads;
   int sk = (n_keys + splits - 1) / splits;
   sk = (sk + 31) & ~31;
   if (sk < 32) sk = 32;
@@ -1012,7 +1023,7 @@ int attn_split_keys(int n_keys, int n_kv_heads, int R) {
   return sk > cap ? cap : sk;
 }
 int attn_max_splits(int n_keys, int n_kv_heads, int R) {
-  return (ATT_TARGET_ITEMS + n_kv_heads - 1) / n_kv_heads + (n_keys + 4096 / R - 1) / (4096 / R) + 1;
+  return (att_target_items() + n_kv_heads - 1) / n_kv_heads + (n_keys + 4096 / R - 1) / (4096 / R) + 1;
 }
 static int attn_smem_bytes(int R, int sk, int splits) {
   const int scores = R * sk, merge = R * splits + R;
