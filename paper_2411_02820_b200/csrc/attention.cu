@@ -1142,27 +1142,14 @@ __global__ void __maxnreg__(80)
 #endif
       const int kbase = j * FA_BN + hf * 64;
       const bool maskit = j * FA_BN + FA_BN - 1 > tile_pos0;
-      // pass 1: this half's masked row max (both 32-column loads in flight)
+      // pass 1: this half's masked row max.  DS_FA_PASS1_BOTH 2: the second half's
+      // loads are issued while the first half's max is computed (48 registers)
       float mx = -INFINITY;
-#if DS_FA_PASS1_BOTH
-      uint32_t rr[2][32];
-      tmem_ld32_nowait(tS, rr[0]);
-      tmem_ld32_nowait(tS + 32, rr[1]);
-      tmem_wait_ld();
-#endif
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-#if DS_FA_PASS1_BOTH
-        uint32_t* r = rr[c];
-#else
-        uint32_t r[32];
-        tmem_ld32_nowait(tS + 32 * c, r);
-        tmem_wait_ld();
-#endif
+      auto max32 = [&](uint32_t* r, int col0) {  // masks r in place
         if (maskit) {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
-            if (kbase + 32 * c + e > qpos) r[e] = __float_as_uint(-INFINITY);
+            if (kbase + col0 + e > qpos) r[e] = __float_as_uint(-INFINITY);
         }
         float m4[4];
 #pragma unroll
@@ -1173,7 +1160,40 @@ __global__ void __maxnreg__(80)
 #pragma unroll
           for (int q = 0; q < 4; ++q) m4[q] = fmax3(m4[q], __uint_as_float(r[e + q]), __uint_as_float(r[e + 4 + q]));
         mx = fmax3(mx, fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      };
+#if DS_FA_PASS1_BOTH == 2
+      {
+        uint32_t r0[32], r1[16];
+        tmem_ld32_nowait(tS, r0);
+        tmem_wait_ld();
+        tmem_ld16_nowait(tS + 32, r1);  // in flight while the first half's max runs
+        max32(r0, 0);
+        tmem_ld16_nowait(tS + 48, r0);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r0[16 + e] = r0[e];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r0[e] = r1[e];
+        max32(r0, 32);
       }
+#elif DS_FA_PASS1_BOTH == 1
+      {
+        uint32_t rr[2][32];
+        tmem_ld32_nowait(tS, rr[0]);
+        tmem_ld32_nowait(tS + 32, rr[1]);
+        tmem_wait_ld();
+        max32(rr[0], 0);
+        max32(rr[1], 32);
+      }
+#else
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[32];
+        tmem_ld32_nowait(tS + 32 * c, r);
+        tmem_wait_ld();
+        max32(r, 32 * c);
+      }
+#endif
       // the pair agrees on the (lazily moved) max: one vote; maxima exchanged only when needed
       float ocorr = 1.f;
       if (bar_red_or(pair, 64, mx > m_used + thr)) {
