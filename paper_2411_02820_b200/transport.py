@@ -182,13 +182,25 @@ def job_tensors(prefill: PrefillResult, job: LinkJob, window: int) -> list:
     """The producer-side tensors one link job moves: E(a) [window, d], or K and
     V of layer l over the window (contiguous [KVH, window, D] each)."""
     if job.kind == "e":
-        return [prefill.e_map()[job.layer].hidden[:window]]
-    return [prefill.kv.k[job.layer, :, :window].contiguous(), prefill.kv.v[job.layer, :, :window].contiguous()]
+        return [job_tensor(prefill, job, window, 0)]
+    return [job_tensor(prefill, job, window, 0), job_tensor(prefill, job, window, 1)]
+
+
+def job_tensor(prefill: PrefillResult, job: LinkJob, window: int, part: int) -> torch.Tensor:
+    """Message ``part`` of a link job: E(a) (part 0), or K (0) / V (1) of the layer."""
+    if job.kind == "e":
+        return prefill.e_map()[job.layer].hidden[:window]
+    src = prefill.kv.k if part == 0 else prefill.kv.v
+    return src[job.layer, :, :window].contiguous()
 
 
 class NcclSender:
-    """Producer side: serves link jobs to consumer ranks in the planner's FIFO
-    order (sched.py:217-223) with point-to-point sends."""
+    """Producer side: serves link jobs to consumer ranks, each consumer's jobs
+    in the planner's FIFO order (sched.py:217-223).  The consumers are served
+    concurrently: message i of every consumer goes out in one grouped
+    point-to-point call (``batch_isend_irecv``: one NCCL group, so the sends to
+    different consumers overlap instead of queueing behind each other), and a
+    round's payloads are staged only for that round."""
 
     def __init__(self, group=None):
         self.group = group
@@ -197,10 +209,20 @@ class NcclSender:
         """requests: [(dst_rank, RecomputeConfig, n_tokens)] in arrival order."""
         import torch.distributed as dist
         sched = [ScheduledRequest(str(i), float(i), "m", cfg, n_layers) for i, (_, cfg, _) in enumerate(requests)]
+        per_dst: dict = {}
         for job in link_order(sched):
             dst, _, n = requests[job.request]
-            for t in job_tensors(prefill, job, n - 1):
-                dist.send(t, dst, group=self.group)
+            kinds = 1 if job.kind == "e" else 2  # E, or K then V
+            per_dst.setdefault(dst, []).extend((job, n, part) for part in range(kinds))
+        queues = list(per_dst.items())
+        for i in range(max((len(q) for _, q in queues), default=0)):
+            ops = []
+            for dst, q in queues:
+                if i < len(q):
+                    job, n, part = q[i]
+                    ops.append(dist.P2POp(dist.isend, job_tensor(prefill, job, n - 1, part), dst, group=self.group))
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
 
 
 class NcclTransport:
