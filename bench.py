@@ -51,8 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=150.0, help="seconds for the CPU reference leg")
     ap.add_argument("--graph", type=int, default=1, help="replay the consumer step as a CUDA graph")
-    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="N>1: consumers pull the producer's export over NVLink (CUDA IPC), or NCCL send/recv")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl", "bcast"],
+                    help="N>1: consumers pull the producer's export over NVLink (CUDA IPC), NCCL send/recv, or "
+                         "the export broadcast to all consumers (collectives: NVLS multicast on NVSwitch)")
     ap.add_argument("--mlp", default="ungated", choices=["ungated", "swiglu"],
                     help="ungated = the reference block (headline); swiglu = real Llama-3-8B MLP (second row)")
     ap.add_argument("--vocab", type=int, default=128256, help="32000 = Mistral-7B shape (config 3)")
@@ -834,9 +835,21 @@ def run_fanout(args, world, rank, local):
                     return P.partial_prefill_batch(B, batch_ids, rc, [r_.kv for r_ in remotes],
                                                    [r_.e_map for r_ in remotes], out=caches, stream=stream,
                                                    copy_stream=side, tokens_dev=batch_tok, workspace=ws_b)[0]
+        elif args.transport == "bcast":
+            from paper_2411_02820_b200.transport import broadcast_export
+            reused = rc.reused_layers(L)
+
+            def step():  # receive this step's context export, then the partial prefill on it
+                kv_b, e_b = broadcast_export(None, 0, cfg, n, rc.transition_layers, dev, layers=reused)
+                return P.partial_prefill(B, ids, rc, kv_b, e_b, out=cache, stream=stream, copy_stream=side,
+                                         tokens_dev=tok_dev)
         else:
             pipe = ConsumerPipeline(B, transport=NcclTransport(0, cfg, n, dev))
             step = lambda: pipe.run(ids, rc, None, None, out=cache, tokens_dev=tok_dev)  # noqa
+    elif args.transport == "bcast":
+        from paper_2411_02820_b200.transport import broadcast_export
+        step = lambda: broadcast_export(prod, 0, cfg, n, rc.transition_layers, dev,  # noqa
+                                        layers=rc.reused_layers(L))
     else:
         sender = NcclSender()
         step = lambda: sender.serve(prod, [(r, rc, n) for r in consumers], L)  # noqa
@@ -844,7 +857,7 @@ def run_fanout(args, world, rank, local):
     run = step
     use_graph = bool(args.graph) and args.transport == "p2p" and not producer
     graphed = bool(args.graph) and args.transport == "p2p"  # what the consumers do
-    if not producer or args.transport == "nccl":
+    if not producer or args.transport in ("nccl", "bcast"):
         with torch.cuda.stream(stream):
             step()
         torch.cuda.synchronize()
@@ -854,7 +867,7 @@ def run_fanout(args, world, rank, local):
             step()
         run = graph.replay
     for _ in range(args.warmup):
-        if not producer or args.transport == "nccl":
+        if not producer or args.transport in ("nccl", "bcast"):
             with torch.cuda.stream(stream):
                 run()
     torch.cuda.synchronize()
@@ -866,7 +879,7 @@ def run_fanout(args, world, rank, local):
     with ClockSampler(local) as clocks:
         for i in range(args.steps):
             starts[i].record(stream)
-            if not producer or args.transport == "nccl":
+            if not producer or args.transport in ("nccl", "bcast"):
                 with torch.cuda.stream(stream):
                     run()
             ends[i].record(stream)

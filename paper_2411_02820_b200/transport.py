@@ -15,6 +15,11 @@ pipelined plan (sched.py:212-263):
 * **NCCL send/recv (baseline).**  ``NcclSender.serve`` sends E(a) then KV(l) in
   the planner's link order; the consumer's ``NcclTransport`` receives each job
   into a staging slot on the link stream and ingests it from there.
+* **Broadcast fan-out.**  ``broadcast_export`` sends one context's export to
+  every consumer with collectives (E first, then K/V per layer ascending): on
+  NVSwitch systems NCCL runs them as in-switch multicast (NVLS), so the
+  producer's egress is one copy of the export whatever the consumer count
+  (unicast pulls cost it one copy per consumer).
 
 Handles and metadata travel as small picklable objects (``torch.distributed``
 object collectives), so the same code runs one process per GPU under torchrun.
@@ -291,3 +296,39 @@ def _ingest_slot(layer, k, v, dst_desc, window, cfg, link):
     rc = L.lib().ds_kv_ingest(C.byref(src), C.byref(dst_desc), arr, 1, window, cfg.n_kv_heads, cfg.head_dim,
                               link.cuda_stream, C.byref(miss))
     L.check(rc, miss.value, 1)
+
+
+# ---------------------------------------------------------------------------
+# Broadcast fan-out (collectives; NVLS multicast on NVSwitch)
+# ---------------------------------------------------------------------------
+
+
+def broadcast_export(prefill: PrefillResult | None, src: int, config, n_tokens: int, e_layers, device,
+                     layers=None, group=None):
+    """One context's export from rank ``src`` to every rank of ``group``:
+    E at ``e_layers`` first (it gates the recompute), then K and V of
+    ``layers`` (default: all) ascending -- the planner's link order
+    (sched.py:217-223) as collectives.  ``prefill`` is the producer's result on
+    ``src`` (None elsewhere).  Returns ``(LayerKV, {layer: ECache})`` on every
+    rank (the producer's own tensors on ``src``, fresh buffers elsewhere, with
+    the producer's context tag); layers not broadcast stay zero on receivers."""
+    import torch.distributed as dist
+    from .engine import LayerKV
+    rank = dist.get_rank(group) if group is not None else dist.get_rank()
+    e_layers = sorted(set(int(l) for l in e_layers))
+    layers = list(range(config.n_layers)) if layers is None else sorted(set(int(l) for l in layers))
+    tag = [prefill.kv.context if rank == src else None]
+    dist.broadcast_object_list(tag, src=src, group=group)
+    if rank == src:
+        kv = prefill.kv
+        e = {l: prefill.e_map()[l].hidden for l in e_layers}
+    else:
+        kv = LayerKV.empty(config, n_tokens, device)
+        e = {l: torch.empty(n_tokens - 1, config.d_model, dtype=torch.float32, device=device) for l in e_layers}
+    for l in e_layers:
+        dist.broadcast(e[l], src=src, group=group)
+    for l in layers:
+        dist.broadcast(kv.k[l], src=src, group=group)  # [KVH, n, D]: contiguous
+        dist.broadcast(kv.v[l], src=src, group=group)
+    kv.context = tag[0]
+    return kv, {l: ECache(l, t) for l, t in e.items()}

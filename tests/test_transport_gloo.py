@@ -95,3 +95,45 @@ def test_nccl_transport_sequence_over_gloo():
     # E first, then KV ascending (planner link order)
     assert order1 == [("e", 2), ("kv", 0), ("kv", 1), ("kv", 4), ("kv", 5)]
     assert order2 == [("e", 4), ("kv", 2), ("kv", 3), ("kv", 5)]
+
+
+def _bcast_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+
+    import paper_2411_02820_b200 as P
+    from paper_2411_02820_b200.transport import broadcast_export
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        Ln, G, n, D, d = 5, 2, 70, 16, 64
+        cfg = P.ModelConfig(Ln, d, 4, G, D, 128, 256, 512, 0)
+        pf = _prefill(Ln, G, n, D, d)
+        pf.kv.context = "ctx-digest"
+        rc = P.RecomputeConfig([(3, 4)])
+        kv, e = broadcast_export(pf if rank == 0 else None, 0, cfg, n, rc.transition_layers, "cpu",
+                                 layers=rc.reused_layers(Ln))
+        ok = kv.context == "ctx-digest" and sorted(e) == list(rc.transition_layers)
+        for l in rc.reused_layers(Ln):
+            ok = ok and torch.equal(kv.k[l], pf.kv.k[l]) and torch.equal(kv.v[l], pf.kv.v[l])
+        for l in rc.transition_layers:
+            ok = ok and torch.equal(e[l].hidden, pf.e_map()[l].hidden)
+        out_q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_fanout_gloo():
+    """broadcast_export (the collective fan-out): every consumer rank receives
+    the producer's E and reused-layer K/V bit-exactly, with the context tag."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_bcast_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
