@@ -8,6 +8,7 @@ recompute-layer set, and the consumer partial prefill.
 from .config import ModelConfig, PerturbationSpec, RecomputeConfig
 from .engine import (
     CapturedPartialPrefill,
+    CapturedPartialPrefillBatch,
     ECache,
     LayerKV,
     MixedPrefill,
@@ -31,7 +32,7 @@ from .weights import ModelWeights, build_model, model_ident, random_model, refer
 __version__ = "0.1.0"
 
 __all__ = [
-    "CapturedPartialPrefill", "CacheMissError", "CapacityError", "DegenerateInputError", "ECache", "LayerKV", "MixedPrefill",
+    "CapturedPartialPrefill", "CapturedPartialPrefillBatch", "CacheMissError", "CapacityError", "DegenerateInputError", "ECache", "LayerKV", "MixedPrefill",
     "ModelConfig", "ModelWeights", "PagedKV", "PerturbationSpec", "PrefillResult", "RecomputeConfig",
     "SchemaError", "build_model", "check_tokens", "full_prefill", "make_synthetic_dataset", "model_ident",
     "partial_prefill", "partial_prefill_batch", "random_model", "token_selective_prefill", "reference_weights", "workspace_bytes",

@@ -480,6 +480,82 @@ class CapturedPartialPrefill:
         return self.result
 
 
+class CapturedPartialPrefillBatch:
+    """:func:`partial_prefill_batch` captured once as a CUDA graph and replayed
+    per batch -- the serving form of config 4 for a fixed receiver, recompute
+    config, request lengths and one export per batch slot.  As
+    :class:`CapturedPartialPrefill`, slot b serves only the context of the export
+    it was captured with: :meth:`run` hashes each request's tokens and raises
+    ``CacheMissError`` for another context (store.py:351-395) instead of reusing
+    the wrong KV.  Construction runs the batch once eagerly (every validation and
+    cache-miss error surfaces there), then captures it with a private workspace
+    and fixed device token buffers; :meth:`run` copies the batch's tokens in and
+    replays the two-stream step.  The returned results are the same tensors on
+    every call."""
+
+    def __init__(self, receiver: ModelWeights, n_tokens: Sequence[int], config: RecomputeConfig,
+                 sender_kv: Sequence[LayerKV | None], sender_e: Sequence | None = None, *,
+                 out: Sequence[PagedKV] | None = None, stream=None, copy_stream=None, contexts=None):
+        cfg = receiver.config
+        self.receiver, self.ns = receiver, [int(n) for n in n_tokens]
+        nb = len(self.ns)
+        reads_export = bool(config.reused_layers(cfg.n_layers)) or any(a > 0 for a, _ in config.groups)
+        self.contexts = []
+        for b in range(nb):
+            if contexts is not None and contexts[b] is not None:
+                tag = _context_digest(check_tokens(contexts[b], cfg))
+            else:
+                tag = getattr(sender_kv[b], "context", None) if sender_kv[b] is not None else None
+            if reads_export and tag is None:
+                raise ValueError(f"slot {b}: the export carries no context tag: pass contexts=[...]")
+            self.contexts.append(tag if reads_export else None)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=receiver.device)
+        self.copy_stream = copy_stream if copy_stream is not None else torch.cuda.Stream(device=receiver.device)
+        with torch.cuda.stream(self.stream):
+            self.tokens_dev = [torch.zeros(n, dtype=torch.int64, device=receiver.device) for n in self.ns]
+            self.workspace = torch.empty(batch_workspace_bytes(cfg, max(self.ns), nb), dtype=torch.uint8,
+                                         device=receiver.device)
+        self.out = list(out) if out is not None else [PagedKV.allocate(cfg, n, receiver.device, zero=False)
+                                                     for n in self.ns]
+        probes = [np.zeros(n, dtype=np.int64) for n in self.ns]
+
+        def call():
+            return partial_prefill_batch(receiver, probes, config, sender_kv, sender_e, out=self.out,
+                                         stream=self.stream, copy_stream=self.copy_stream,
+                                         tokens_dev=self.tokens_dev, workspace=self.workspace)
+
+        with torch.cuda.stream(self.stream):
+            call()  # eager: raises like partial_prefill_batch
+        torch.cuda.synchronize(receiver.device)
+        reused = config.reused_layers(cfg.n_layers)
+        self._miss = (reused[0], "kv") if reused else (config.transition_layers[0] if config.transition_layers else 0,
+                                                      "e")
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self.result = call()
+
+    def run(self, tokens: Sequence) -> list:
+        if len(tokens) != len(self.ns):
+            raise ValueError(f"captured for a batch of {len(self.ns)}, got {len(tokens)}")
+        srcs = []
+        for b, t in enumerate(tokens):
+            ids = check_tokens(t.numpy() if isinstance(t, torch.Tensor) else t, self.receiver.config)
+            if ids.shape[0] != self.ns[b]:
+                raise ValueError(f"slot {b}: captured for {self.ns[b]} tokens, got {ids.shape[0]}")
+            if self.contexts[b] is not None and _context_digest(ids) != self.contexts[b]:
+                layer, kind = self._miss
+                raise CacheMissError(layer, kind, f"request {b} tokens are not the context of its captured export")
+            srcs.append(t if isinstance(t, torch.Tensor) else torch.from_numpy(ids))
+        caller = torch.cuda.current_stream(self.receiver.device)
+        self.stream.wait_stream(caller)
+        with torch.cuda.stream(self.stream):
+            for dst, src in zip(self.tokens_dev, srcs):
+                dst.copy_(src, non_blocking=True)
+            self.graph.replay()
+        caller.wait_stream(self.stream)
+        return self.result
+
+
 def token_selective_prefill(receiver: ModelWeights, tokens, sender_kv: LayerKV, ratio: float, *,
                             out: PagedKV | None = None, stream=None,
                             tokens_dev: torch.Tensor | None = None) -> MixedPrefill:

@@ -100,3 +100,27 @@ def test_batch_errors_name_the_request():
                                 [p.e_map() for p in prods] + [None])
     with pytest.raises(P.DegenerateInputError):
         P.partial_prefill_batch(B, [toks[0], np.array([1])], rc, [prods[0].kv, prods[0].kv])
+
+
+def test_captured_batch_replays_and_guards_contexts():
+    """CapturedPartialPrefillBatch: one graph replay per batch equals the eager
+    batch bit for bit; a request whose tokens are not its slot's context raises
+    CacheMissError instead of reusing another context's KV."""
+    import paper_2411_02820_b200 as P
+    cfg, A, B = _pair(P, "tiny")
+    rng = np.random.default_rng(17)
+    toks = [rng.integers(0, cfg.vocab_size, size=n, dtype=np.int64) for n in (300, 180, 257)]
+    rc = P.RecomputeConfig([(2, 3)])
+    prods = [P.full_prefill(A, t, e_layers=rc.transition_layers) for t in toks]
+    cap = P.CapturedPartialPrefillBatch(B, [len(t) for t in toks], rc, [p.kv for p in prods],
+                                        [p.e_map() for p in prods])
+    got = [r.logits.clone() for r in cap.run(toks)]
+    ref = P.partial_prefill_batch(B, toks, rc, [p.kv for p in prods], [p.e_map() for p in prods])
+    torch.cuda.synchronize()
+    for b in range(3):
+        assert torch.equal(got[b], ref[b].logits), b
+    swapped = [toks[0], toks[1], rng.integers(0, cfg.vocab_size, size=257, dtype=np.int64)]  # not slot 2's context
+    with pytest.raises(P.CacheMissError):
+        cap.run(swapped)
+    with pytest.raises(ValueError):
+        cap.run(toks[:2])
