@@ -764,15 +764,18 @@ DS_DEV void gemv_finish_rows(const GemvArgs& a, const GemvBatch& bt, int b0, int
   sync();  // red[] reused by the next tile
 }
 
-template <int KS, int NBW, int WG>
+template <int KS, int NBW, int WG, bool xstream>
 __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80)))
     gemv_batch_kernel(const __grid_constant__ GemvArgs a, const __grid_constant__ GemvBatch bt, int slots) {
   constexpr int SLOT = GEMV_ROWS * KS * 2;
   constexpr int CPT = KS / (GEMV_THREADS * 8);
   constexpr int NC = WG * GEMV_THREADS;
+  // xstream (bf16 x too large to stage whole, e.g. W2 at 8 rows): each ring slot
+  // also carries the rows' x slice for its K range (the same bytes, per tile)
+  const int SLOTX = xstream ? SLOT + bt.nb * KS * 2 : SLOT;
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* ring = smem_dyn;
-  bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * SLOT);  // [nb][K]
+  bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * SLOTX);  // [nb][K] (not xstream)
   __shared__ __align__(8) uint64_t full[16], empty[16];
   __shared__ float red[WG][GEMV_WARPS][NBW * GEMV_ROWS];
   __shared__ float ssq[WG][GEMV_WARPS];
@@ -788,17 +791,27 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
   __syncthreads();
   pdl_trigger();
   if (tid >= NC) {
-    if (tid == NC) {  // producer: the weights never depend on the predecessor
+    if (tid == NC) {  // producer: the weights never depend on the predecessor (x does)
       int slot = 0;
       uint32_t phase = 0;
+      bool waited = false;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x)
         for (int s = 0; s < ks; ++s) {
           mbar_wait(&empty[slot], phase ^ 1);
-          mbar_expect_tx(&full[slot], SLOT);
+          mbar_expect_tx(&full[slot], SLOTX);
+          uint8_t* dst = ring + (size_t)slot * SLOTX;
 #pragma unroll
           for (int r = 0; r < GEMV_ROWS; ++r)
-            bulk_g2s(ring + slot * SLOT + r * KS * 2, a.W + (long long)gemv_row(a, t, r) * a.ldw + (long long)s * KS,
-                     KS * 2, &full[slot]);
+            bulk_g2s(dst + r * KS * 2, a.W + (long long)gemv_row(a, t, r) * a.ldw + (long long)s * KS, KS * 2,
+                     &full[slot]);
+          if (xstream) {
+            if (!waited) {
+              pdl_wait();
+              waited = true;
+            }
+            for (int b = 0; b < bt.nb; ++b)
+              bulk_g2s(dst + SLOT + b * KS * 2, a.x_bf16 + b * bt.x_stride + (long long)s * KS, KS * 2, &full[slot]);
+          }
           if (++slot == slots) {
             slot = 0;
             phase ^= 1;
@@ -812,9 +825,11 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
   const int nbw = min(NBW, bt.nb - b0);
   auto sync = [wg] { bar_named(1 + wg, GEMV_THREADS); };
   pdl_wait();
-  for (int i = 0; i < nbw; ++i) {
-    const GemvArgs v = gemv_row_view(a, bt, b0 + i);
-    gemv_stage_x_t(v, xs + (long long)(b0 + i) * a.K, ssq[wg], t, sync);
+  if (!xstream) {
+    for (int i = 0; i < nbw; ++i) {
+      const GemvArgs v = gemv_row_view(a, bt, b0 + i);
+      gemv_stage_x_t(v, xs + (long long)(b0 + i) * a.K, ssq[wg], t, sync);
+    }
   }
   int slot = 0;
   uint32_t phase = 0;
@@ -837,8 +852,11 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
         float2 xf[NBW][4];
 #pragma unroll
         for (int i = 0; i < NBW; ++i) {
-          const uint4 xv = i < nbw ? *reinterpret_cast<const uint4*>(xs + (long long)(b0 + i) * a.K + c * 8)
-                                   : make_uint4(0u, 0u, 0u, 0u);
+          const uint4* xp =
+              xstream ? reinterpret_cast<const uint4*>(ring + (size_t)slot * SLOTX + SLOT + (b0 + i) * KS * 2 +
+                                                       (cc * GEMV_THREADS + t) * 16)
+                      : reinterpret_cast<const uint4*>(xs + (long long)(b0 + i) * a.K + c * 8);
+          const uint4 xv = i < nbw ? *xp : make_uint4(0u, 0u, 0u, 0u);
           xf[i][0] = bf16x2_to_float2(xv.x);
           xf[i][1] = bf16x2_to_float2(xv.y);
           xf[i][2] = bf16x2_to_float2(xv.z);
@@ -847,7 +865,7 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
 #pragma unroll
         for (int r = 0; r < GEMV_ROWS; ++r) {
           const uint4 w =
-              *reinterpret_cast<const uint4*>(ring + slot * SLOT + r * KS * 2 + (cc * GEMV_THREADS + t) * 16);
+              *reinterpret_cast<const uint4*>(ring + (size_t)slot * SLOTX + r * KS * 2 + (cc * GEMV_THREADS + t) * 16);
           const float2 w0 = bf16x2_to_float2(w.x), w1 = bf16x2_to_float2(w.y);
           const float2 w2 = bf16x2_to_float2(w.z), w3 = bf16x2_to_float2(w.w);
 #pragma unroll
@@ -882,17 +900,18 @@ __global__ void __maxnreg__(WG == 1 ? 168 : (WG == 2 ? 136 : (WG == 3 ? 104 : 80
 }
 
 template <int KS, int NBW, int WG>
-static int gemv_batch_launch_t(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream) {
+static int gemv_batch_launch_t(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream, bool xstream = false) {
   constexpr int SLOT = GEMV_ROWS * KS * 2;
-  const int xbytes = (bt.nb * a.K * 2 + 127) & ~127;
+  const int slotx = xstream ? SLOT + bt.nb * KS * 2 : SLOT;
+  const int xbytes = xstream ? 0 : (bt.nb * a.K * 2 + 127) & ~127;
   static const int budget = env_int("DS_GEMV_SMEM_KB", 196) * 1024;  // fits beside a persistent anchor CTA
-  int slots = (budget - xbytes) / SLOT;
+  int slots = (budget - xbytes) / slotx;
   slots = slots > 16 ? 16 : slots;
   if (slots < 2) return DS_ERR_INVALID;
-  const int smem = slots * SLOT + xbytes;
-  auto kern = gemv_batch_kernel<KS, NBW, WG>;
-  static PerDevice attr;
-  if (int rc_ = launch_status(ensure_smem_attr(kern, smem, attr))) return rc_;
+  const int smem = slots * slotx + xbytes;
+  auto kern = xstream ? gemv_batch_kernel<KS, NBW, WG, true> : gemv_batch_kernel<KS, NBW, WG, false>;
+  static PerDevice attr[2];
+  if (int rc_ = launch_status(ensure_smem_attr(kern, smem, attr[xstream ? 1 : 0]))) return rc_;
   const int tiles = a.N / GEMV_ROWS, cap = num_sms();
   const int grid = tiles < cap ? tiles : cap;
   count_launch();
@@ -903,31 +922,34 @@ static int gemv_batch_launch_t(const GemvArgs& a, const GemvBatch& bt, cudaStrea
 #define DS_GEMVB_NBW 2  // rows per consumer warpgroup (experiments: 1, 2, 4)
 #endif
 template <int KS>
-static int gemv_batch_launch_ks(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream) {
+static int gemv_batch_launch_ks(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream, bool xstream = false) {
   if (DS_GEMVB_NBW == 1 && bt.nb <= 4) {
     switch (bt.nb) {
-      case 1: return gemv_batch_launch_t<KS, 1, 1>(a, bt, stream);
-      case 2: return gemv_batch_launch_t<KS, 1, 2>(a, bt, stream);
-      case 3: return gemv_batch_launch_t<KS, 1, 3>(a, bt, stream);
-      default: return gemv_batch_launch_t<KS, 1, 4>(a, bt, stream);
+      case 1: return gemv_batch_launch_t<KS, 1, 1>(a, bt, stream, xstream);
+      case 2: return gemv_batch_launch_t<KS, 1, 2>(a, bt, stream, xstream);
+      case 3: return gemv_batch_launch_t<KS, 1, 3>(a, bt, stream, xstream);
+      default: return gemv_batch_launch_t<KS, 1, 4>(a, bt, stream, xstream);
     }
   }
   if (DS_GEMVB_NBW == 4) {
-    if (bt.nb <= 4) return gemv_batch_launch_t<KS, 4, 1>(a, bt, stream);
-    return gemv_batch_launch_t<KS, 4, 2>(a, bt, stream);
+    if (bt.nb <= 4) return gemv_batch_launch_t<KS, 4, 1>(a, bt, stream, xstream);
+    return gemv_batch_launch_t<KS, 4, 2>(a, bt, stream, xstream);
   }
   switch ((bt.nb + 1) / 2) {
-    case 1: return gemv_batch_launch_t<KS, 2, 1>(a, bt, stream);
-    case 2: return gemv_batch_launch_t<KS, 2, 2>(a, bt, stream);
-    case 3: return gemv_batch_launch_t<KS, 2, 3>(a, bt, stream);
-    default: return gemv_batch_launch_t<KS, 2, 4>(a, bt, stream);
+    case 1: return gemv_batch_launch_t<KS, 2, 1>(a, bt, stream, xstream);
+    case 2: return gemv_batch_launch_t<KS, 2, 2>(a, bt, stream, xstream);
+    case 3: return gemv_batch_launch_t<KS, 2, 3>(a, bt, stream, xstream);
+    default: return gemv_batch_launch_t<KS, 2, 4>(a, bt, stream, xstream);
   }
 }
 
-// Rows per launch: as many as fit in shared memory beside a 2-slot ring (W2 at
-// d_ff = 14336: 4 rows of 28 KB; the 8B shape's other GEMVs: 8).  Shapes the
-// TMA kernel does not take (K not a multiple of 1024, fewer tiles than SMs)
-// run the single-row GEMV per row -- the same bits.
+// Rows per launch: as many as fit in shared memory beside a 2-slot ring (the
+// 8B shape's K = 4096 GEMVs: 8).  A bf16 x that does not fit whole (W2 at
+// d_ff = 14336 beyond 4 rows of 28 KB) is streamed through the ring with the
+// weights instead (DS_GEMVB_XSTREAM=0: split into launches of `fit` rows, each
+// re-reading the weights).  Shapes the TMA kernel does not take (K not a
+// multiple of 1024, fewer tiles than SMs) run the single-row GEMV per row --
+// the same bits either way.
 int gemv_batch_launch(const GemvArgs& a, const GemvBatch& bt, cudaStream_t stream) {
   if (bt.nb < 1 || bt.nb > kMaxBatch) return DS_ERR_INVALID;
   if ((a.N % GEMV_ROWS) || (a.K & 7) || (a.mode == EPI_SWIGLU_BF16 && a.N % 32)) return DS_ERR_INVALID;
@@ -942,6 +964,12 @@ int gemv_batch_launch(const GemvArgs& a, const GemvBatch& bt, cudaStream_t strea
     for (int b = 0; b < bt.nb; ++b)
       if (int rc = gemv_launch(gemv_row_view(a, bt, b), stream)) return rc;
     return DS_OK;
+  }
+  static const bool xstream_ok = env_int("DS_GEMVB_XSTREAM", 1) != 0;
+  if (xstream_ok && bt.nb > fit && !a.x_f32 && a.x_bf16) {
+    if (ks == 4096) return gemv_batch_launch_ks<4096>(a, bt, stream, true);
+    if (ks == 2048) return gemv_batch_launch_ks<2048>(a, bt, stream, true);
+    return gemv_batch_launch_ks<1024>(a, bt, stream, true);
   }
   for (int b0 = 0; b0 < bt.nb; b0 += fit) {
     GemvArgs sa = gemv_row_view(a, bt, b0);  // row b0 becomes row 0 of the launch
