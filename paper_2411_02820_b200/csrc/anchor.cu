@@ -966,7 +966,12 @@ int gemv_batch_launch(const GemvArgs& a, const GemvBatch& bt, cudaStream_t strea
     return DS_OK;
   }
   static const bool xstream_ok = env_int("DS_GEMVB_XSTREAM", 1) != 0;
-  if (xstream_ok && bt.nb > fit && !a.x_f32 && a.x_bf16) {
+  // bf16 x: stream it with the weights when that keeps more weight slots in
+  // flight than staging it whole (or when it does not fit at all)
+  const int slot_b = GEMV_ROWS * ks * 2;
+  const int staged_slots = bt.nb <= fit ? (budget - ((bt.nb * a.K * 2 + 127) & ~127)) / slot_b : 0;
+  const int stream_slots = budget / (slot_b + bt.nb * ks * 2);
+  if (xstream_ok && !a.x_f32 && a.x_bf16 && stream_slots >= 2 && stream_slots > staged_slots) {
     if (ks == 4096) return gemv_batch_launch_ks<4096>(a, bt, stream, true);
     if (ks == 2048) return gemv_batch_launch_ks<2048>(a, bt, stream, true);
     return gemv_batch_launch_ks<1024>(a, bt, stream, true);
