@@ -355,9 +355,10 @@ def run_reference(args, world, rank):
 # ---------------------------------------------------------------------------
 
 
-def time_kernel(fn, reps, stream):
+def time_kernel(fn, reps, stream, warmup=1):
     import torch
-    fn()
+    for _ in range(warmup):
+        fn()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
@@ -408,7 +409,7 @@ def batch_leg(P, _lib, cfg, A, B, rc, n, sizes, single_ttft_ms, single_anchor_ms
         bdesc = B.desc()
         anc = time_kernel(lambda: _lib.check(_lib.lib().ds_anchor_batch(
             ctypes.byref(bdesc), nb, anc_ids.data_ptr(), pos, descs, lg.data_ptr(), tk.data_ptr(), ws.data_ptr(),
-            ws.numel(), stream.cuda_stream)), 5, stream)
+            ws.numel(), stream.cuda_stream)), 10, stream, warmup=3)
         # batched greedy decode: dsteps tokens per sequence after the prefills
         with torch.cuda.stream(stream):
             decode_greedy_batch(B, caches, res, 2, [n] * nb)  # warm-up

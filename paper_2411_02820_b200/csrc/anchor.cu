@@ -34,6 +34,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -1363,11 +1365,29 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_decode_kernel(AttnArgs a) {
 // barrier) or by a recompute the chain waited on with an event before the
 // layer's QKV GEMV / this kernel launched.
 constexpr int ATT_PIECE = 32;  // keys per ring piece (pages are 64-key aligned)
+// P.V by key streams across warps (1, default) or attn_item's lane layout (0: A/B)
+#ifndef DS_ATT_PV_STREAMS
+#define DS_ATT_PV_STREAMS 1
+#endif
 constexpr int ATT_SLOTS_MAX = 16;
 constexpr int ATT_TW = 8;                         // compute warps
 constexpr int ATT_TTHREADS = ATT_TW * 32 + 32;  // + producer warp
 
 DS_DEV void named_sync_compute() { asm volatile("bar.sync 2, %0;" ::"n"(ATT_TW * 32) : "memory"); }
+
+#if DS_ATT_STAMPS
+// Debug timeline (build with DS_NVCC_EXTRA=-DDS_ATT_STAMPS=1): a few CTAs of
+// one launch print global-timer stamps of their phases.
+__device__ unsigned int g_att_launch;
+#define ATT_STAMP(i) \
+  do {                \
+    if (tid == 0) st_ns[i] = global_ns(); \
+  } while (0)
+#else
+#define ATT_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
 
 // attn_finish for the 8-warp stand-alone kernel: the same (m, l) store,
 // arrival count and merge arithmetic (same max, same lane-strided sums, each
@@ -1377,7 +1397,7 @@ DS_DEV void named_sync_compute() { asm volatile("bar.sync 2, %0;" ::"n"(ATT_TW *
 // instead of one per group of splits.
 template <int D, int R>
 DS_DEV void attn_finish_wide(const AttnArgs& a, int g, int s, float* sc, const float* stat, unsigned int* is_last,
-                             uint8_t* stage, int stage_bytes, uint64_t* bar) {
+                             uint8_t* stage, int stage_bytes, uint64_t* bar, unsigned long long* st_ns) {
   constexpr int NT = ATT_TW * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < R) {
@@ -1385,12 +1405,20 @@ DS_DEV void attn_finish_wide(const AttnArgs& a, int g, int s, float* sc, const f
     __stcg(ml, stat[2 * tid]);
     __stcg(ml + 1, stat[2 * tid + 1]);
   }
-  __threadfence();
+  // release: the CTA barrier orders every thread's part_o / (m, l) stores
+  // before thread 0's gpu-scope fence and arrival; the last arrival's thread 0
+  // fences again (acquire) before the barrier that releases the merge's
+  // reads (the grid-barrier pattern: one thread waits on each fence)
   named_sync_compute();
-  if (tid == 0) *is_last = (atomicAdd(a.counters + g, 1u) == (unsigned)a.splits - 1);
+  if (tid == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const bool last = atomicAdd(a.counters + g, 1u) == (unsigned)a.splits - 1;
+    if (last) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    *is_last = last;
+  }
   named_sync_compute();
+  ATT_STAMP(7);
   if (!*is_last) return;
-  __threadfence();
   const int n_ml = R * a.splits * 2;
   const uint32_t o_bytes = (uint32_t)R * a.splits * D * 4;
   const bool staged = (int)o_bytes + 4 * n_ml <= stage_bytes;
@@ -1430,41 +1458,71 @@ DS_DEV void attn_finish_wide(const AttnArgs& a, int g, int s, float* sc, const f
   }
   if (staged) mbar_wait(bar, 0);
   named_sync_compute();  // wts / den written, partial outputs landed
+  ATT_STAMP(8);
+  // each output over the splits in ascending order (attn_finish's chain); a
+  // thread's PER outputs advance together (independent chains), the staged
+  // form reads shared memory explicitly and keeps 8 splits' loads ahead
   constexpr int PER = (R * D + NT - 1) / NT;
+  float num[PER];
+  int rq[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    num[q] = 0.f;
+    rq[q] = min((tid + q * NT) / D, R - 1);
+  }
+  const int sp = a.splits;
+  if (staged) {
+    uint32_t pa[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int idx = min(tid + q * NT, R * D - 1);
+      pa[q] = smem_u32(po_s + (long long)rq[q] * sp * D + idx % D);
+    }
+    int s2 = 0;
+    for (; s2 + 8 <= sp; s2 += 8) {
+      float v[PER][8];
+#pragma unroll
+      for (int q = 0; q < PER; ++q)
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[q][u]) : "r"(pa[q] + (uint32_t)((s2 + u) * D * 4)));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int q = 0; q < PER; ++q) num[q] = fmaf(wts[rq[q] * sp + s2 + u], v[q][u], num[q]);
+    }
+    for (; s2 < sp; ++s2)
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(pa[q] + (uint32_t)(s2 * D * 4)));
+        num[q] = fmaf(wts[rq[q] * sp + s2], v, num[q]);
+      }
+  } else {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int idx = min(tid + q * NT, R * D - 1);
+      const float* po = po_g + (long long)rq[q] * sp * D + idx % D;
+      for (int s2 = 0; s2 < sp; ++s2) num[q] = fmaf(wts[rq[q] * sp + s2], __ldcg(po + (long long)s2 * D), num[q]);
+    }
+  }
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int idx = tid + q * NT;
-    if (idx < R * D) {
-      const int r = idx / D, dd = idx % D;
-      const float* po = (staged ? po_s : po_g) + (long long)r * a.splits * D + dd;
-      float num = 0.f;
-      for (int s2 = 0; s2 < a.splits; ++s2)
-        num = fmaf(wts[r * a.splits + s2], staged ? po[(long long)s2 * D] : __ldcg(po + (long long)s2 * D), num);
-      a.out[(long long)(g * R + r) * D + dd] = __float2bfloat16_rn(num / den[r]);
-    }
+    if (idx < R * D) a.out[(long long)(g * R) * D + idx] = __float2bfloat16_rn(num[q] / den[rq[q]]);
   }
   if (tid == 0) a.counters[g] = 0u;
 }
 
-#if DS_ATT_STAMPS
-// Debug timeline (build with DS_NVCC_EXTRA=-DDS_ATT_STAMPS=1): a few CTAs of
-// one launch print global-timer stamps of their phases.
-__device__ unsigned int g_att_launch;
-#define ATT_STAMP(i) \
-  do {                \
-    if (tid == 0) st_ns[i] = global_ns(); \
-  } while (0)
-#else
-#define ATT_STAMP(i) \
-  do {                \
-  } while (0)
-#endif
 
 // One (kv head, split) item of row `a` (the kernel body; `item` replaces item).
 template <int D, int R>
 DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) {
 #if DS_ATT_STAMPS
-  unsigned long long st_ns[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long st_ns[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long ck0 = 0, ck1 = 0;  // SM cycles over the P.V phase (clock rate check)
+#else
+  unsigned long long* st_ns = nullptr;
 #endif
   constexpr int ROWB = D * 2, PIECE_B = ATT_PIECE * ROWB;
   // scores: each warp takes ATT_PIECE / ATT_TW keys of a piece, LPK lanes per key
@@ -1473,8 +1531,9 @@ DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) 
   // P.V: warps (w & 3) own dim chunks like attn_item's 4 warps; warps >= 4
   // take the upper half of the heads (R >= 2), so every accumulator sums the
   // same keys in the same order
-  constexpr int CPW = LPK / 4, NS = 32 / CPW, UV = ATT_PIECE / NS;
-  constexpr int HR = R >= 2 ? R / 2 : 1;
+  constexpr int CPW = LPK / 4, NS = 32 / CPW;
+  [[maybe_unused]] constexpr int UV = ATT_PIECE / NS;
+  [[maybe_unused]] constexpr int HR = R >= 2 ? R / 2 : 1;
   constexpr int RP = R >= 2 ? R / 2 : 1;  // head pairs (scores, packed)
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* ring = smem_dyn;
@@ -1498,8 +1557,8 @@ DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) 
   }
   // optionally pull the whole item toward L2 first (the ring then reads L2)
   if (prefetch & 1) attn_prefetch(a, item, D);
-  // timing experiments (results are wrong): data movement only, or no scores / no P.V math
-  const bool no_scores = prefetch & 6, no_pv = prefetch & 10;
+  // timing experiments (results are wrong): data movement only, or no scores / no P.V math / no softmax (bit 4)
+  const bool no_scores = prefetch & 6, no_pv = prefetch & 10, no_softmax = prefetch & 16;
   __syncthreads();
   pdl_trigger();
   if (warp == ATT_TW) {
@@ -1577,6 +1636,7 @@ DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) 
       const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
       mbar_wait(&full[slot], phase);
       if (p == 0) ATT_STAMP(2);
+      if (p == np - 1) ATT_STAMP(9);
       const uint8_t* src = ring + slot * PIECE_B;
       if (no_scores) {
         release();
@@ -1623,9 +1683,108 @@ DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) 
   }
   named_sync_compute();
   ATT_STAMP(3);
-  if (warp < ATT_THREADS / 32) attn_softmax<R>(nk, sk, sc, stat);
+  if (warp < ATT_THREADS / 32 && !no_softmax) attn_softmax<R>(nk, sk, sc, stat);
   named_sync_compute();
   ATT_STAMP(4);
+#if DS_ATT_STAMPS
+  if (tid == 0) ck0 = clock64();
+#endif
+#if DS_ATT_PV_STREAMS
+  // ---- P.V, key streams across warps: warp w runs streams w, w + 8, ... (keys
+  // st, st + NS, ... of attn_item's lane (chunk, st)), each lane D/32
+  // contiguous dims of every head -- conflict-free row reads, broadcast P.
+  // The streams' partials then meet in shared memory in the xor-butterfly's
+  // tree ((s0 + s1) + (s2 + s3)) + ..., so every output is attn_item's bit for bit.
+  {
+    constexpr int DPL = D / 32, SPW = NS / ATT_TW;
+    static_assert(NS % ATT_TW == 0, "streams per warp");
+    float2 acc[SPW][R][DPL / 2];
+#pragma unroll
+    for (int q = 0; q < SPW; ++q)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < DPL / 2; ++e) acc[q][r][e] = make_float2(0.f, 0.f);
+    for (int p = 0; p < np; ++p) {
+      const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
+      mbar_wait(&full[slot], phase);
+      if (p == np - 1) ATT_STAMP(10);
+      const uint8_t* src = ring + slot * PIECE_B;
+      // a full piece loads every key's V slice and P values before the first
+      // FMA (no per-key guards); the last piece of a split keeps the guards
+      auto piece = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        constexpr int KJ = ATT_PIECE / NS;
+        constexpr int RP = R <= 4 ? R : 1;  // P values held ahead (R = 8 reads them at the FMA: registers)
+        float2 vf[SPW][KJ][DPL / 2];
+        float pp[SPW][KJ][RP];
+#pragma unroll
+        for (int q = 0; q < SPW; ++q)
+#pragma unroll
+          for (int j = 0; j < KJ; ++j) {
+            const int key = warp + q * ATT_TW + j * NS;
+            if (FULL || key < cnt) {
+              if constexpr (DPL == 4) {
+                const uint2 vv = *reinterpret_cast<const uint2*>(src + key * ROWB + lane * 8);
+                vf[q][j][0] = unpack_bf16x2(vv.x);
+                vf[q][j][1] = unpack_bf16x2(vv.y);
+              } else {
+                vf[q][j][0] = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(src + key * ROWB + lane * 4));
+              }
+              if constexpr (R <= 4)
+#pragma unroll
+                for (int r = 0; r < R; ++r) pp[q][j][r] = sc[r * sk + pk0 + key];
+            }
+          }
+#pragma unroll
+        for (int q = 0; q < SPW; ++q)
+#pragma unroll
+          for (int j = 0; j < KJ; ++j) {
+            const int key = warp + q * ATT_TW + j * NS;
+            if (FULL || key < cnt) {
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const float pr = R <= 4 ? pp[q][j][r < RP ? r : 0] : sc[r * sk + pk0 + key];
+                const float2 p2 = make_float2(pr, pr);
+#pragma unroll
+                for (int e = 0; e < DPL / 2; ++e) acc[q][r][e] = ffma2(p2, vf[q][j][e], acc[q][r][e]);
+              }
+            }
+          }
+      };
+      if (!no_pv) {
+        if (cnt == ATT_PIECE)
+          piece(std::true_type{});
+        else
+          piece(std::false_type{});
+      }
+      ingest(true, k0 + pk0, cnt, src);
+      release();
+    }
+    named_sync_compute();  // every warp is done with the ring: it stages the stream partials
+    float* part = reinterpret_cast<float*>(ring);  // [NS][R][D]
+#pragma unroll
+    for (int q = 0; q < SPW; ++q)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int e = 0; e < DPL / 2; ++e)
+          *reinterpret_cast<float2*>(part + ((warp + q * ATT_TW) * R + r) * D + lane * DPL + 2 * e) = acc[q][r][e];
+    named_sync_compute();
+    constexpr int NT = ATT_TW * 32;
+    for (int idx = tid; idx < R * D; idx += NT) {
+      float t[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) t[q] = part[q * R * D + idx];
+#pragma unroll
+      for (int w = 1; w < NS; w <<= 1)
+#pragma unroll
+        for (int q = 0; q < NS; q += 2 * w) t[q] += t[q + w];
+      const int r = idx / D, dd = idx - r * D;
+      __stcg(a.part_o + ((long long)(g * R + r) * a.splits + s) * D + dd, t[0]);
+    }
+  }
+#else
   // ---- P.V
   {
     const int cw = lane % CPW, st = lane / CPW;
@@ -1640,6 +1799,7 @@ DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) 
     for (int p = 0; p < np; ++p) {
       const int pk0 = p * ATT_PIECE, cnt = min(ATT_PIECE, nk - pk0);
       mbar_wait(&full[slot], phase);
+      if (p == np - 1) ATT_STAMP(10);
       const uint8_t* src = ring + slot * PIECE_B;
       if (active && !no_pv) {
 #pragma unroll
@@ -1676,19 +1836,22 @@ DS_DEV void attn_tma_item(const AttnArgs& a, int item, int slots, int prefetch) 
       attn_store_part<D, R, HR>(a, g, s, accs, chunk, r0);
     }
   }
-  __threadfence();
-  named_sync_compute();  // every part_o store is fenced before the arrival count
+#endif
   ATT_STAMP(5);
+#if DS_ATT_STAMPS
+  if (tid == 0) ck1 = clock64();
+#endif
   // every piece is consumed: the ring is free to stage the merge
-  attn_finish_wide<D, R>(a, g, s, sc, stat, &is_last, ring, slots * PIECE_B, &merge_bar);
+  attn_finish_wide<D, R>(a, g, s, sc, stat, &is_last, ring, slots * PIECE_B, &merge_bar, st_ns);
   if (a.copy_lo && tid == 0) bulk_wait<0>();  // the ingest stores land before the grid completes
   ATT_STAMP(6);
 #if DS_ATT_STAMPS
   if (tid == 0) {
     const unsigned int launch = *(volatile unsigned int*)&g_att_launch;
     if (launch == 100 && (s == 0 || s == a.splits - 1 || is_last))
-      printf("ATT %d %d %d last=%d %llu %llu %llu %llu %llu %llu %llu\n", launch, g, s, (int)is_last, st_ns[0], st_ns[1],
-             st_ns[2], st_ns[3], st_ns[4], st_ns[5], st_ns[6]);
+      printf("ATT %d %d %d last=%d %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu pv_cycles=%lld\n", launch, g, s,
+             (int)is_last, st_ns[0], st_ns[1], st_ns[2], st_ns[3], st_ns[4], st_ns[5], st_ns[6], st_ns[7], st_ns[8],
+             st_ns[9], st_ns[10], ck1 - ck0);
     if (item == 0) atomicAdd(&g_att_launch, 1u);
   }
 #endif
@@ -1715,12 +1878,24 @@ __global__ void __launch_bounds__(ATT_TTHREADS, 2) attn_batch_tma_kernel(const _
   attn_tma_item<D, R>(ab.r[b], (int)blockIdx.x - ab.start[b], slots, prefetch);
 }
 
+// Ring slots: DS_ATT_SLOTS clamped to [2, ATT_SLOTS_MAX] and, with the
+// stream-per-warp P.V, to what holds the streams' partials (NS x R x D floats).
+template <int D, int R>
+static int att_slots(int want) {
+  int lo = 2;
+#if DS_ATT_PV_STREAMS
+  const int need = (32 * 32 / D) * R * D * 4, piece = ATT_PIECE * D * 2;
+  lo = (need + piece - 1) / piece > lo ? (need + piece - 1) / piece : lo;
+#endif
+  return want < lo ? lo : (want > ATT_SLOTS_MAX ? ATT_SLOTS_MAX : want);
+}
+
 template <int D, int R>
 static cudaError_t attn_tma_launch_t(const AttnArgs& a, int smem, cudaStream_t stream) {
   // ring slots and L2 prefetch (DS_ATT_SLOTS, DS_ATT_PREFETCH: experiments)
   static const int slots_env = env_int("DS_ATT_SLOTS", 12);
-  static const int prefetch = env_int("DS_ATT_PREFETCH", 0);  // bit 0 L2 prefetch; bits 1-3 timing experiments
-  const int slots = slots_env < 2 ? 2 : (slots_env > ATT_SLOTS_MAX ? ATT_SLOTS_MAX : slots_env);
+  static const int prefetch = env_int("DS_ATT_PREFETCH", 0);  // bit 0 L2 prefetch; bits 1-4 timing experiments
+  const int slots = att_slots<D, R>(slots_env);
   auto kern = attn_decode_tma_kernel<D, R>;
   static PerDevice attr;
   const int total = slots * ATT_PIECE * D * 2 + smem;
@@ -1769,7 +1944,7 @@ template <int D, int R>
 static cudaError_t attn_batch_launch_t(const AttnBatch& ab, int smem, cudaStream_t stream) {
   static const int slots_env = env_int("DS_ATT_SLOTS", 12);
   static const int prefetch = env_int("DS_ATT_PREFETCH", 0);
-  const int slots = slots_env < 2 ? 2 : (slots_env > ATT_SLOTS_MAX ? ATT_SLOTS_MAX : slots_env);
+  const int slots = att_slots<D, R>(slots_env);
   auto kern = attn_batch_tma_kernel<D, R>;
   static PerDevice attr;
   const int total = slots * ATT_PIECE * D * 2 + smem;
