@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, in
   uint8_t* ring = smem_dyn;
   bf16* xs = reinterpret_cast<bf16*>(smem_dyn + (size_t)slots * SLOT);
   __shared__ __align__(8) uint64_t full[16], empty[16];
+  __shared__ int tile_of[16];  // the tile whose first slice a slot holds (-1: no more tiles)
   __shared__ float red[GEMV_WARPS][GEMV_ROWS];
   __shared__ float ssq[GEMV_WARPS];
   const int tid = threadIdx.x;
@@ -491,19 +492,41 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, in
     if (tid == GEMV_THREADS) {
       int slot = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+      // the next tile's ticket is claimed as soon as the current tile's first
+      // slice is issued, so its round trip overlaps the slot waits
+      int t = a.tile_ctr ? (int)atomicAdd(a.tile_ctr, 1u) : (int)blockIdx.x;
+      for (;;) {
+        mbar_wait(&empty[slot], phase ^ 1);
+        if (t >= tiles) {
+          tile_of[slot] = -1;
+          mbar_arrive(&full[slot]);
+          break;
+        }
+        tile_of[slot] = t;
+        int nt = 0;
         for (int s = 0; s < ks; ++s) {
-          mbar_wait(&empty[slot], phase ^ 1);
+          if (s) mbar_wait(&empty[slot], phase ^ 1);
           mbar_expect_tx(&full[slot], SLOT);
 #pragma unroll
           for (int r = 0; r < GEMV_ROWS; ++r)
             bulk_g2s(ring + slot * SLOT + r * KS * 2, a.W + (long long)gemv_row(a, t, r) * a.ldw + (long long)s * KS,
                      KS * 2, &full[slot]);
+          if (s == 0) nt = a.tile_ctr ? (int)atomicAdd(a.tile_ctr, 1u) : t + (int)gridDim.x;
           if (++slot == slots) {
             slot = 0;
             phase ^= 1;
           }
         }
+        t = nt;
+      }
+      // every ticket of this CTA is claimed: the grid's last CTA re-zeroes the counters
+      if (a.tile_ctr) {
+        __threadfence();
+        if (atomicAdd(a.tile_ctr + 1, 1u) == gridDim.x - 1) {
+          a.tile_ctr[0] = 0u;
+          a.tile_ctr[1] = 0u;
+        }
+      }
     }
     return;
   }
@@ -512,13 +535,16 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) gemv_tma_kernel(GemvArgs a, in
   int slot = 0;
   uint32_t phase = 0;
   unsigned long long best = 0ull;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+  for (;;) {
+    mbar_wait(&full[slot], phase);  // the tile's first slice (or the end mark)
+    const int t = *reinterpret_cast<volatile int*>(&tile_of[slot]);
+    if (t < 0) break;
     const EpiPre pre = gemv_epi_pre(a, t);
     float2 s2[GEMV_ROWS];
 #pragma unroll
     for (int r = 0; r < GEMV_ROWS; ++r) s2[r] = make_float2(0.f, 0.f);
     for (int s = 0; s < ks; ++s) {
-      mbar_wait(&full[slot], phase);
+      if (s) mbar_wait(&full[slot], phase);
 #pragma unroll
       for (int cc = 0; cc < CPT; ++cc) {
         const int c = s * (KS / 8) + cc * GEMV_THREADS + tid;  // this thread's chunk
@@ -604,7 +630,10 @@ static int gemv_tma_launch_t(const GemvArgs& a, cudaStream_t stream, int ctas_pe
 }
 
 // Slice width and CTAs per SM (DS_GEMV_KS, DS_GEMV_TMA_CTAS: experiments).
-static int gemv_tma_launch(const GemvArgs& a, cudaStream_t stream) {
+static int gemv_tma_launch(const GemvArgs& a_in, cudaStream_t stream) {
+  static const bool claim = env_int("DS_GEMV_CLAIM", 1) != 0;  // 0: blockIdx-strided tiles (A/B)
+  GemvArgs a = a_in;
+  if (!claim) a.tile_ctr = nullptr;
   static const int ks_max = env_int("DS_GEMV_KS", 4096);
   static const int ctas = env_int("DS_GEMV_TMA_CTAS", 1) < 1 ? 1 : env_int("DS_GEMV_TMA_CTAS", 1);
   if (ks_max >= 4096 && a.K % 4096 == 0) return gemv_tma_launch_t<4096>(a, stream, ctas);
@@ -674,6 +703,7 @@ DS_HOST_DEV_INLINE GemvArgs gemv_row_view(const GemvArgs& a, const GemvBatch& bt
   if (v.out_bf16) v.out_bf16 += b * bt.out_stride;
   if (v.q_out) v.q_out += b * bt.q_stride;
   if (v.argmax) v.argmax += b;
+  v.tile_ctr = nullptr;  // rows launched one by one would share the counters
   v.pos = bt.pos[b];
   v.kv = bt.kv[b];
   return v;

@@ -107,6 +107,7 @@ struct Workspace {
   bf16* k0;           // [KVH][n][D] receiver's exact layer-0 K of the window
   bf16* v0;
   unsigned int* dec_count;  // [n_kv_heads] split-merge counters (zero between launches)
+  unsigned int* gemv_ctr;   // [kGemvCtrWords] per-launch GEMV tile tickets (zero between launches; after dec_count)
   float* ssq;               // [ceil(d/128)][n] per-column-tile sums of squares (RMSNorm folded into the GEMMs)
   long long rows;           // positions the workspace was carved for
   unsigned int* an_ctl;     // persistent anchor control block: done[kMaxLayers], bar[2], smid[kMaxAnchorCtas]
@@ -146,7 +147,8 @@ Workspace carve(const ds_dims& m, int n, void* base) {
   w.sel_tok = reinterpret_cast<int64_t*>(take(8ull * n));
   w.k0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
   w.v0 = reinterpret_cast<bf16*>(take(2ull * m.n_kv_heads * n * m.head_dim));
-  w.dec_count = reinterpret_cast<unsigned int*>(take(4ull * m.n_kv_heads));
+  w.dec_count = reinterpret_cast<unsigned int*>(take(4ull * (m.n_kv_heads + kGemvCtrWords)));
+  w.gemv_ctr = w.dec_count ? w.dec_count + m.n_kv_heads : nullptr;
   w.ssq = reinterpret_cast<float*>(take(4ull * ((m.d_model + 127) / 128) * n));
   w.an_ctl = reinterpret_cast<unsigned int*>(take(4ull * kAnchorCtlWords));
   w.an_stamps = reinterpret_cast<unsigned long long*>(take(8ull * (1 + 5 * kMaxLayers)));
@@ -356,6 +358,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   g.kv = layer_addr(*c.kv, l, d.head_dim);
   g.rope_cos = c.m->rope_cos;
   g.rope_sin = c.m->rope_sin;
+  g.tile_ctr = c.w.gemv_ctr + 0;  // one [ticket, done] pair per GEMV of the layer: consecutive launches never share
   if (!(skip & 1)) DS_TRY(gemv_launch(g, c.s), "anchor qkv");
   if (wait && cudaStreamWaitEvent(c.s, wait, 0) != cudaSuccess) return cuda_fail("wait");
   const KvAddr ka = g.kv;
@@ -383,6 +386,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   o.mode = EPI_RESID_F32;
   o.out_f32 = h_a;
   o.resid = h_a;
+  o.tile_ctr = c.w.gemv_ctr + 2;
   if (!(skip & 4)) DS_TRY(gemv_launch(o, c.s), "anchor o-proj");
   GemvArgs f{};
   f.W = static_cast<const bf16*>(W.w1);
@@ -393,6 +397,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   f.gain = W.g_mlp;
   f.mode = d.mlp_kind == DS_MLP_SWIGLU ? EPI_SWIGLU_BF16 : EPI_SILU_BF16;
   f.out_bf16 = c.w.u_a;
+  f.tile_ctr = c.w.gemv_ctr + 4;
   if (!(skip & 8)) DS_TRY(gemv_launch(f, c.s), "anchor w1");
   GemvArgs s2{};
   s2.W = static_cast<const bf16*>(W.w2);
@@ -403,6 +408,7 @@ int anchor_layer(Ctx& c, int l, int pos, float* h_a, const ds_kv_cache* sender =
   s2.mode = EPI_RESID_F32;
   s2.out_f32 = h_a;
   s2.resid = h_a;
+  s2.tile_ctr = c.w.gemv_ctr + 6;
   if (!(skip & 16)) DS_TRY(gemv_launch(s2, c.s), "anchor w2");
   return DS_OK;
 }
@@ -421,6 +427,7 @@ int lm_head(Ctx& c, const float* h_a, float* logits, int32_t* token, int64_t* to
   g.mode = EPI_STORE_F32;
   g.out_f32 = logits;
   g.argmax = c.w.argmax;
+  g.tile_ctr = c.w.gemv_ctr + 8;
   static const bool lm_tma = !(getenv("DS_LMHEAD_TMA") && getenv("DS_LMHEAD_TMA")[0] == '0');  // A/B switch
   DS_TRY(gemv_launch(g, c.s, /*staged=*/lm_tma), "lm head");
   if (token || token64) DS_TRY(argmax_finalize_launch(c.w.argmax, token, token64, c.s), "argmax");
@@ -471,7 +478,8 @@ int recompute_group(Ctx& c, const int64_t* tok, int P, int a, int b, const void*
 // The anchor position P through every layer, then logits + greedy token
 // (model.py:627-637).
 int reset_counters(Ctx& c) {
-  if (cudaMemsetAsync(c.w.dec_count, 0, 4ull * c.d.n_kv_heads, c.s) != cudaSuccess) return cuda_fail("memset");
+  if (cudaMemsetAsync(c.w.dec_count, 0, 4ull * (c.d.n_kv_heads + kGemvCtrWords), c.s) != cudaSuccess)
+    return cuda_fail("memset");
   return DS_OK;
 }
 
@@ -538,7 +546,7 @@ int anchor_persistent(Ctx& c, const int64_t* token_id, int P, const AnchorPlan* 
 
 int zero_anchor_ctl(Ctx& c, cudaStream_t s) {
   if (cudaMemsetAsync(c.w.an_ctl, 0, 4ull * kAnchorCtlWords, s) != cudaSuccess ||
-      cudaMemsetAsync(c.w.dec_count, 0, 4ull * c.d.n_kv_heads, s) != cudaSuccess)
+      cudaMemsetAsync(c.w.dec_count, 0, 4ull * (c.d.n_kv_heads + kGemvCtrWords), s) != cudaSuccess)
     return cuda_fail("memset");
   return DS_OK;
 }

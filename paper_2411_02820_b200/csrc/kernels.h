@@ -181,9 +181,15 @@ struct GemvArgs {
   const float* rope_cos;
   const float* rope_sin;
   unsigned long long* argmax;  // EPI_STORE_F32: packed (orderable value, ~index) max
+  // TMA kernel: [ticket, done] words, zero at launch (the last CTA re-zeroes
+  // them): tiles are claimed in order by whichever CTA is ready, instead of
+  // blockIdx-strided, so CTAs that start late (an SM still merging the
+  // attention before it) take fewer tiles.  nullptr: strided.
+  unsigned int* tile_ctr;
 };
 
 int gemv_launch(const GemvArgs& a, cudaStream_t stream, bool staged = true);
+constexpr int kGemvCtrWords = 16;  // workspace words for GemvArgs::tile_ctr pairs (5 launch roles used)
 int argmax_finalize_launch(const unsigned long long* packed, int32_t* token, int64_t* token64, cudaStream_t stream);
 
 // Batched GEMV: nb rows (requests) against one weight stream.  Row b's view is
