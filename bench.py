@@ -413,11 +413,13 @@ def batch_leg(P, _lib, cfg, A, B, rc, n, sizes, single_ttft_ms, single_anchor_ms
         # batched greedy decode: dsteps tokens per sequence after the prefills
         with torch.cuda.stream(stream):
             decode_greedy_batch(B, caches, res, 2, [n] * nb)  # warm-up
+            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            decode_greedy_batch(B, caches, res, dsteps + 1, [n] * nb)
-            e1.record(stream)
-        torch.cuda.synchronize()
+            with ClockSampler(dev.index or 0) as clk:
+                e0.record(stream)
+                decode_greedy_batch(B, caches, res, dsteps + 1, [n] * nb)
+                e1.record(stream)
+                torch.cuda.synchronize()
         dec = e0.elapsed_time(e1) / dsteps
         out[str(nb)] = {
             "ttft_ms": round(ttft, 3), "ms_per_request": round(ttft / nb, 3), "tok_s": nb * n / (ttft / 1e3),
@@ -425,6 +427,7 @@ def batch_leg(P, _lib, cfg, A, B, rc, n, sizes, single_ttft_ms, single_anchor_ms
             "anchor_ms": round(anc, 3), "anchor_ms_per_request": round(anc / nb, 3),
             "anchor_per_request_vs_single": round(anc / nb / single_anchor_ms, 3),
             "decode_ms_per_step": round(dec, 3), "decode_tok_s": nb * 1e3 / dec,
+            "decode_clocks": clk.summary(),
         }
         del prods, caches, res, ws, kvs, es
         torch.cuda.synchronize()
