@@ -19,7 +19,14 @@ from paper_2411_02820_b200 import _lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="4,8")
 ap.add_argument("--n", type=int, default=8192)
+ap.add_argument("--fragment-gb", type=float, default=0.0,
+                help="allocate this much in 256 MB blocks and free every other one first (allocator state probe)")
 args = ap.parse_args()
+keep = []
+if args.fragment_gb:
+    blocks = [torch.empty(256 << 20, dtype=torch.uint8, device="cuda") for _ in range(int(args.fragment_gb * 4))]
+    keep = blocks[::2]
+    del blocks
 n, k = args.n, 6
 cfg = P.ModelConfig(max_seq=max(n, 8192) + 64, base_seed=0, mlp_kind="ungated", **dict(bench.SHAPE, vocab_size=128256))
 L = cfg.n_layers
