@@ -70,16 +70,17 @@ DS_DEV float row_inv_rms(const GemmEpi& e, int row, bool row_ok) {
 // Epilogue warps: bring this thread's row of the tile's f32 residual into L2
 // while the tile's mainloop runs, so the residual epilogue's loads hit L2.
 template <int BN>
-DS_DEV void prefetch_resid(const GemmEpi& e, int row, int nb) {
+DS_DEV void prefetch_resid(const GemmEpi& e, int row, int col0) {
   if (e.mode != EPI_RESID_F32 || row >= e.M) return;
-  const int col0 = nb * BN, ncols = min(BN, e.N - col0);
+  const int ncols = min(BN, e.N - col0);
   if (ncols > 0) prefetch_l2(e.resid + (long long)row * e.ld_resid + col0, (uint32_t)ncols * 4);
 }
 
+// BN accumulator columns starting at output column col0 (tbase = their first
+// TMEM column); the residual epilogue's sum of squares is partial `part`.
 template <int BN>
-DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
+DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int col0, int part) {
   const bool row_ok = row < e.M;
-  const int col0 = nb * BN;
   const float inv = row_inv_rms(e, row, row_ok);
   if (e.mode == EPI_QKV_ROPE) {
     // j outer, heads inner: one row's cos/sin chunk (16-byte vector loads of
@@ -192,7 +193,7 @@ DS_DEV void epilogue_tile(const GemmEpi& e, uint32_t tbase, int row, int nb) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) r0[i] = r1[i];
     }
-    if (e.ssq_out && row_ok) e.ssq_out[nb * e.ld_ssq + row] = ss;
+    if (e.ssq_out && row_ok) e.ssq_out[part * e.ld_ssq + row] = ss;
     return;
   }
   if (e.mode == EPI_SWIGLU_BF16) {
@@ -358,11 +359,11 @@ __global__ void __maxnreg__(128)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, num_m, num_n, epi.group, mb, nb);
-      prefetch_resid<BN>(epi, mb * GEMM_BM + quarter * 32 + lane, nb);
+      prefetch_resid<BN>(epi, mb * GEMM_BM + quarter * 32 + lane, nb * BN);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      epilogue_tile<BN>(epi, tbase, mb * GEMM_BM + quarter * 32 + lane, nb);
+      epilogue_tile<BN>(epi, tbase, mb * GEMM_BM + quarter * 32 + lane, nb * BN, nb);
       tc_fence_before();
       if (epi.done) __threadfence();  // this warp's stores, before its completion count (release)
       __syncwarp();
@@ -472,6 +473,12 @@ DS_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// EW epilogue warps: 4 (one per TMEM lane quarter, all 256 columns of a row) or
+// 8 (two per lane quarter, 128 columns each: twice the epilogue's loads and
+// stores in flight, for the K = 4096 residual GEMM whose mainloop per tile is
+// short).  With 8 the residual epilogue writes one sum-of-squares partial per
+// 128 columns (gemm_col_tile), and 16 warps arrive per pair tile.
+template <int EW>
 __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                     GemmEpi epi) {
@@ -506,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], 2 * EW);
     }
     fence_mbar_init();
   }
@@ -592,18 +599,22 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(128)
       }
     }
   } else {
+    constexpr int EC = PAIR_BN * 4 / EW;      // columns per epilogue warp
     const int quarter = warp & 3;
+    const int part = (warp - 2) >> 2;         // column part of the tile (0 with 4 warps)
     const uint32_t leader_tempty0 = map_to_rank(&tempty[0], 0);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = pair; t < num_tiles; t += n_pairs) {
       int mb, nb;
       tile_coords(t, num_m, num_n, epi.group, mb, nb);
-      prefetch_resid<PAIR_BN>(epi, mb * 2 * GEMM_BM + (int)rank * GEMM_BM + quarter * 32 + lane, nb);
+      const int row = mb * 2 * GEMM_BM + (int)rank * GEMM_BM + quarter * 32 + lane;
+      const int col0 = nb * PAIR_BN + part * EC;
+      prefetch_resid<EC>(epi, row, col0);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * PAIR_BN;
-      epilogue_tile<PAIR_BN>(epi, tbase, mb * 2 * GEMM_BM + (int)rank * GEMM_BM + quarter * 32 + lane, nb);
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * PAIR_BN + part * EC;
+      epilogue_tile<EC>(epi, tbase, row, col0, nb * (PAIR_BN / EC) + part);
       tc_fence_before();
       if (epi.done) __threadfence();
       __syncwarp();
@@ -703,28 +714,43 @@ static bool use_pair(int M, int N) {
   return env && N >= 1024 && M > GEMM_BM && num_sms() >= 2;
 }
 
-int gemm_col_tile(int M, int N) { return use_pair(M, N) ? PAIR_BN : gemm_bn(N); }
+// Epilogue warps of the pair kernel (DS_GEMM_EPI_WARPS=8: A/B switch; 4 kept --
+// 8 measured no step gain, DESIGN 6.1).
+static int pair_epi_warps() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("DS_GEMM_EPI_WARPS");
+    v = (e && atoi(e) == 8) ? 8 : 4;
+  }
+  return v;
+}
+
+int gemm_col_tile(int M, int N) { return use_pair(M, N) ? PAIR_BN * 4 / pair_epi_warps() : gemm_bn(N); }
 
 // Arrivals on GemmEpi::done once the GEMM has finished: 4 epilogue warps per
-// 128-row CTA tile (the pair kernel: 2 CTA tiles per 256 x 256 pair tile).
+// 128-row CTA tile (the pair kernel: 2 CTA tiles per 256 x 256 pair tile, EW
+// epilogue warps each).
 unsigned int gemm_done_target(int M, int N) {
   if (use_pair(M, N))
-    return 8u * (unsigned)(((M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((N + PAIR_BN - 1) / PAIR_BN));
+    return 2u * (unsigned)pair_epi_warps() *
+           (unsigned)(((M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((N + PAIR_BN - 1) / PAIR_BN));
   const int bn = gemm_bn(N);
   return 4u * (unsigned)(((M + GEMM_BM - 1) / GEMM_BM) * ((N + bn - 1) / bn));
 }
 
 static cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, int K, const GemmEpi& epi,
                                    cudaStream_t stream, int max_ctas) {
-  static PerDevice smem_set;
-  if (cudaError_t e = ensure_smem_attr(gemm_tc2_kernel, Gemm2Smem::TOTAL, smem_set)) return e;
+  const int ew = pair_epi_warps();
+  auto kern = ew == 4 ? gemm_tc2_kernel<4> : gemm_tc2_kernel<8>;
+  static PerDevice smem_set4, smem_set8;
+  if (cudaError_t e = ensure_smem_attr(kern, Gemm2Smem::TOTAL, ew == 4 ? smem_set4 : smem_set8)) return e;
   const int tiles = ((epi.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((epi.N + PAIR_BN - 1) / PAIR_BN);
   int pairs = num_sms() / 2;
   if (max_ctas > 0 && pairs > max_ctas / 2) pairs = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
   if (pairs > tiles) pairs = tiles;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.blockDim = dim3(64 + 32 * ew);
   cfg.dynamicSmemBytes = Gemm2Smem::TOTAL;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -733,7 +759,7 @@ static cudaError_t launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   count_launch();
-  return cudaLaunchKernelEx(&cfg, gemm_tc2_kernel, ta, tb, K, epi);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, K, epi);
 }
 
 // A: [M][K] (lda), B: [N][K] (ldb) bf16 row-major.  Picks the kernel from the shape.
