@@ -229,3 +229,47 @@ def test_multiple_groups_and_layer0_group(pkg, tiny):
         assert torch.equal(d.k[l, :, :P_], prod.kv.k[l, :, :P_])
     for l in (0, 2):
         assert rel(_host(d.k)[l, :, :P_], ck[l, :, :P_]) < 2e-2
+
+
+def _random_case(i):
+    """Seeded random (n, recompute groups) on TINY: the reference's identity /
+    partial properties over configs its hypothesis test draws (test_model.py:298-314)."""
+    rng = np.random.default_rng(4242 + i)
+    n = int(rng.choice([2, 3, 64, 65, 127, 300, 511, 700, 1024]))
+    L = TINY[0]
+    groups = []
+    for _ in range(int(rng.integers(0, 3))):
+        a = int(rng.integers(0, L))
+        b = int(rng.integers(a, L))
+        groups.append((a, b))
+    return n, groups
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_random_configs_vs_oracle(pkg, tiny, case):
+    cfg, A, B, oA, oB = tiny
+    n, groups = _random_case(case)
+    toks = O.synthetic_tokens(300 + case, 1, n, 4096)[0]
+    rc = pkg.RecomputeConfig(groups)
+    prod = pkg.full_prefill(A, toks)
+    cons = pkg.partial_prefill(B, toks, rc, prod.kv, prod.e_map())
+    torch.cuda.synchronize()
+    P = n - 1
+    k, v, e, _ = O.full_prefill(oA, toks)
+    ck, cv, lc = O.partial_prefill(oB, toks, [tuple(g) for g in rc.groups], k, v, e)
+    dense = cons.kv.dense()
+    gk, gv = _host(dense.k), _host(dense.v)
+    recomputed = set(rc.layer_set())
+    for l in range(cfg.n_layers):
+        if l in recomputed:
+            if P >= 16:  # rel-L2 over a handful of values is dominated by bf16 rounding
+                assert rel(gk[l, :, :P], ck[l, :, :P]) < 2e-2, (l, n, groups)
+                assert rel(gv[l, :, :P], cv[l, :, :P]) < 2e-2, (l, n, groups)
+        else:
+            assert torch.equal(dense.k[l, :, :P], prod.kv.k[l, :, :P]), (l, n, groups)
+            assert torch.equal(dense.v[l, :, :P], prod.kv.v[l, :, :P]), (l, n, groups)
+    logits = _host(cons.logits)
+    assert np.isfinite(logits).all()
+    assert np.abs(logits - lc).max() < 0.1, (n, groups)
+    assert rel(logits, lc) < 3e-2, (n, groups)
+    assert cons.token == int(np.argmax(logits))
