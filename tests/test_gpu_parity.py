@@ -273,3 +273,33 @@ def test_random_configs_vs_oracle(pkg, tiny, case):
     assert np.abs(logits - lc).max() < 0.1, (n, groups)
     assert rel(logits, lc) < 3e-2, (n, groups)
     assert cons.token == int(np.argmax(logits))
+
+
+@pytest.fixture(scope="module")
+def mid(pkg):
+    return _pair(pkg, MID, [1], 0.5, 77)
+
+
+@pytest.mark.parametrize("n,groups", [(129, [(0, 0)]), (257, [(1, 1)]), (640, [(0, 1)]), (1000, [])])
+def test_mid_configs_vs_oracle(pkg, mid, n, groups):
+    """Head dim 128, GQA 4, CTA-pair GEMMs and the tcgen05 FA at ragged lengths."""
+    cfg, A, B, oA, oB = mid
+    toks = O.synthetic_tokens(50 + n, 1, n, 8192)[0]
+    prod = pkg.full_prefill(A, toks)
+    cons = pkg.partial_prefill(B, toks, pkg.RecomputeConfig(groups), prod.kv, prod.e_map())
+    torch.cuda.synchronize()
+    P = n - 1
+    k, v, e, _ = O.full_prefill(oA, toks)
+    ck, cv, lc = O.partial_prefill(oB, toks, groups, k, v, e)
+    dense = cons.kv.dense()
+    recomputed = set(pkg.RecomputeConfig(groups).layer_set())
+    for l in range(cfg.n_layers):
+        if l in recomputed:
+            assert rel(_host(dense.k[l, :, :P]), ck[l, :, :P]) < 2e-2, l
+            assert rel(_host(dense.v[l, :, :P]), cv[l, :, :P]) < 2e-2, l
+        else:
+            assert torch.equal(dense.k[l, :, :P], prod.kv.k[l, :, :P]), l
+            assert torch.equal(dense.v[l, :, :P], prod.kv.v[l, :, :P]), l
+    logits = _host(cons.logits)
+    assert np.abs(logits - lc).max() < 0.1 and rel(logits, lc) < 3e-2
+    assert cons.token == int(np.argmax(logits))
